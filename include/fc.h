@@ -1,0 +1,222 @@
+/*
+ * fc.h -- C ABI of the B200-native FlashCodec preprocessing hot path.
+ *
+ * The library (paper_2512_17574_b200/libfc.so) turns the sampled, decoded
+ * NV12 frames of one video request into Qwen2-VL patch tokens + grid_thw,
+ * with the request's GOPs partitioned over W GPUs (one process per GPU) and
+ * the token shards gathered to the encoder GPU.
+ *
+ * Citations: P:n = arXiv 2512.17574 line n; S:n = SPEC.md line n;
+ * readings R1..R12 are listed in DESIGN.md ("Readings of the paper").
+ *
+ * The calls follow the paper's FlashCodec API shape:
+ *   analyse_bitstream       ~ fc_plan        (metadata -> per-rank GOP plan)
+ *   add_decoding_request +
+ *   get_decoding_output     ~ fc_preprocess  (stream-async; result ready when
+ *                                             the caller synchronises the stream)
+ * and its deferred allocation rule: the caller allocates the token
+ * buffer only after planning, from the sizes fc_plan_rank reports.
+ *
+ * Conventions for every entry point:
+ *   - Status codes only; nothing throws across the ABI.  On error nothing has
+ *     been enqueued and no output has been written ("report, do not guess",
+ *     S:34; no partial effects).  fc_last_error() returns a
+ *     thread-local message describing the last failure on the calling thread.
+ *   - "device pointer" = memory of the CUDA device current on the calling
+ *     thread; "host pointer" = ordinary CPU memory.
+ *   - The library never frees caller memory.  Device buffers are borrowed
+ *     until the enqueued stream work completes.
+ *   - There is no CPU fallback: on a machine without a usable sm_100 device
+ *     fc_preprocess returns FC_ERR_CUDA.
+ */
+#ifndef FC_H_
+#define FC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FC_ABI_VERSION 1
+#define FC_TOKEN_COLS 1176 /* 3 channels * 2 (temporal patch) * 14 * 14 */
+
+typedef enum {
+  FC_OK = 0,
+  FC_ERR_INVALID_ARG = 1,     /* NULL / out-of-range argument, malformed meta */
+  FC_ERR_EMPTY_SELECTION = 2, /* sampling yields n == 0 or n > N (HF ValueError) */
+  FC_ERR_ASPECT_RATIO = 3,    /* max(H,W)/min(H,W) > 200 (smart_resize precondition) */
+  FC_ERR_UNSUPPORTED = 4,     /* odd dims, pitch % 16, unaligned surface, filter too wide */
+  FC_ERR_MISSING_SURFACE = 5, /* a surface this rank must read is NULL */
+  FC_ERR_RANK = 6,            /* rank outside [0, world_size) */
+  FC_ERR_OOM = 7,             /* host or device allocation failed */
+  FC_ERR_CUDA = 8,            /* CUDA launch/config error, or no sm_100 device */
+  FC_ERR_NCCL = 9             /* NCCL call failed */
+} fc_status;
+
+/* Exact rational frame rate (e.g. 30000/1001). */
+typedef struct {
+  int64_t num, den;
+} fc_rational;
+
+/* Video metadata M (Alg. 1 l.2; SPEC VideoMeta S:17-23).
+ * Frames are in presentation order, constant frame rate (reading R11).
+ * GOP g = frames [gop_start[g], gop_start[g+1]) (last GOP ends at num_frames);
+ * gop_start[0] == 0, strictly increasing, all < num_frames. */
+typedef struct {
+  int32_t width, height; /* luma size; both even and >= 2 */
+  int64_t num_frames;    /* N >= 1 */
+  fc_rational fps;       /* source frame rate, num > 0, den > 0 */
+  int64_t num_gops;      /* >= 1 */
+  const int64_t* gop_start; /* host pointer, num_gops entries; copied by fc_plan */
+} fc_video_meta;
+
+/* Frame-set policy for I.  R1: FPS_STRIDE = HF Qwen2VLVideoProcessor
+ * sample_frames (idx_i = floor(i*N/n)); LINSPACE = round(i*(N-1)/(n-1));
+ * EXPLICIT = caller-given strictly increasing list (odd counts are padded). */
+typedef enum { FC_SAMPLE_FPS_STRIDE = 0, FC_SAMPLE_LINSPACE = 1, FC_SAMPLE_EXPLICIT = 2 } fc_sampling;
+
+/* Model / preprocessing configuration (Qwen2-VL video processor defaults,
+ * filled by fc_model_cfg_default). */
+typedef struct {
+  int32_t patch_size;          /* 14 (only 14 supported) */
+  int32_t temporal_patch_size; /* T = 2 (only 2 supported) */
+  int32_t merge_size;          /* 2 (only 2 supported) */
+  int64_t min_pixels;          /* 128*28*28 = 100352 (R2) */
+  int64_t max_pixels;          /* 768*28*28 = 602112 (R2) */
+  double total_pixels;         /* 0 = off; qwen-vl-utils total budget (R2 variant) */
+  fc_sampling sampling;        /* FC_SAMPLE_FPS_STRIDE */
+  double sample_fps;           /* 2.0 */
+  int64_t num_frames;          /* 0 = use sample_fps; else HF num_frames rule */
+  int32_t min_frames;          /* 4 */
+  int32_t max_frames;          /* 768 */
+  const int64_t* explicit_indices; /* host pointer, FC_SAMPLE_EXPLICIT only; copied */
+  int64_t num_explicit;
+  int32_t resized_height;      /* 0 = smart_resize; else fixed, multiple of 28 (224) */
+  int32_t resized_width;
+  float image_mean[3];         /* OpenAI CLIP mean */
+  float image_std[3];          /* OpenAI CLIP std */
+  double rescale_factor;       /* 1/255 */
+  int32_t world_size;          /* W >= 1: GPUs the request is partitioned over */
+  int32_t encoder_rank;        /* rank that receives the gathered tokens (default 0) */
+} fc_model_cfg;
+
+void fc_model_cfg_default(fc_model_cfg* cfg);
+
+/* Opaque, immutable plan.  Safe to share between threads; per-device
+ * coefficient tables are created lazily inside it under a mutex.  Do not
+ * destroy a plan while work that uses it is in flight. */
+typedef struct fc_plan_s fc_plan_t;
+
+/* fc_plan -- the planning half of Alg. 1 (l.1-4): frame sampling
+ * (R1), smart_resize (R2), GOP->rank partition (get_GOPs_per_rank, R8) with
+ * method-b temporal alignment (make_align_to_temporal_patch_size),
+ * last-frame padding on the last rank, Pillow bicubic coefficient
+ * tables (R4) and the normalisation table (R5).  Host only; no CUDA call.
+ * *out receives a new plan (free with fc_plan_destroy) or NULL on error. */
+fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t** out);
+void fc_plan_destroy(fc_plan_t* plan);
+
+typedef struct {
+  int64_t grid_thw[3];      /* (ceil(n/2), H'/14, W'/14) */
+  int32_t resized_h, resized_w;
+  int64_t num_sampled;      /* n = |I| */
+  int64_t pad_frames;       /* (-n) mod 2, applied on the last non-empty rank */
+  int64_t token_rows;       /* grid_thw product */
+  int64_t token_cols;       /* 1176 */
+  double sampled_fps;       /* n / N * fps_src */
+  double second_per_grid;   /* T / sampled_fps (Qwen2.5-VL metadata) */
+  int32_t ranks_used;       /* non-empty ranks (empty ones are compacted to the end) */
+  int32_t world_size;
+  int32_t max_taps_h, max_taps_v; /* widest resize window per axis */
+} fc_plan_info;
+
+fc_status fc_plan_info_get(const fc_plan_t* plan, fc_plan_info* info);
+/* Copies the n sampled frame indices (ascending) into host array `out`. */
+fc_status fc_plan_sampled_indices(const fc_plan_t* plan, int64_t* out);
+
+/* Rank r's share (Alg. 1 GOPs_VEC).  Owned GOPs [gop_begin,
+ * gop_end); under method b a rank may additionally decode one frame of the
+ * next GOP (tail_gop, tail_frame; -1 if none).  Its sampled frames are
+ * sampled[sampled_begin .. sampled_begin+sampled_count) followed by pad_frames
+ * copies of the last one; its token rows are [row_begin, row_end) of the
+ * single-GPU result.  est_decode_frames = frames NVDEC would decode
+ * (keyframe .. last target per GOP) -- reported, decode is out of scope. */
+typedef struct {
+  int64_t gop_begin, gop_end, tail_gop, tail_frame;
+  int64_t sampled_begin, sampled_count, pad_frames;
+  int64_t row_begin, row_end;
+  int64_t est_decode_frames;
+} fc_rank_plan;
+
+fc_status fc_plan_rank(const fc_plan_t* plan, int32_t rank, fc_rank_plan* out);
+
+/* One decoded NV12 frame in device memory: luma plane y (height rows x
+ * pitch_y bytes) and interleaved U,V plane uv (height/2 rows x pitch_uv
+ * bytes).  Both pointers 16-byte aligned; both pitches multiples of 16 and
+ * >= width.  Surfaces must stay valid until the enqueued work completes. */
+typedef struct {
+  const uint8_t* y;
+  const uint8_t* uv;
+  int64_t pitch_y, pitch_uv;
+} fc_nv12_surface;
+
+/* fc_preprocess -- Alg. 1 l.21-22 (convert_AVframes_to_tensor_and_resize)
+ * for rank `rank`: one fused kernel launch on `stream` computing, for the
+ * rank's sampled frames, NV12 -> BT.601 RGB (R3) -> Pillow bicubic resize (R4)
+ * -> rescale + normalise (R5) -> temporal pad + 14x14x2 patchify in 2x2 merge
+ * order (R6).
+ *   surfaces:     host array of num_surfaces descriptors indexed by GLOBAL
+ *                 frame index (0..N-1); entries this rank does not read may
+ *                 have NULL pointers (FC_ERR_MISSING_SURFACE otherwise).
+ *   tokens:       device pointer, (row_end-row_begin) x 1176 fp32, contiguous.
+ *   grid_thw:     host out (3 values) or NULL.
+ *   stream:       cudaStream_t (0 = legacy default stream).
+ * Asynchronous: returns after enqueueing.  Validation happens before any
+ * launch.  A rank with no rows returns FC_OK without launching. */
+fc_status fc_preprocess(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
+                        int64_t num_surfaces, float* tokens, int64_t grid_thw[3], void* stream);
+
+/* Same, additionally dumping the integer intermediates for parity tests:
+ *   rgb_src:     device u8 [n_r, H, W, 3]  (BT.601 output) or NULL
+ *   rgb_resized: device u8 [n_r, H', W', 3] (resize output)  or NULL
+ * where n_r = the rank's frames including padding, in order. */
+fc_status fc_preprocess_debug(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
+                              int64_t num_surfaces, float* tokens, int64_t grid_thw[3], void* stream,
+                              uint8_t* rgb_src, uint8_t* rgb_resized);
+
+/* Throughput mode (config 5): `count` independent (plan, rank) jobs in ONE
+ * launch on `stream`.  surfaces[i] / num_surfaces[i] / tokens[i] as in
+ * fc_preprocess for job i.  All plans must share resized size and taps class. */
+fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* ranks, int32_t count,
+                              const fc_nv12_surface* const* surfaces, const int64_t* num_surfaces,
+                              float* const* tokens, void* stream);
+
+/* ---- exchange: gather row shards to the encoder rank ---- */
+
+/* NCCL communicator bootstrap without a torch type in the ABI: rank 0 calls
+ * fc_nccl_unique_id (128 bytes into `id`), the caller broadcasts the bytes
+ * over its process group, then every rank calls fc_nccl_comm_init with the
+ * CUDA device already current.  Returned comm is an ncclComm_t. */
+fc_status fc_nccl_unique_id(uint8_t id[128]);
+fc_status fc_nccl_comm_init(const uint8_t id[128], int32_t world_size, int32_t rank, void** comm);
+fc_status fc_nccl_comm_destroy(void* comm);
+
+/* fc_gather -- gatherv of every rank's contiguous row shard into the encoder
+ * rank's full token buffer (grouped ncclSend/ncclRecv, R9):
+ *   shard: device pointer, this rank's (row_end-row_begin) x 1176 fp32
+ *   full:  encoder rank: device pointer token_rows x 1176 fp32 (its own shard
+ *          is copied in with cudaMemcpyAsync unless shard already aliases
+ *          full + row_begin*1176); other ranks: ignored (may be NULL).
+ * Collective: every rank of the plan's world must call it.  Async on stream. */
+fc_status fc_gather(const fc_plan_t* plan, int32_t rank, void* comm, const float* shard, float* full,
+                    void* stream);
+
+const char* fc_status_string(fc_status s);
+const char* fc_last_error(void);
+int32_t fc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FC_H_ */

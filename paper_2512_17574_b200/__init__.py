@@ -1,0 +1,266 @@
+"""B200-native FlashCodec preprocessing hot path (arXiv 2512.17574).
+
+Thin Python binding over the C ABI in ``include/fc.h`` (``libfc.so``):
+argument marshalling only -- every step of the path runs in the library's
+sm_100a kernels / host planner.  PyTorch is used for device memory, streams
+and process groups.
+
+    meta = VideoMeta(1920, 1080, 1800, fps=(30, 1), gop_start=range(0, 1800, 30))
+    plan = Plan(meta, ModelCfg(world_size=1))            # fc_plan
+    surf = SurfaceTable.from_tensors(ys, uvs)            # fc_nv12_surface[]
+    tokens = preprocess(plan, 0, surf)                   # fc_preprocess
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+from fractions import Fraction
+from typing import Sequence
+
+from . import _native
+from ._native import FcError, FC_TOKEN_COLS, check, lib
+
+__all__ = ["VideoMeta", "ModelCfg", "Plan", "SurfaceTable", "preprocess", "preprocess_debug", "preprocess_batch",
+           "NcclComm", "gather", "FcError", "FC_TOKEN_COLS", "lib"]
+
+
+@dataclass
+class VideoMeta:
+    """Video metadata M (Alg. 1 l.2): luma size, frame count,
+    frame rate (rational), GOP start indices (presentation order)."""
+    width: int
+    height: int
+    num_frames: int
+    fps: tuple[int, int] | Fraction | int = (30, 1)
+    gop_start: Sequence[int] = (0,)
+
+    def to_c(self):
+        fr = Fraction(self.fps[0], self.fps[1]) if isinstance(self.fps, tuple) else Fraction(self.fps)
+        gs = list(self.gop_start)
+        arr = (ctypes.c_int64 * len(gs))(*gs)
+        m = _native.VideoMetaC(self.width, self.height, self.num_frames, _native.Rational(fr.numerator, fr.denominator),
+                               len(gs), ctypes.cast(arr, ctypes.POINTER(ctypes.c_int64)))
+        return m, arr
+
+
+@dataclass
+class ModelCfg:
+    """Preprocessing configuration; defaults = Qwen2-VL video processor (R1, R2, R5)."""
+    world_size: int = 1
+    encoder_rank: int = 0
+    sampling: str = "fps_stride"
+    sample_fps: float = 2.0
+    num_frames: int = 0
+    min_frames: int = 4
+    max_frames: int = 768
+    explicit_indices: Sequence[int] | None = None
+    min_pixels: int = 128 * 28 * 28
+    max_pixels: int = 768 * 28 * 28
+    total_pixels: float = 0.0
+    resized_height: int = 0
+    resized_width: int = 0
+    image_mean: tuple[float, float, float] | None = None
+    image_std: tuple[float, float, float] | None = None
+    rescale_factor: float | None = None
+
+    def to_c(self):
+        c = _native.ModelCfgC()
+        lib().fc_model_cfg_default(ctypes.byref(c))
+        c.world_size = self.world_size
+        c.encoder_rank = self.encoder_rank
+        c.sampling = _native.SAMPLING[self.sampling]
+        c.sample_fps = self.sample_fps
+        c.num_frames = self.num_frames
+        c.min_frames = self.min_frames
+        c.max_frames = self.max_frames
+        c.min_pixels = self.min_pixels
+        c.max_pixels = self.max_pixels
+        c.total_pixels = self.total_pixels
+        c.resized_height = self.resized_height
+        c.resized_width = self.resized_width
+        if self.image_mean is not None:
+            c.image_mean = (ctypes.c_float * 3)(*self.image_mean)
+        if self.image_std is not None:
+            c.image_std = (ctypes.c_float * 3)(*self.image_std)
+        if self.rescale_factor is not None:
+            c.rescale_factor = self.rescale_factor
+        keep = None
+        if self.explicit_indices is not None:
+            keep = (ctypes.c_int64 * len(self.explicit_indices))(*self.explicit_indices)
+            c.explicit_indices = ctypes.cast(keep, ctypes.POINTER(ctypes.c_int64))
+            c.num_explicit = len(self.explicit_indices)
+        return c, keep
+
+
+class Plan:
+    """fc_plan: sampling + smart_resize + GOP->rank partition + tables (host)."""
+
+    def __init__(self, meta: VideoMeta, cfg: ModelCfg | None = None):
+        self.meta = meta
+        self.cfg = cfg or ModelCfg()
+        m, _keep_m = meta.to_c()
+        c, _keep_c = self.cfg.to_c()
+        h = ctypes.c_void_p()
+        check(lib().fc_plan(ctypes.byref(m), ctypes.byref(c), ctypes.byref(h)), "fc_plan")
+        self._h = h
+        info = _native.PlanInfoC()
+        check(lib().fc_plan_info_get(h, ctypes.byref(info)), "fc_plan_info_get")
+        self.grid_thw = tuple(info.grid_thw)
+        self.resized = (info.resized_h, info.resized_w)
+        self.num_sampled = info.num_sampled
+        self.pad_frames = info.pad_frames
+        self.token_rows = info.token_rows
+        self.sampled_fps = info.sampled_fps
+        self.second_per_grid = info.second_per_grid
+        self.ranks_used = info.ranks_used
+        self.world_size = info.world_size
+        self.max_taps = (info.max_taps_h, info.max_taps_v)
+        idx = (ctypes.c_int64 * max(self.num_sampled, 1))()
+        check(lib().fc_plan_sampled_indices(h, idx), "fc_plan_sampled_indices")
+        self.sampled_indices = list(idx)[: self.num_sampled]
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def rank(self, r: int) -> dict:
+        rp = _native.RankPlanC()
+        check(lib().fc_plan_rank(self._h, r, ctypes.byref(rp)), "fc_plan_rank")
+        return {n: getattr(rp, n) for n, _ in rp._fields_}
+
+    def ranks(self) -> list[dict]:
+        return [self.rank(r) for r in range(self.world_size)]
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().fc_plan_destroy(h)
+            self._h = None
+
+
+class SurfaceTable:
+    """A host array of fc_nv12_surface descriptors, indexed by GLOBAL frame
+    index (entries a rank does not read may be empty).  Holds references to
+    the tensors so they stay alive."""
+
+    def __init__(self, num_frames: int):
+        self.arr = (_native.Nv12SurfaceC * max(num_frames, 1))()
+        self.n = num_frames
+        self._keep: dict[int, tuple] = {}
+
+    def set(self, frame: int, y, uv) -> None:
+        """y: uint8 [H, pitch_y] device tensor; uv: uint8 [H/2, pitch_uv]."""
+        self.arr[frame] = _native.Nv12SurfaceC(y.data_ptr(), uv.data_ptr(), y.stride(0), uv.stride(0))
+        self._keep[frame] = (y, uv)
+
+    @classmethod
+    def from_tensors(cls, frames: dict | Sequence, num_frames: int | None = None) -> "SurfaceTable":
+        items = frames.items() if isinstance(frames, dict) else enumerate(frames)
+        items = list(items)
+        n = num_frames if num_frames is not None else (max(k for k, _ in items) + 1 if items else 0)
+        t = cls(n)
+        for k, v in items:
+            if v is not None:
+                t.set(k, v[0], v[1])
+        return t
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _rank_rows(plan: Plan, rank: int) -> int:
+    rp = plan.rank(rank)
+    return rp["row_end"] - rp["row_begin"]
+
+
+def preprocess(plan: Plan, rank: int, surfaces: SurfaceTable, out=None, stream=None):
+    """fc_preprocess: enqueue the fused kernel for `rank` on `stream`; returns
+    the (row_end-row_begin) x 1176 fp32 token shard (allocated after planning
+    if `out` is None)."""
+    import torch
+    rows = _rank_rows(plan, rank)
+    if out is None:
+        out = torch.empty((rows, FC_TOKEN_COLS), dtype=torch.float32, device="cuda")
+    grid = (ctypes.c_int64 * 3)()
+    check(lib().fc_preprocess(plan.handle, rank, surfaces.arr, surfaces.n, ctypes.c_void_p(out.data_ptr()), grid,
+                              _stream_ptr(stream)), "fc_preprocess")
+    return out
+
+
+def preprocess_debug(plan: Plan, rank: int, surfaces: SurfaceTable, stream=None):
+    """fc_preprocess_debug: tokens plus the integer intermediates
+    (BT.601 RGB [n_r,H,W,3] and resized RGB [n_r,H',W',3], u8)."""
+    import torch
+    rp = plan.rank(rank)
+    rows = rp["row_end"] - rp["row_begin"]
+    nr = rp["sampled_count"] + rp["pad_frames"]
+    h2, w2 = plan.resized
+    tokens = torch.empty((rows, FC_TOKEN_COLS), dtype=torch.float32, device="cuda")
+    src = torch.empty((nr, plan.meta.height, plan.meta.width, 3), dtype=torch.uint8, device="cuda")
+    rs = torch.empty((nr, h2, w2, 3), dtype=torch.uint8, device="cuda")
+    grid = (ctypes.c_int64 * 3)()
+    check(lib().fc_preprocess_debug(plan.handle, rank, surfaces.arr, surfaces.n, ctypes.c_void_p(tokens.data_ptr()),
+                                    grid, _stream_ptr(stream), ctypes.c_void_p(src.data_ptr()),
+                                    ctypes.c_void_p(rs.data_ptr())), "fc_preprocess_debug")
+    return tokens, src, rs
+
+
+def preprocess_batch(jobs: Sequence[tuple[Plan, int, SurfaceTable]], outs=None, stream=None):
+    """fc_preprocess_batch: several independent (plan, rank) jobs on one stream."""
+    import torch
+    n = len(jobs)
+    if outs is None:
+        outs = [torch.empty((_rank_rows(p, r), FC_TOKEN_COLS), dtype=torch.float32, device="cuda")
+                for p, r, _ in jobs]
+    plans = (ctypes.c_void_p * n)(*[p.handle.value for p, _, _ in jobs])
+    ranks = (ctypes.c_int32 * n)(*[r for _, r, _ in jobs])
+    surfs = (ctypes.POINTER(_native.Nv12SurfaceC) * n)(*[ctypes.cast(s.arr, ctypes.POINTER(_native.Nv12SurfaceC))
+                                                         for _, _, s in jobs])
+    nsurf = (ctypes.c_int64 * n)(*[s.n for _, _, s in jobs])
+    toks = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs])
+    check(lib().fc_preprocess_batch(plans, ranks, n, surfs, nsurf, toks, _stream_ptr(stream)), "fc_preprocess_batch")
+    return outs
+
+
+class NcclComm:
+    """An NCCL communicator owned by libfc (fc_nccl_comm_init), bootstrapped
+    over an existing torch.distributed process group (the 128-byte unique id
+    is broadcast with it)."""
+
+    def __init__(self, rank: int, world_size: int, group=None):
+        import torch
+        import torch.distributed as dist
+        idbuf = (ctypes.c_uint8 * 128)()
+        if rank == 0:
+            check(lib().fc_nccl_unique_id(idbuf), "fc_nccl_unique_id")
+        t = torch.tensor(list(bytes(idbuf)), dtype=torch.uint8)
+        backend = dist.get_backend(group)
+        if backend == "nccl":
+            t = t.cuda()
+        dist.broadcast(t, src=0, group=group)
+        idbuf = (ctypes.c_uint8 * 128)(*t.cpu().tolist())
+        h = ctypes.c_void_p()
+        check(lib().fc_nccl_comm_init(idbuf, world_size, rank, ctypes.byref(h)), "fc_nccl_comm_init")
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            check(lib().fc_nccl_comm_destroy(self.handle), "fc_nccl_comm_destroy")
+            self.handle = None
+
+
+def gather(plan: Plan, rank: int, comm: NcclComm | None, shard, full=None, stream=None):
+    """fc_gather: gatherv of the row shards into the encoder rank's full
+    token buffer (returned on the encoder rank, None elsewhere)."""
+    import torch
+    enc = plan.cfg.encoder_rank
+    if rank == enc and full is None:
+        full = torch.empty((plan.token_rows, FC_TOKEN_COLS), dtype=torch.float32, device="cuda")
+    check(lib().fc_gather(plan.handle, rank, comm.handle if comm else None,
+                          ctypes.c_void_p(shard.data_ptr()) if shard is not None else None,
+                          ctypes.c_void_p(full.data_ptr()) if full is not None else None,
+                          _stream_ptr(stream)), "fc_gather")
+    return full if rank == enc else None

@@ -1,0 +1,121 @@
+"""ctypes declaration of the C ABI in include/fc.h (argument marshalling only).
+
+Loading fails loudly when libfc.so is missing: there is no CPU or Python
+fallback for any step of the path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfc.so")
+
+FC_TOKEN_COLS = 1176
+STATUS = {0: "FC_OK", 1: "FC_ERR_INVALID_ARG", 2: "FC_ERR_EMPTY_SELECTION", 3: "FC_ERR_ASPECT_RATIO",
+          4: "FC_ERR_UNSUPPORTED", 5: "FC_ERR_MISSING_SURFACE", 6: "FC_ERR_RANK", 7: "FC_ERR_OOM",
+          8: "FC_ERR_CUDA", 9: "FC_ERR_NCCL"}
+SAMPLING = {"fps_stride": 0, "linspace": 1, "explicit": 2}
+
+
+class FcError(RuntimeError):
+    def __init__(self, status: int, where: str, detail: str):
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+        super().__init__(f"{where}: {self.name}: {detail}")
+
+
+class Rational(ctypes.Structure):
+    _fields_ = [("num", ctypes.c_int64), ("den", ctypes.c_int64)]
+
+
+class VideoMetaC(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("height", ctypes.c_int32), ("num_frames", ctypes.c_int64),
+                ("fps", Rational), ("num_gops", ctypes.c_int64), ("gop_start", ctypes.POINTER(ctypes.c_int64))]
+
+
+class ModelCfgC(ctypes.Structure):
+    _fields_ = [("patch_size", ctypes.c_int32), ("temporal_patch_size", ctypes.c_int32),
+                ("merge_size", ctypes.c_int32), ("min_pixels", ctypes.c_int64), ("max_pixels", ctypes.c_int64),
+                ("total_pixels", ctypes.c_double), ("sampling", ctypes.c_int), ("sample_fps", ctypes.c_double),
+                ("num_frames", ctypes.c_int64), ("min_frames", ctypes.c_int32), ("max_frames", ctypes.c_int32),
+                ("explicit_indices", ctypes.POINTER(ctypes.c_int64)), ("num_explicit", ctypes.c_int64),
+                ("resized_height", ctypes.c_int32), ("resized_width", ctypes.c_int32),
+                ("image_mean", ctypes.c_float * 3), ("image_std", ctypes.c_float * 3),
+                ("rescale_factor", ctypes.c_double), ("world_size", ctypes.c_int32),
+                ("encoder_rank", ctypes.c_int32)]
+
+
+class PlanInfoC(ctypes.Structure):
+    _fields_ = [("grid_thw", ctypes.c_int64 * 3), ("resized_h", ctypes.c_int32), ("resized_w", ctypes.c_int32),
+                ("num_sampled", ctypes.c_int64), ("pad_frames", ctypes.c_int64), ("token_rows", ctypes.c_int64),
+                ("token_cols", ctypes.c_int64), ("sampled_fps", ctypes.c_double),
+                ("second_per_grid", ctypes.c_double), ("ranks_used", ctypes.c_int32),
+                ("world_size", ctypes.c_int32), ("max_taps_h", ctypes.c_int32), ("max_taps_v", ctypes.c_int32)]
+
+
+class RankPlanC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("gop_begin", "gop_end", "tail_gop", "tail_frame", "sampled_begin",
+                                              "sampled_count", "pad_frames", "row_begin", "row_end",
+                                              "est_decode_frames")]
+
+
+class Nv12SurfaceC(ctypes.Structure):
+    _fields_ = [("y", ctypes.c_void_p), ("uv", ctypes.c_void_p), ("pitch_y", ctypes.c_int64),
+                ("pitch_uv", ctypes.c_int64)]
+
+
+EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_get", "fc_plan_sampled_indices",
+           "fc_plan_rank", "fc_preprocess", "fc_preprocess_debug", "fc_preprocess_batch", "fc_nccl_unique_id",
+           "fc_nccl_comm_init", "fc_nccl_comm_destroy", "fc_gather", "fc_status_string", "fc_last_error",
+           "fc_abi_version"]
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                          f"g.build()'` (there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    L.fc_model_cfg_default.argtypes = [ctypes.POINTER(ModelCfgC)]
+    L.fc_model_cfg_default.restype = None
+    L.fc_plan.argtypes = [ctypes.POINTER(VideoMetaC), ctypes.POINTER(ModelCfgC), ctypes.POINTER(vp)]
+    L.fc_plan_destroy.argtypes = [vp]
+    L.fc_plan_destroy.restype = None
+    L.fc_plan_info_get.argtypes = [vp, ctypes.POINTER(PlanInfoC)]
+    L.fc_plan_sampled_indices.argtypes = [vp, ctypes.POINTER(ctypes.c_int64)]
+    L.fc_plan_rank.argtypes = [vp, i32, ctypes.POINTER(RankPlanC)]
+    L.fc_preprocess.argtypes = [vp, i32, ctypes.POINTER(Nv12SurfaceC), i64, vp, ctypes.POINTER(ctypes.c_int64), vp]
+    L.fc_preprocess_debug.argtypes = [vp, i32, ctypes.POINTER(Nv12SurfaceC), i64, vp, ctypes.POINTER(ctypes.c_int64),
+                                      vp, vp, vp]
+    L.fc_preprocess_batch.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_int32), i32,
+                                      ctypes.POINTER(ctypes.POINTER(Nv12SurfaceC)), ctypes.POINTER(ctypes.c_int64),
+                                      ctypes.POINTER(vp), vp]
+    L.fc_nccl_unique_id.argtypes = [ctypes.POINTER(ctypes.c_uint8)]
+    L.fc_nccl_comm_init.argtypes = [ctypes.POINTER(ctypes.c_uint8), i32, i32, ctypes.POINTER(vp)]
+    L.fc_nccl_comm_destroy.argtypes = [vp]
+    L.fc_gather.argtypes = [vp, i32, vp, vp, vp, vp]
+    L.fc_status_string.argtypes = [ctypes.c_int]
+    L.fc_status_string.restype = ctypes.c_char_p
+    L.fc_last_error.argtypes = []
+    L.fc_last_error.restype = ctypes.c_char_p
+    L.fc_abi_version.argtypes = []
+    L.fc_abi_version.restype = ctypes.c_int32
+    for name in EXPORTS:
+        fn = getattr(L, name)
+        if name not in ("fc_model_cfg_default", "fc_plan_destroy", "fc_status_string", "fc_last_error",
+                        "fc_abi_version"):
+            fn.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def check(status: int, where: str) -> None:
+    if status != 0:
+        detail = lib().fc_last_error().decode(errors="replace")
+        raise FcError(status, where, detail)

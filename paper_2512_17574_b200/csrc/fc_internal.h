@@ -1,0 +1,74 @@
+// fc_internal.h -- private types shared by the host planner, the runtime and
+// the CUDA launcher of libfc.so.  Not part of the ABI (include/fc.h is).
+#pragma once
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "fc.h"
+
+namespace fc {
+
+constexpr int kPatch = 14;
+constexpr int kTps = 2;
+constexpr int kMerge = 2;
+constexpr int kBlock = kPatch * kMerge;  // 28: merge-block side in pixels
+constexpr int kCols = FC_TOKEN_COLS;     // 1176
+constexpr int kPrecisionBits = 22;       // Pillow 8bpc fixed point (R4)
+constexpr int kMaxWords = 16;            // <= 64 taps per output on either axis
+
+// One resize axis in the form the kernel consumes (R4):
+// per output index o: first source index xmin[o], tap count cnt[o], and the
+// 22-bit integer weights split into three byte planes packed 4 taps per word
+// (plane 0/1 unsigned bytes, plane 2 signed byte), so that
+//   sum_k px[k]*iw[k] = dp4a(px,P0) + 256*dp4a(px,P1) + 65536*dp4a(px,P2).
+struct AxisTable {
+  int in = 0, out = 0;
+  int ksize = 0;   // Pillow ksize
+  int max_cnt = 0; // widest window actually used
+  int words = 0;   // ceil(max_cnt/4)
+  std::vector<int32_t> xmin, cnt;
+  std::vector<int32_t> iw;       // out x ksize integer weights
+  std::vector<uint32_t> planes;  // out x 3 x words
+};
+
+struct RankPlan {
+  fc_rank_plan p{};
+};
+
+struct DeviceTables {
+  int32_t* hx = nullptr;
+  int32_t* hcnt = nullptr;
+  uint32_t* hw = nullptr;
+  int32_t* vx = nullptr;
+  int32_t* vcnt = nullptr;
+  uint32_t* vw = nullptr;
+  float* lut = nullptr;
+};
+
+}  // namespace fc
+
+struct fc_plan_s {
+  fc_video_meta meta{};
+  std::vector<int64_t> gop_start;
+  fc_model_cfg cfg{};
+  std::vector<int64_t> sampled;  // global frame indices, ascending
+  int64_t n = 0;
+  int32_t h2 = 0, w2 = 0;
+  int64_t gt = 0, gh = 0, gw = 0;
+  double sampled_fps = 0, second_per_grid = 0;
+  int32_t world = 1, ranks_used = 0;
+  std::vector<fc::RankPlan> ranks;
+  fc::AxisTable th, tv;      // horizontal (W -> W'), vertical (H -> H')
+  std::vector<float> lut;    // 3 x 256 (R5)
+  std::mutex mu;             // guards dev
+  std::unordered_map<int, fc::DeviceTables> dev;
+};
+
+namespace fc {
+void set_error(const std::string& msg);
+fc_status fail(fc_status s, const std::string& msg);
+fc_status build_axis(int in, int out, AxisTable* t);
+}  // namespace fc

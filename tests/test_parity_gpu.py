@@ -1,0 +1,173 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle.
+
+Bar (BASELINE.json north star):
+  * sampling indices, grid_thw, the BT.601 RGB intermediate and the resized
+    RGB intermediate: bit-exact;
+  * normalised fp32 tokens: |gpu - oracle| <= 1e-5 * max(|oracle|, 1) per
+    element (reading R7; bit-exact expected, and the count is reported).
+Small cases are compared element by element on the whole output; the full
+BASELINE configs run in the bench's launch configuration (one launch per
+rank, all frames) and are compared on sampled temporal pairs.
+"""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def tol_check(got, ref, what=""):
+    assert got.shape == ref.shape, (what, got.shape, ref.shape)
+    tol = 1e-5 * np.maximum(np.abs(ref), 1.0)
+    bad = np.abs(got - ref) > tol
+    nbad = int(bad.sum())
+    if nbad:
+        i = np.argwhere(bad)[0]
+        raise AssertionError(f"{what}: {nbad} elements out of tolerance, first at {tuple(i)}: "
+                             f"gpu {got[tuple(i)]!r} oracle {ref[tuple(i)]!r}")
+    return int((got.view(np.uint32) == ref.view(np.uint32)).sum())
+
+
+def make_plan(fc, W, H, N, gops, world=1, **cfg):
+    meta = fc.VideoMeta(W, H, N, (30, 1), gops)
+    return fc.Plan(meta, fc.ModelCfg(world_size=world, **cfg))
+
+
+def run_case(fc, oracle, cuda, W, H, N, gops, kind="natural", seed=7, world=1, check_rgb=True, **cfg):
+    plan = make_plan(fc, W, H, N, gops, world, **cfg)
+    idx = plan.sampled_indices
+    pitch = synth.pitch_for(W)
+    host = {i: synth.frame_nv12(W, H, i, kind, seed, pitch) for i in idx}
+    dev = synth.to_device(host)
+    surf = fc.SurfaceTable.from_tensors(dev, N)
+    h2, w2 = plan.resized
+    ref_tok, ref_src, ref_rs = oracle.preprocess([host[i] for i in idx], W, H, w2, h2, want_rgb=True)
+    parts = []
+    for r in range(world):
+        rp = plan.rank(r)
+        if rp["row_end"] == rp["row_begin"]:
+            continue
+        tok, src, rs = fc.preprocess_debug(plan, r, surf)
+        cuda.cuda.synchronize()
+        parts.append(tok.cpu().numpy())
+        if check_rgb:
+            fr = list(range(rp["sampled_begin"], rp["sampled_begin"] + rp["sampled_count"]))
+            fr += [fr[-1]] * rp["pad_frames"]
+            np.testing.assert_array_equal(src.cpu().numpy(), ref_src[fr], err_msg=f"rgb_src rank {r}")
+            np.testing.assert_array_equal(rs.cpu().numpy(), ref_rs[fr], err_msg=f"rgb_resized rank {r}")
+    got = np.concatenate(parts, axis=0)
+    exact = tol_check(got, ref_tok, f"{W}x{H}->{w2}x{h2} {kind} W={world}")
+    return plan, exact, got.size
+
+
+@pytest.mark.parametrize("kind", ["natural", "uniform", "edges"])
+def test_c1_shape_all_kinds(fc, oracle, cuda, kind):
+    wl = synth.CONFIGS["c1"]
+    plan, exact, size = run_case(fc, oracle, cuda, wl.width, wl.height, wl.num_frames, wl.gop_start, kind,
+                                 seed=wl.seed, sample_fps=2.0)
+    assert plan.grid_thw == (4, 20, 28)
+    assert exact == size  # bit-exact expected
+
+
+@pytest.mark.parametrize("shape", [
+    (64, 48, 28, 56),      # tiny downscale to one merge block row
+    (200, 120, 56, 84),    # ragged: 3 merge-block columns (partial strip)
+    (96, 40, 56, 140),     # upscale horizontally + vertically
+    (224, 224, 224, 224),  # identity (no resample pass in Pillow)
+    (854, 480, 476, 840),  # c5 tie case, 15 merge-block columns
+    (1280, 720, 560, 1008),
+    (1920, 1080, 224, 224),  # paper eval setting: 8.6x downscale, 37-tap filter
+    (30, 18, 56, 56),      # odd-size-ish small frame, heavy upscale
+])
+@pytest.mark.parametrize("kind", ["natural", "uniform"])
+def test_shapes(fc, oracle, cuda, shape, kind):
+    W, H, h2, w2 = shape
+    N = 8
+    plan, exact, size = run_case(fc, oracle, cuda, W, H, N, [0], kind, seed=11,
+                                 sampling="explicit", explicit_indices=list(range(0, 8, 2)),
+                                 resized_height=h2, resized_width=w2)
+    assert plan.resized == (h2, w2)
+
+
+def test_odd_count_pads_last_frame(fc, oracle, cuda):
+    # 5 explicit frames -> padded to 6 with the last one
+    plan, exact, size = run_case(fc, oracle, cuda, 320, 240, 40, [0, 10, 20, 30], "edges", seed=3,
+                                 sampling="explicit", explicit_indices=[1, 9, 17, 25, 33])
+    assert plan.pad_frames == 1 and plan.grid_thw[0] == 3
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_virtual_ranks_concat_equals_single(fc, oracle, cuda, world):
+    """O12 / P:339: the concatenated rank shards equal the single-GPU result
+    (all ranks run on one device; no NCCL)."""
+    plan, exact, size = run_case(fc, oracle, cuda, 320, 240, 300, list(range(0, 300, 30)), "natural",
+                                 seed=5, world=world, sample_fps=2.0)
+    assert exact == size
+
+
+def test_virtual_ranks_odd_explicit(fc, oracle, cuda):
+    # method-b tails and last-rank padding together
+    plan, exact, size = run_case(fc, oracle, cuda, 256, 144, 100, list(range(0, 100, 10)), "uniform",
+                                 seed=9, world=4, sampling="explicit",
+                                 explicit_indices=[0, 3, 12, 13, 14, 25, 41, 42, 57, 70, 81])
+    rps = plan.ranks()
+    assert rps[-1]["pad_frames"] + sum(r["pad_frames"] for r in rps[:-1]) == 1
+
+
+# ------------------------------------------------------------ full configs
+def _full_config(fc, oracle, cuda, name, pairs_to_check, kind="natural", clip=0):
+    import torch
+    wl = synth.CONFIGS[name]
+    plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
+                   fc.ModelCfg(world_size=1, sample_fps=wl.sample_fps))
+    idx = plan.sampled_indices
+    host = synth.frames_nv12(wl, idx, kind, clip=clip)
+    dev = synth.to_device(host)
+    surf = fc.SurfaceTable.from_tensors(dev, wl.num_frames)
+    tokens = fc.preprocess(plan, 0, surf)  # the bench's launch configuration
+    torch.cuda.synchronize()
+    gt, gh, gw = plan.grid_thw
+    rpp = gh * gw
+    h2, w2 = plan.resized
+    exact_total = size_total = 0
+    for t in pairs_to_check(gt):
+        fr = [idx[min(2 * t + k, len(idx) - 1)] for k in (0, 1)]
+        ref = oracle.preprocess([host[f] for f in fr], wl.width, wl.height, w2, h2)
+        got = tokens[t * rpp:(t + 1) * rpp].cpu().numpy()
+        exact_total += tol_check(got, ref, f"{name} pair {t}")
+        size_total += got.size
+    return plan, exact_total, size_total
+
+
+def _sample_pairs(gt):
+    return sorted({0, 1, gt // 2, gt - 1})
+
+
+def test_full_c1(fc, oracle, cuda):
+    plan, e, s = _full_config(fc, oracle, cuda, "c1", lambda gt: range(gt))
+    assert plan.grid_thw == (4, 20, 28) and e == s
+
+
+def test_full_c2_sampled_pairs(fc, oracle, cuda):
+    plan, e, s = _full_config(fc, oracle, cuda, "c2", _sample_pairs)
+    assert plan.grid_thw == (60, 40, 72)
+    assert e == s
+
+
+def test_full_c4_sampled_pairs(fc, oracle, cuda):
+    plan, e, s = _full_config(fc, oracle, cuda, "c4", _sample_pairs, kind="edges")
+    assert plan.grid_thw == (30, 40, 72)
+    assert e == s
+
+
+def test_full_c3_sampled_pairs(fc, oracle, cuda):
+    plan, e, s = _full_config(fc, oracle, cuda, "c3", _sample_pairs)
+    assert plan.grid_thw == (300, 40, 72)
+    assert e == s
+
+
+def test_full_c5_clip(fc, oracle, cuda):
+    plan, e, s = _full_config(fc, oracle, cuda, "c5", lambda gt: range(gt), kind="uniform", clip=17)
+    assert plan.grid_thw == (10, 34, 60)
+    assert e == s
