@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libfc.so")
 SOURCES = ["fc_plan.cpp", "fc_kernels.cu", "fc_gather.cpp"]
-HEADERS = ["fc_internal.h"]
+HEADERS = ["fc_internal.h", "fc_device.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -25,14 +25,17 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
+#include "fc_device.cuh"
 #include "fc_internal.h"
 
 namespace fc {
 
-constexpr int kChunkRows = 16;             // source rows converted per stage-A step
+constexpr int kChunkRows = 16;             // source rows per stage-A chunk
 constexpr int kMaxFramesPerLaunch = 1200;  // frame descriptors passed by value
 
 struct FrameDesc {
@@ -45,8 +48,9 @@ struct Params {
   int W, H, W2, H2;
   int gh2, gw2;       // merge blocks per column / row
   int nstrips;
-  int SWP;            // bytes per source row in the stage-A chunk buffer
+  int SWP;            // bytes per source row in the chunk buffers
   int TR, TRW, TRS;   // ring rows, ring words, column stride in words
+  int nchunks;        // ceil(H / 16)
   const int32_t* hx;
   const uint32_t* hw;
   const int32_t* vx;
@@ -61,141 +65,132 @@ struct Params {
   FrameDesc fr[kMaxFramesPerLaunch];
 };
 
-__device__ __forceinline__ uint32_t dp4a_uu(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-// a: four unsigned pixel bytes; b: four signed weight bytes
-__device__ __forceinline__ uint32_t dp4a_us(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-
-// Pillow clip8 of the 22-bit fixed-point sum (R4): v>=2^30 -> 255, v<=0 -> 0.
-__device__ __forceinline__ uint32_t clip8(uint32_t s) {
-  int q = static_cast<int>(s) >> 22;
-  return static_cast<uint32_t>(min(max(q, 0), 255));
-}
-
-template <int NW>
-__device__ __forceinline__ uint32_t fir_bytes(const uint32_t (&d)[NW], const uint32_t (&w0)[NW],
-                                              const uint32_t (&w1)[NW], const uint32_t (&w2)[NW]) {
-  uint32_t s0 = 1u << 21, s1 = 0, s2 = 0;  // 2^21: Pillow's rounding half
+// Issue the TMA bulk copies of one 16-row chunk (both frames, Y rows + the
+// 8 UV rows) into raw buffer `buf`.  Executed by warp 0; lane 0 arms the
+// mbarrier with the chunk's byte count first.
+__device__ __forceinline__ void issue_chunk(const Params& p, const FrameDesc* frs, int SX0, int k, uint8_t* raw,
+                                            uint64_t* bar, int lane) {
+  const int r0 = k * kChunkRows;
+  const int rows_y = min(kChunkRows, p.H - r0);
+  const int rows_uv = min(kChunkRows / 2, (p.H >> 1) - (r0 >> 1));
+  if (lane == 0) {
+    uint32_t bytes = 0;
 #pragma unroll
-  for (int i = 0; i < NW; ++i) {
-    s0 = dp4a_uu(d[i], w0[i], s0);
-    s1 = dp4a_uu(d[i], w1[i], s1);
-    s2 = dp4a_us(d[i], w2[i], s2);
+    for (int f = 0; f < 2; ++f) {
+      const int fy = max(min(p.SWP, frs[f].py - SX0), 0), fuv = max(min(p.SWP, frs[f].puv - SX0), 0);
+      bytes += rows_y * fy + rows_uv * fuv;
+    }
+    mbar_arrive_expect_tx(bar, bytes);
   }
-  return clip8(s0 + (s1 << 8) + (s2 << 16));  // modular int32 == exact (R4 headroom)
-}
-
-// Integer BT.601 limited range (R3) on 4 pixels: yw = 4 luma bytes, uvw =
-// U0 V0 U1 V1 (the 2 chroma samples shared by pixel pairs).  Output: one word
-// of 4 bytes per channel.
-//   R = (298Y + 409V - 56992) >> 8, G = (298Y - 100U - 208V + 34784) >> 8,
-//   B = (298Y + 516U - 70688) >> 8, each clamped to [0,255]
-// (the constants fold C = Y-16, D = U-128, E = V-128 and the +128 rounding).
-__device__ __forceinline__ void bt601_4(uint32_t yw, uint32_t uvw, uint32_t& R, uint32_t& G, uint32_t& B) {
-  R = G = B = 0;
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int U = (uvw >> (16 * h)) & 0xFF, V = (uvw >> (16 * h + 8)) & 0xFF;
-    const int cr = 409 * V - 56992;
-    const int cg = 34784 - 100 * U - 208 * V;
-    const int cb = 516 * U - 70688;
-#pragma unroll
-    for (int k = 0; k < 2; ++k) {
-      const int i = 2 * h + k;
-      const int y298 = 298 * static_cast<int>((yw >> (8 * i)) & 0xFF);
-      const int r = min(max((y298 + cr) >> 8, 0), 255);
-      const int g = min(max((y298 + cg) >> 8, 0), 255);
-      const int b = min(max((y298 + cb) >> 8, 0), 255);
-      R |= static_cast<uint32_t>(r) << (8 * i);
-      G |= static_cast<uint32_t>(g) << (8 * i);
-      B |= static_cast<uint32_t>(b) << (8 * i);
+  __syncwarp();
+  // 2 frames x 24 rows = 48 copies spread over the warp
+  for (int i = lane; i < 48; i += 32) {
+    const int f = i / 24, rr = i % 24;
+    const FrameDesc fd = frs[f];
+    uint8_t* dst = raw + (f * 24 + rr) * p.SWP;
+    if (rr < kChunkRows) {
+      const int fy = max(min(p.SWP, fd.py - SX0), 0);
+      if (rr < rows_y && fy > 0)
+        bulk_g2s(dst, fd.y + static_cast<size_t>(r0 + rr) * fd.py + SX0, fy, bar);
+    } else {
+      const int u = rr - kChunkRows;
+      const int fuv = max(min(p.SWP, fd.puv - SX0), 0);
+      if (u < rows_uv && fuv > 0)
+        bulk_g2s(dst, fd.uv + static_cast<size_t>((r0 >> 1) + u) * fd.puv + SX0, fuv, bar);
     }
   }
 }
 
-__device__ __forceinline__ void st_cs_f2(float* p, float a, float b) {
-  asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
-}
-
 template <int NW, int K>
-__global__ void __launch_bounds__(56 * K) fc_fused_kernel(const __grid_constant__ Params p) {
-  constexpr int SW = 28 * K;   // output columns per strip
-  constexpr int NT = 2 * SW;   // threads: one per (frame of the pair, column)
+__global__ void __launch_bounds__(84 * K, 2) fc_fused_kernel(const __grid_constant__ Params p) {
+  constexpr int SW = 28 * K;       // output columns per strip
+  constexpr int NT = 3 * SW;       // threads: one per (channel, column) for the H pass
   constexpr int CH = kChunkRows;
   constexpr int VWS = 1 + 3 * NW;  // words per vertical-table row in smem
-  constexpr int SWR = SW + 4;      // R row stride: odd word count -> conflict-free
 
-  extern __shared__ __align__(16) uint8_t smem[];
-  float* lut = reinterpret_cast<float*>(smem);                       // 768 f32
-  uint32_t* tab = reinterpret_cast<uint32_t*>(lut + 768);            // 588
-  uint32_t* vws = tab + 588;                                          // 28 * VWS
-  uint8_t* rgb = reinterpret_cast<uint8_t*>(vws + 28 * VWS);          // [2][3][CH][SWP]
-  uint32_t* ring = reinterpret_cast<uint32_t*>(rgb + 6 * CH * p.SWP); // [2][3][SW][TRS]
-  uint8_t* Rb = reinterpret_cast<uint8_t*>(ring + 6 * SW * p.TRS);    // [2][3][28][SWR]
+  extern __shared__ __align__(1024) uint8_t smem[];
+  float* lut = reinterpret_cast<float*>(smem);                        // 3 x 256 f32, 1 KB aligned
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 3072);          // 2 mbarriers
+  uint32_t* vws = reinterpret_cast<uint32_t*>(smem + 3072 + 16);      // 28 * VWS
+  uint8_t* raw = smem + 3072 + 16 + ((28 * VWS * 4 + 15) & ~15);      // [2 buf][2 f][24 rows][SWP]
+  uint8_t* rgb = raw + 2 * 48 * p.SWP;                                // [2 f][3 c][16 rows][SWP]
+  uint32_t* ring = reinterpret_cast<uint32_t*>(rgb + 6 * CH * p.SWP); // [2 f][3 c][SW][TRS]
 
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int strip = blockIdx.x, pair = blockIdx.y;
   const int X0 = strip * SW;
   const int sw_act = min(SW, p.W2 - X0);
   const int SX0 = __ldg(p.hx + X0) & ~15;
   const int NQ = p.SWP >> 4;
+  const FrameDesc* frs = &p.fr[2 * pair];
 
-  for (int i = tid; i < 768; i += NT) lut[i] = __ldg(p.lut + i);
-  for (int e = tid; e < 588; e += NT) {
-    const int col = 2 * e, c = col / 392, tp = (col % 392) / 196, ph = (col % 196) / 14, pw = col % 14;
-    tab[e] = static_cast<uint32_t>(((tp * 3 + c) * 28 + ph) * SWR + pw) | (static_cast<uint32_t>(c) << 16);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    fence_mbar_init();
   }
+  for (int i = tid; i < 768; i += NT) lut[i] = __ldg(p.lut + i);
+  __syncthreads();
+  if (warp == 0) issue_chunk(p, frs, SX0, 0, raw, &bars[0], lane);
 
-  // horizontal weights of this thread's output column live in registers
-  const int hf = tid / SW, ho = tid - hf * SW;
+  // H pass: thread = (channel hc, column ho) for both frames; weights in registers
+  const int hc = tid / SW, ho = tid - hc * SW;
   const bool hact = ho < sw_act;
   uint32_t hw0[NW], hw1[NW], hw2[NW];
   int hoff = 0;
-  if (hact) {
-    const uint32_t* w = p.hw + static_cast<size_t>(X0 + ho) * 3 * NW;
+  {
+    const int oo = X0 + min(ho, sw_act - 1);
+    const uint32_t* w = p.hw + static_cast<size_t>(oo) * 3 * NW;
 #pragma unroll
     for (int i = 0; i < NW; ++i) {
       hw0[i] = __ldg(w + i);
       hw1[i] = __ldg(w + NW + i);
       hw2[i] = __ldg(w + 2 * NW + i);
     }
-    hoff = __ldg(p.hx + X0 + ho) - SX0;
-  } else {
-#pragma unroll
-    for (int i = 0; i < NW; ++i) hw0[i] = hw1[i] = hw2[i] = 0;
+    hoff = __ldg(p.hx + oo) - SX0;
   }
   const int hsh = (hoff & 3) * 8;
-  const int hwo = hoff >> 2;
+  const uint8_t* hsrc0 = rgb + (hc * CH) * p.SWP + (hoff & ~3);     // frame 0, row 0
+  const uint8_t* hsrc1 = hsrc0 + 3 * CH * p.SWP;                      // frame 1
+  uint32_t* hdst0 = ring + (hc * SW + ho) * p.TRS;
+  uint32_t* hdst1 = hdst0 + 3 * SW * p.TRS;
 
-  const FrameDesc* frs = &p.fr[2 * pair];
-  int done = 0;  // source rows [.., done) are in the ring (4-aligned)
+  // V pass: thread = (channel vc, column pair vxp, half of the band vjh), both frames
+  const int vc = tid / SW, vrem = tid - vc * SW;
+  const int vxp = vrem % (SW / 2), vjh = vrem / (SW / 2);
+  const int vx = 2 * vxp;
+  const bool vact = vx < sw_act;
+  const uint32_t* vcol00 = ring + (vc * SW + vx) * p.TRS;   // frame 0, column vx
+  const uint32_t* vcol01 = vcol00 + p.TRS;                  // frame 0, column vx+1
+  const uint32_t* vcol10 = vcol00 + 3 * SW * p.TRS;         // frame 1
+  const uint32_t* vcol11 = vcol10 + p.TRS;
+  const uint32_t lutb = smem_u32(lut + vc * 256);
+  // token addressing of this thread's columns (R6): x = 28 wb + 14 wm + pw
+  const int gx = X0 + vx;
+  const int vwb = gx / 28, vwm = (gx / 14) & 1, vpw = gx % 14;
 
+  int next_k = 0;
   for (int hb = 0; hb < p.gh2; ++hb) {
     const int yo0 = hb * 28;
-    const int ylo = __ldg(p.vx + yo0) & ~3;
-    const int yend = (__ldg(p.vx + yo0 + 27) + __ldg(p.vcnt + yo0 + 27) + 3) & ~3;
-    for (int r0 = max(done, ylo); r0 < yend; r0 += CH) {
-      const int rows = min(CH, yend - r0);
-      // ---- stage A1: NV12 -> RGB planes (a5), 16 pixels per item
-      for (int it = tid; it < 2 * rows * NQ; it += NT) {
+    const int yend = __ldg(p.vx + yo0 + 27) + __ldg(p.vcnt + yo0 + 27);
+    const int kneed = min(p.nchunks, (yend + CH - 1) / CH);
+    for (; next_k < kneed; ++next_k) {
+      const int k = next_k, buf = k & 1;
+      uint8_t* rawb = raw + buf * 48 * p.SWP;
+      if (warp == 0 && k + 1 < p.nchunks) {
+        fence_proxy_async();
+        issue_chunk(p, frs, SX0, k + 1, raw + (buf ^ 1) * 48 * p.SWP, &bars[buf ^ 1], lane);
+      }
+      mbar_wait(&bars[buf], (k >> 1) & 1);
+      // ---- a5: NV12 -> RGB planes, 16 pixels per item
+      const int r0 = k * CH;
+      for (int it = tid; it < 2 * CH * NQ; it += NT) {
         const int q = it % NQ;
-        const int rr = (it / NQ) % rows;
-        const int f = it / (NQ * rows);
-        const int y = r0 + rr;
-        const int x = SX0 + 16 * q;
-        uint4 Yv = make_uint4(0, 0, 0, 0), UVv = make_uint4(0, 0, 0, 0);
-        const FrameDesc fd = frs[f];
-        if (y < p.H && x < p.W) {
-          Yv = __ldg(reinterpret_cast<const uint4*>(fd.y + static_cast<size_t>(y) * fd.py + x));
-          UVv = __ldg(reinterpret_cast<const uint4*>(fd.uv + static_cast<size_t>(y >> 1) * fd.puv + x));
-        }
+        const int rr = (it / NQ) % CH;
+        const int f = it / (NQ * CH);
+        const uint4 Yv = *reinterpret_cast<const uint4*>(rawb + (f * 24 + rr) * p.SWP + 16 * q);
+        const uint4 UVv = *reinterpret_cast<const uint4*>(rawb + (f * 24 + CH + (rr >> 1)) * p.SWP + 16 * q);
         uint4 Rv, Gv, Bv;
         bt601_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x);
         bt601_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y);
@@ -205,113 +200,123 @@ __global__ void __launch_bounds__(56 * K) fc_fused_kernel(const __grid_constant_
         *reinterpret_cast<uint4*>(dst) = Rv;
         *reinterpret_cast<uint4*>(dst + CH * p.SWP) = Gv;
         *reinterpret_cast<uint4*>(dst + 2 * CH * p.SWP) = Bv;
-        if (p.dbg_src != nullptr && y < p.H) {
-          const uint32_t cw[3][4] = {{Rv.x, Rv.y, Rv.z, Rv.w}, {Gv.x, Gv.y, Gv.z, Gv.w}, {Bv.x, Bv.y, Bv.z, Bv.w}};
-          const size_t fi = static_cast<size_t>(p.frame_base + 2 * pair + f);
-          for (int i = 0; i < 16 && x + i < p.W; ++i)
-            for (int c = 0; c < 3; ++c)
-              p.dbg_src[((fi * p.H + y) * p.W + x + i) * 3 + c] = (cw[c][i >> 2] >> (8 * (i & 3))) & 0xFF;
-        }
-      }
-      __syncthreads();
-      // ---- stage A2: horizontal pass (a6) into the column-major u8 ring
-      if (hact) {
-        for (int g = 0; g < (rows >> 2); ++g) {
-          const int ringw = ((r0 >> 2) + g) % p.TRW;
-#pragma unroll 1
-          for (int c = 0; c < 3; ++c) {
-            uint32_t word = 0;
-#pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-              const uint32_t* src =
-                  reinterpret_cast<const uint32_t*>(rgb + ((hf * 3 + c) * CH + 4 * g + rr) * p.SWP) + hwo;
-              uint32_t w[NW + 1], d[NW];
-#pragma unroll
-              for (int i = 0; i <= NW; ++i) w[i] = src[i];
-#pragma unroll
-              for (int i = 0; i < NW; ++i) d[i] = __funnelshift_r(w[i], w[i + 1], hsh);
-              word |= fir_bytes<NW>(d, hw0, hw1, hw2) << (8 * rr);
-            }
-            ring[((hf * 3 + c) * SW + ho) * p.TRS + ringw] = word;
+        if (p.dbg_src != nullptr) {
+          const int y = r0 + rr, x = SX0 + 16 * q;
+          if (y < p.H) {
+            const uint32_t cw[3][4] = {{Rv.x, Rv.y, Rv.z, Rv.w}, {Gv.x, Gv.y, Gv.z, Gv.w}, {Bv.x, Bv.y, Bv.z, Bv.w}};
+            const size_t fi = static_cast<size_t>(p.frame_base + 2 * pair + f);
+            for (int i = 0; i < 16 && x + i < p.W; ++i)
+              for (int c = 0; c < 3; ++c)
+                p.dbg_src[((fi * p.H + y) * p.W + x + i) * 3 + c] = (cw[c][i >> 2] >> (8 * (i & 3))) & 0xFF;
           }
         }
       }
       __syncthreads();
+      // ---- a6: horizontal pass -> ring (4 rows packed per word, column-major)
+      if (hact) {
+        const int wbase = ((r0 >> 2) % p.TRW);
+#pragma unroll 1
+        for (int g = 0; g < CH / 4; ++g) {
+          int qa[4], qb[4];
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) {
+            const int row = 4 * g + rr;
+            const uint32_t* s0 = reinterpret_cast<const uint32_t*>(hsrc0 + row * p.SWP);
+            const uint32_t* s1 = reinterpret_cast<const uint32_t*>(hsrc1 + row * p.SWP);
+            uint32_t a[NW + 1], b[NW + 1], da[NW], db[NW];
+#pragma unroll
+            for (int i = 0; i <= NW; ++i) {
+              a[i] = s0[i];
+              b[i] = s1[i];
+            }
+#pragma unroll
+            for (int i = 0; i < NW; ++i) {
+              da[i] = __funnelshift_r(a[i], a[i + 1], hsh);
+              db[i] = __funnelshift_r(b[i], b[i + 1], hsh);
+            }
+            qa[rr] = fir_sum<NW>(da, hw0, hw1, hw2) >> 22;  // clip8 = saturating pack below
+            qb[rr] = fir_sum<NW>(db, hw0, hw1, hw2) >> 22;
+          }
+          const uint32_t word0 = pack_sat_u8(qa[1], qa[0], pack_sat_u8(qa[3], qa[2], 0));
+          const uint32_t word1 = pack_sat_u8(qb[1], qb[0], pack_sat_u8(qb[3], qb[2], 0));
+          int w = wbase + g;
+          if (w >= p.TRW) w -= p.TRW;
+          hdst0[w] = word0;
+          hdst1[w] = word1;
+        }
+      }
+      __syncthreads();
     }
-    done = max(done, yend);
-
     // ---- vertical tables of this band's 28 output rows -> smem
     for (int i = tid; i < 28 * VWS; i += NT) {
-      const int j = i / VWS, k = i - j * VWS;
+      const int j = i / VWS, kk = i - j * VWS;
       const int yo = yo0 + j;
-      vws[i] = (k == 0) ? static_cast<uint32_t>(__ldg(p.vx + yo) % p.TR)
-                        : __ldg(p.vw + static_cast<size_t>(yo) * 3 * NW + (k - 1));
+      vws[i] = (kk == 0) ? static_cast<uint32_t>(__ldg(p.vx + yo) % p.TR)
+                         : __ldg(p.vw + static_cast<size_t>(yo) * 3 * NW + (kk - 1));
     }
     __syncthreads();
-
-    // ---- stage B: vertical pass (a7) -> R[f][c][j][x] u8
-    // lanes run over output rows j (distinct ring words, conflict-free)
-    for (int it = tid; it < 14 * SW; it += NT) {
-      const int j = it % 28;
-      const int q = (it / 28) % (SW / 4);
-      const int f = it / (7 * SW);
-      const uint32_t* vj = vws + j * VWS;
-      const int ypos = static_cast<int>(vj[0]);
-      const int vwo = ypos >> 2, vsh = (ypos & 3) * 8;
-      uint32_t v0[NW], v1[NW], v2[NW];
-#pragma unroll
-      for (int i = 0; i < NW; ++i) {
-        v0[i] = vj[1 + i];
-        v1[i] = vj[1 + NW + i];
-        v2[i] = vj[1 + 2 * NW + i];
-      }
-      int widx[NW + 1];
-#pragma unroll
-      for (int i = 0; i <= NW; ++i) {
-        const int t = vwo + i;
-        widx[i] = t >= p.TRW ? t - p.TRW : t;
-      }
+    // ---- a7 + a8 + a9: vertical pass, normalise, patchify (float2 stores)
+    if (vact) {
+      const size_t trow = (static_cast<size_t>(pair) * p.gh2 + hb) * p.gw2 * 4 + vwb * 4 + vjh * 2 + vwm;
+      float* out0 = p.tokens + trow * kCols + (vc * 2 + 0) * 196 + vpw;
+      float* out1 = out0 + 196;
 #pragma unroll 1
-      for (int c = 0; c < 3; ++c) {
-        uint32_t outw = 0;
+      for (int jj = 0; jj < 14; ++jj) {
+        const int j = vjh * 14 + jj;
+        const uint32_t* vj = vws + j * VWS;
+        const int ypos = static_cast<int>(vj[0]);
+        const int vsh = (ypos & 3) * 8;
+        uint32_t v0[NW], v1[NW], v2[NW];
 #pragma unroll
-        for (int xx = 0; xx < 4; ++xx) {
-          const uint32_t* col = ring + ((f * 3 + c) * SW + 4 * q + xx) * p.TRS;
-          uint32_t w[NW + 1], d[NW];
-#pragma unroll
-          for (int i = 0; i <= NW; ++i) w[i] = col[widx[i]];
-#pragma unroll
-          for (int i = 0; i < NW; ++i) d[i] = __funnelshift_r(w[i], w[i + 1], vsh);
-          outw |= fir_bytes<NW>(d, v0, v1, v2) << (8 * xx);
+        for (int i = 0; i < NW; ++i) {
+          v0[i] = vj[1 + i];
+          v1[i] = vj[1 + NW + i];
+          v2[i] = vj[1 + 2 * NW + i];
         }
-        *reinterpret_cast<uint32_t*>(Rb + ((f * 3 + c) * 28 + j) * SWR + 4 * q) = outw;
+        int widx[NW + 1];
+#pragma unroll
+        for (int i = 0; i <= NW; ++i) {
+          const int t = (ypos >> 2) + i;
+          widx[i] = t >= p.TRW ? t - p.TRW : t;
+        }
+        uint32_t a0[NW + 1], a1[NW + 1], b0[NW + 1], b1[NW + 1];
+#pragma unroll
+        for (int i = 0; i <= NW; ++i) {
+          a0[i] = vcol00[widx[i]];
+          a1[i] = vcol01[widx[i]];
+          b0[i] = vcol10[widx[i]];
+          b1[i] = vcol11[widx[i]];
+        }
+        uint32_t da0[NW], da1[NW], db0[NW], db1[NW];
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+          da0[i] = __funnelshift_r(a0[i], a0[i + 1], vsh);
+          da1[i] = __funnelshift_r(a1[i], a1[i + 1], vsh);
+          db0[i] = __funnelshift_r(b0[i], b0[i + 1], vsh);
+          db1[i] = __funnelshift_r(b1[i], b1[i + 1], vsh);
+        }
+        // clip8 then table index: clamp S to [0, 2^30-1], byte = S >> 22
+        const uint32_t s00 = static_cast<uint32_t>(add_min_relu(fir_sum<NW>(da0, v0, v1, v2), 0, (1 << 30) - 1));
+        const uint32_t s01 = static_cast<uint32_t>(add_min_relu(fir_sum<NW>(da1, v0, v1, v2), 0, (1 << 30) - 1));
+        const uint32_t s10 = static_cast<uint32_t>(add_min_relu(fir_sum<NW>(db0, v0, v1, v2), 0, (1 << 30) - 1));
+        const uint32_t s11 = static_cast<uint32_t>(add_min_relu(fir_sum<NW>(db1, v0, v1, v2), 0, (1 << 30) - 1));
+        float o00, o01, o10, o11;
+        asm("ld.shared.f32 %0, [%1];" : "=f"(o00) : "r"(((s00 >> 20) & 0x3FCu) + lutb));
+        asm("ld.shared.f32 %0, [%1];" : "=f"(o01) : "r"(((s01 >> 20) & 0x3FCu) + lutb));
+        asm("ld.shared.f32 %0, [%1];" : "=f"(o10) : "r"(((s10 >> 20) & 0x3FCu) + lutb));
+        asm("ld.shared.f32 %0, [%1];" : "=f"(o11) : "r"(((s11 >> 20) & 0x3FCu) + lutb));
+        st_cs_f2(out0 + jj * 14, o00, o01);
+        st_cs_f2(out1 + jj * 14, o10, o11);
         if (p.dbg_rs != nullptr) {
-          const size_t fi = static_cast<size_t>(p.frame_base + 2 * pair + f);
-          for (int xx = 0; xx < 4; ++xx) {
-            const int x = X0 + 4 * q + xx;
-            if (x < p.W2)
-              p.dbg_rs[((fi * p.H2 + yo0 + j) * p.W2 + x) * 3 + c] = (outw >> (8 * xx)) & 0xFF;
-          }
+          const size_t fi0 = static_cast<size_t>(p.frame_base + 2 * pair);
+          const int yo = yo0 + j;
+          uint8_t* d0 = p.dbg_rs + ((fi0 * p.H2 + yo) * p.W2 + gx) * 3 + vc;
+          uint8_t* d1 = d0 + static_cast<size_t>(p.H2) * p.W2 * 3;
+          d0[0] = s00 >> 22;
+          d0[3] = s01 >> 22;
+          d1[0] = s10 >> 22;
+          d1[3] = s11 >> 22;
         }
-      }
-    }
-    __syncthreads();
-
-    // ---- stage C: normalise (a8) + patchify (a9), coalesced float2 stores
-    {
-      const int kact = min(K, p.gw2 - strip * K);
-      const int nrows = 4 * kact;
-      const size_t row0 = (static_cast<size_t>(pair) * p.gh2 * p.gw2 + static_cast<size_t>(hb) * p.gw2 +
-                           static_cast<size_t>(strip) * K) * 4;
-      float* out = p.tokens + row0 * kCols;
-      for (int it = tid; it < nrows * 588; it += NT) {
-        const int r = it / 588, e = it - r * 588;
-        const uint32_t te = tab[e];
-        const int wbl = r >> 2, hm = (r >> 1) & 1, wm = r & 1;
-        const int roff = static_cast<int>(te & 0xFFFF) + 14 * hm * SWR + 28 * wbl + 14 * wm;
-        const uint32_t v2 = *reinterpret_cast<const uint16_t*>(Rb + roff);
-        const float* l = lut + (te >> 16) * 256;
-        st_cs_f2(out + static_cast<size_t>(it) * 2, l[v2 & 0xFF], l[v2 >> 8]);
       }
     }
     __syncthreads();
@@ -375,6 +380,21 @@ static cudaError_t upload(T** dst, const std::vector<T>& v) {
 
 static int plan_nw(const fc_plan_s* P) { return pick_nw(std::max(P->th.words, P->tv.words)); }
 
+// Process-wide cache of uploaded tables, keyed by everything the tables are
+// a function of (device, W->W', H->H', packing width, normalisation).  Plans
+// of equally shaped requests share one upload, so fc_plan + fc_preprocess
+// never touch the device synchronously after the first request of a shape.
+struct TableKey {
+  int dev, w, w2, h, h2, nw;
+  uint32_t lut_bits[768];
+  bool operator<(const TableKey& o) const {
+    return std::memcmp(this, &o, sizeof(TableKey)) < 0;
+  }
+};
+
+static std::mutex g_tables_mu;
+static std::map<TableKey, DeviceTables>* g_tables = new std::map<TableKey, DeviceTables>();  // never freed
+
 static fc_status device_tables(fc_plan_s* P, int dev, DeviceTables** out) {
   std::lock_guard<std::mutex> lk(P->mu);
   auto it = P->dev.find(dev);
@@ -383,6 +403,21 @@ static fc_status device_tables(fc_plan_s* P, int dev, DeviceTables** out) {
     return FC_OK;
   }
   const int nw = plan_nw(P);
+  TableKey key;
+  std::memset(&key, 0, sizeof(key));
+  key.dev = dev;
+  key.w = P->th.in;
+  key.w2 = P->th.out;
+  key.h = P->tv.in;
+  key.h2 = P->tv.out;
+  key.nw = nw;
+  std::memcpy(key.lut_bits, P->lut.data(), sizeof(key.lut_bits));
+  std::lock_guard<std::mutex> gk(g_tables_mu);
+  auto git = g_tables->find(key);
+  if (git != g_tables->end()) {
+    *out = &(P->dev[dev] = git->second);
+    return FC_OK;
+  }
   DeviceTables t;
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = upload(&t.hx, P->th.xmin);
@@ -398,19 +433,20 @@ static fc_status device_tables(fc_plan_s* P, int dev, DeviceTables** out) {
     return e == cudaErrorMemoryAllocation ? fail(FC_ERR_OOM, "table upload: out of device memory")
                                           : cuda_fail(e, "table upload");
   }
+  (*g_tables)[key] = t;
   *out = &(P->dev[dev] = t);
   return FC_OK;
 }
 
 struct Geometry {
-  int K, nw, SWP, TR, TRW, TRS, nstrips;
+  int K, nw, SWP, TR, TRW, TRS, nstrips, nchunks;
   size_t smem;
 };
 
 static size_t smem_bytes(int K, int nw, int SWP, int TRS) {
   const int SW = 28 * K;
-  return 768 * 4 + 588 * 4 + 28 * (1 + 3 * nw) * 4 + static_cast<size_t>(6) * kChunkRows * SWP +
-         static_cast<size_t>(6) * SW * TRS * 4 + static_cast<size_t>(6) * 28 * (SW + 4);
+  return 3072 + 16 + ((28 * (1 + 3 * nw) * 4 + 15) & ~15) + static_cast<size_t>(2) * 48 * SWP +
+         static_cast<size_t>(6) * kChunkRows * SWP + static_cast<size_t>(6) * SW * TRS * 4;
 }
 
 static bool geometry(const fc_plan_s* P, int K, Geometry* g) {
@@ -432,11 +468,16 @@ static bool geometry(const fc_plan_s* P, int K, Geometry* g) {
     }
     swp = std::max(swp, (need + 15) & ~15);
   }
+  // ring: after the chunks a band needs (16-row granularity) the ring must
+  // still hold the band's first source row
   int tr = 4 * (nw + 1);
+  int kmax = 0;
   for (int hb = 0; hb < P->h2 / 28; ++hb) {
     const int ylo = tv.xmin[hb * 28] & ~3;
-    const int yend = (tv.xmin[hb * 28 + 27] + tv.cnt[hb * 28 + 27] + 3) & ~3;
-    tr = std::max(tr, yend - ylo);
+    const int yend = tv.xmin[hb * 28 + 27] + tv.cnt[hb * 28 + 27];
+    const int kneed = (yend + kChunkRows - 1) / kChunkRows;
+    tr = std::max(tr, kneed * kChunkRows - ylo);
+    kmax = std::max(kmax, kneed);
   }
   tr = (tr + 3) & ~3;
   g->K = K;
@@ -446,6 +487,7 @@ static bool geometry(const fc_plan_s* P, int K, Geometry* g) {
   g->TRW = tr / 4;
   g->TRS = (g->TRW & 1) ? g->TRW : g->TRW + 1;
   g->nstrips = nstrips;
+  g->nchunks = std::min(kmax, (P->meta.height + kChunkRows - 1) / kChunkRows);
   g->smem = smem_bytes(K, nw, swp, g->TRS);
   return true;
 }
@@ -521,6 +563,7 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
   prm.TR = g.TR;
   prm.TRW = g.TRW;
   prm.TRS = g.TRS;
+  prm.nchunks = g.nchunks;
   prm.hx = dt->hx;
   prm.hw = dt->hw;
   prm.vx = dt->vx;
@@ -542,7 +585,7 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
       prm.fr[i] = FrameDesc{sf.y, sf.uv, static_cast<int32_t>(sf.pitch_y), static_cast<int32_t>(sf.pitch_uv)};
     }
     dim3 grid(g.nstrips, static_cast<unsigned>(cnt / 2));
-    fn<<<grid, 56 * g.K, g.smem, s>>>(prm);
+    fn<<<grid, 84 * g.K, g.smem, s>>>(prm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   }
@@ -581,16 +624,7 @@ fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* rank
 }
 
 void fc_plan_destroy(fc_plan_t* P) {
-  if (!P) return;
-  for (auto& kv : P->dev) {
-    int cur = 0;
-    cudaGetDevice(&cur);
-    cudaSetDevice(kv.first);
-    DeviceTables& t = kv.second;
-    cudaFree(t.hx); cudaFree(t.hcnt); cudaFree(t.hw); cudaFree(t.vx); cudaFree(t.vcnt); cudaFree(t.vw);
-    cudaFree(t.lut);
-    cudaSetDevice(cur);
-  }
+  // device tables belong to the process-wide cache (shared by equal shapes)
   delete P;
 }
 
