@@ -42,6 +42,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// 2-D tensor copy global -> shared through the TMA engine (UTMALDG): the box
+// at element coordinates (x, y) of the tensor map; out-of-bounds bytes are
+// zero-filled and still counted in the transaction bytes.
+__device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
 // ---------------------------------------------------------------- integer math
 __device__ __forceinline__ uint32_t dp4a_uu(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -71,6 +85,12 @@ __device__ __forceinline__ uint32_t pack_sat_u8(int a, int b, uint32_t c) {
   asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
   return d;
 }
+// (sat_u16(a) << 16) | sat_u16(b)
+__device__ __forceinline__ uint32_t pack_sat_u16(int a, int b) {
+  uint32_t d;
+  asm("cvt.pack.sat.u16.s32 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
 // relu(min(a + b, c)): one VIADDMNMX.RELU
 __device__ __forceinline__ int add_min_relu(int a, int b, int c) {
   int d;
@@ -79,18 +99,23 @@ __device__ __forceinline__ int add_min_relu(int a, int b, int c) {
 }
 
 // Exact 22-bit fixed-point FIR over NW words of 4 taps (R4):
-//   S = 2^21 + sum px*iw = s0 + 256*s1 + 65536*s2 (int32, modular == exact).
+//   S = 2^21 + sum px*iw = ((s2*256 + s1)*256 + s0), with the byte planes
+// accumulated as one DP4A chain (plane 2 first, seeded with 32 = 2^21/2^16,
+// shifted left 8 between planes).  int32 arithmetic is modular, so the
+// result equals the exact sum whenever the exact sum fits (R4 headroom).
 template <int NW>
 __device__ __forceinline__ int fir_sum(const uint32_t (&d)[NW], const uint32_t (&w0)[NW], const uint32_t (&w1)[NW],
                                        const uint32_t (&w2)[NW]) {
-  uint32_t s0 = 1u << 21, s1 = 0, s2 = 0;
+  uint32_t s = 32u;
 #pragma unroll
-  for (int i = 0; i < NW; ++i) {
-    s0 = dp4a_uu(d[i], w0[i], s0);
-    s1 = dp4a_uu(d[i], w1[i], s1);
-    s2 = dp4a_us(d[i], w2[i], s2);
-  }
-  return static_cast<int>(s0 + (s1 << 8) + (s2 << 16));
+  for (int i = 0; i < NW; ++i) s = dp4a_us(d[i], w2[i], s);
+  s <<= 8;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) s = dp4a_uu(d[i], w1[i], s);
+  s <<= 8;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) s = dp4a_uu(d[i], w0[i], s);
+  return static_cast<int>(s);
 }
 
 // Integer BT.601 limited range (R3) on 4 pixels.  yw = Y0..Y3 bytes, uvw =
@@ -112,15 +137,88 @@ __device__ __forceinline__ void bt601_4(uint32_t yw, uint32_t uvw, uint32_t& R, 
   const uint32_t yu23 = __byte_perm(yw, uvw, 0x6362);
   const int g0 = dp2a_lo(kGv, yv01, 34784);  // -208*V0 + 34784
   const int g1 = dp2a_lo(kGv, yv23, 34784);
-  const int r0 = dp2a_lo(kR, yv01, -56992) >> 8, r1 = dp2a_hi(kR, yv01, -56992) >> 8;
-  const int r2 = dp2a_lo(kR, yv23, -56992) >> 8, r3 = dp2a_hi(kR, yv23, -56992) >> 8;
-  const int b0 = dp2a_lo(kB, yu01, -70688) >> 8, b1 = dp2a_hi(kB, yu01, -70688) >> 8;
-  const int b2 = dp2a_lo(kB, yu23, -70688) >> 8, b3 = dp2a_hi(kB, yu23, -70688) >> 8;
-  const int q0 = dp2a_lo(kG, yu01, g0) >> 8, q1 = dp2a_hi(kG, yu01, g0) >> 8;
-  const int q2 = dp2a_lo(kG, yu23, g1) >> 8, q3 = dp2a_hi(kG, yu23, g1) >> 8;
-  R = pack_sat_u8(r1, r0, pack_sat_u8(r3, r2, 0));
-  G = pack_sat_u8(q1, q0, pack_sat_u8(q3, q2, 0));
-  B = pack_sat_u8(b1, b0, pack_sat_u8(b3, b2, 0));
+  // t -> clamp(t >> 8, 0, 255) == byte 1 of sat_u16(t): pack two saturated
+  // halves, then gather the high bytes of four values with one PRMT.
+  const uint32_t r01 = pack_sat_u16(dp2a_hi(kR, yv01, -56992), dp2a_lo(kR, yv01, -56992));
+  const uint32_t r23 = pack_sat_u16(dp2a_hi(kR, yv23, -56992), dp2a_lo(kR, yv23, -56992));
+  const uint32_t b01 = pack_sat_u16(dp2a_hi(kB, yu01, -70688), dp2a_lo(kB, yu01, -70688));
+  const uint32_t b23 = pack_sat_u16(dp2a_hi(kB, yu23, -70688), dp2a_lo(kB, yu23, -70688));
+  const uint32_t g01 = pack_sat_u16(dp2a_hi(kG, yu01, g0), dp2a_lo(kG, yu01, g0));
+  const uint32_t g23 = pack_sat_u16(dp2a_hi(kG, yu23, g1), dp2a_lo(kG, yu23, g1));
+  R = __byte_perm(r01, r23, 0x7531);
+  G = __byte_perm(g01, g23, 0x7531);
+  B = __byte_perm(b01, b23, 0x7531);
+}
+
+// ---------------------------------------------------------------- int8 MMA
+// D = A(16x32 u8, row) * B(32x8, col) + C, s32.  Fragment layout (g = lane/4,
+// t = lane%4; verified on B200 by tools/ubench/mma_layout.cu):
+//   a0: row g,  k 4t..4t+3   a1: row g+8   a2: k+16   a3: row g+8, k+16
+//   b0: col g,  k 4t..4t+3   b1: k+16
+//   d0,d1: row g, cols 2t,2t+1   d2,d3: row g+8
+template <bool kSignedB>
+__device__ __forceinline__ void mma_u8(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  if constexpr (kSignedB) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  } else {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+}
+
+// Exact 22-bit fixed-point FIR as three independent byte-plane MMAs (R4):
+//   S = 2^21 + sum px*iw = ((D2 << 8) + D1) << 8) + D0,  D2 = A*B2 + 32,
+// D1 = A*B1, D0 = A*B0 (s32, modular == exact).  The planes are independent so
+// the three MMAs overlap; the combine is two LEAs on the ALU pipe.
+// bf[ks][plane][2]: B fragments of the KS k-steps.
+template <int KS>
+__device__ __forceinline__ void fir_mma_planes(int (&d2)[4], int (&d1)[4], int (&d0)[4], const uint32_t (&a)[KS][4],
+                                               const uint32_t (&bf)[KS][3][2]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    d2[i] = 32;
+    d1[i] = 0;
+    d0[i] = 0;
+  }
+#pragma unroll
+  for (int k = 0; k < KS; ++k) {
+    mma_u8<true>(d2, a[k], bf[k][2][0], bf[k][2][1]);
+    mma_u8<false>(d1, a[k], bf[k][1][0], bf[k][1][1]);
+    mma_u8<false>(d0, a[k], bf[k][0][0], bf[k][0][1]);
+  }
+}
+__device__ __forceinline__ int combine_planes(int d2, int d1, int d0) {
+  const uint32_t t = (static_cast<uint32_t>(d2) << 8) + static_cast<uint32_t>(d1);
+  return static_cast<int>((t << 8) + static_cast<uint32_t>(d0));
+}
+
+__device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void sts8(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float ldsf(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
 }
 
 __device__ __forceinline__ void st_cs_f2(float* p, float a, float b) {

@@ -38,14 +38,17 @@ struct RankPlan {
   fc_rank_plan p{};
 };
 
+// Device copies of a plan's tables (see fc_kernels.cu: MMA fragment tables).
 struct DeviceTables {
-  int32_t* hx = nullptr;
-  int32_t* hcnt = nullptr;
-  uint32_t* hw = nullptr;
-  int32_t* vx = nullptr;
-  int32_t* vcnt = nullptr;
-  uint32_t* vw = nullptr;
-  float* lut = nullptr;
+  int ksh = 1, ksv = 1;        // MMA k-steps of the H / V windows
+  int32_t* hx = nullptr;       // H xmin per output column
+  int32_t* hxs = nullptr;      // H window start per 8-column tile
+  uint32_t* hfr = nullptr;     // H B fragments
+  int32_t* vx = nullptr;       // V ymin per output row
+  int32_t* vcnt = nullptr;     // V taps per output row
+  int32_t* vys = nullptr;      // V window start per (band, 8-row group)
+  uint32_t* vfr = nullptr;     // V B fragments
+  float* lut = nullptr;        // 3 x 256 normalisation table (R5)
 };
 
 }  // namespace fc

@@ -20,14 +20,17 @@
 // that 4 vertically adjacent taps are one 32-bit word); the vertical pass
 // reads the ring.  All resize MACs are exact integer DP4A on byte planes of
 // Pillow's 22-bit weights:  sum px*iw = d0 + 256*d1 + 65536*d2.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "fc_device.cuh"
@@ -35,340 +38,389 @@
 
 namespace fc {
 
-constexpr int kChunkRows = 16;             // source rows per stage-A chunk
-constexpr int kMaxFramesPerLaunch = 1200;  // frame descriptors passed by value
-
-struct FrameDesc {
-  const uint8_t* y;
-  const uint8_t* uv;
-  int32_t py, puv;
-};
+constexpr int kChunkRows = 16;             // source rows per chunk
+constexpr int kTileN = 8;                  // outputs per H-pass MMA tile (N of m16n8k32)
+constexpr int kStrip = 84;                 // output columns per strip: 3 merge blocks = 6 patches
+constexpr int kComputeWarps = 12;
+constexpr int kComputeThreads = 32 * kComputeWarps;
+constexpr int kThreads = kComputeThreads + 32;  // + 1 TMA producer warp
+constexpr int kMaxFramesPerLaunch = 120;   // TMA tensor maps (2 per frame) passed by value
+constexpr int kRingStride = 6 * kStrip + 16;  // ring row stride (words): == 8 mod 32, conflict-free A loads
+constexpr int kStages = 4;                 // raw NV12 chunk buffers (TMA runs kStages-1 chunks ahead)
 
 struct Params {
   int W, H, W2, H2;
   int gh2, gw2;       // merge blocks per column / row
-  int nstrips;
-  int SWP;            // bytes per source row in the chunk buffers
-  int TR, TRW, TRS;   // ring rows, ring words, column stride in words
-  int nchunks;        // ceil(H / 16)
-  const int32_t* hx;
-  const uint32_t* hw;
-  const int32_t* vx;
+  int nstrips, npairs;
+  int sw, htiles;      // strip width (84 or 28 output columns), H tiles per strip
+  int SWP;            // RGB-plane row stride (odd multiple of 16)
+  int SWPN;           // source-window bytes needed per row
+  int BW, NX;         // TMA box width (<= 256) and boxes per row: NX*BW >= SWPN
+  int TR, TRW;        // ring rows / words
+  int nchunks;        // chunks any band needs
+  const int32_t* hx;    // H table: xmin per output column
+  const int32_t* hxs;   // H MMA tiles: 4-aligned window start per tile of 8 outputs
+  const uint32_t* hfr;  // H MMA tiles: B fragments [tile][KS][3][32][2]
+  const int32_t* vx;    // V table: ymin / count per output row
   const int32_t* vcnt;
-  const uint32_t* vw;
+  const int32_t* vys;   // V MMA groups: 4-aligned window start per (band, group of 8 rows)
+  const uint32_t* vfr;  // V MMA groups: B fragments [group][KS][3][32][2]
   const float* lut;
   float* tokens;      // first token row of this launch's first pair
   uint8_t* dbg_src;   // [nframes_total, H, W, 3] or null
   uint8_t* dbg_rs;    // [nframes_total, H2, W2, 3] or null
   int frame_base;     // index of fr[0] within the rank's frame list (debug dumps)
+  int skip;           // profiling only (FC_PROFILE_SKIP): 1 = colour, 2 = H pass, 4 = V pass
   int nframes;
-  FrameDesc fr[kMaxFramesPerLaunch];
+  CUtensorMap tm[2 * kMaxFramesPerLaunch];  // per frame: Y plane (box BW x 16), UV plane (box BW x 8)
 };
 
-// Issue the TMA bulk copies of one 16-row chunk (both frames, Y rows + the
-// 8 UV rows) into raw buffer `buf`.  Executed by warp 0; lane 0 arms the
-// mbarrier with the chunk's byte count first.
-__device__ __forceinline__ void issue_chunk(const Params& p, const FrameDesc* frs, int SX0, int k, uint8_t* raw,
-                                            uint64_t* bar, int lane) {
-  const int r0 = k * kChunkRows;
-  const int rows_y = min(kChunkRows, p.H - r0);
-  const int rows_uv = min(kChunkRows / 2, (p.H >> 1) - (r0 >> 1));
-  if (lane == 0) {
-    uint32_t bytes = 0;
-#pragma unroll
-    for (int f = 0; f < 2; ++f) {
-      const int fy = max(min(p.SWP, frs[f].py - SX0), 0), fuv = max(min(p.SWP, frs[f].puv - SX0), 0);
-      bytes += rows_y * fy + rows_uv * fuv;
-    }
-    mbar_arrive_expect_tx(bar, bytes);
-  }
+// Walk of one CTA's work: contiguous (pair, strip, band) items, split into
+// runs that stay inside one (pair, strip).
+struct Run {
+  int pair, strip, hb0, hb1, kfirst, klast;
+};
+
+__device__ __forceinline__ bool next_run(const Params& p, int& cur, int i1, Run& r) {
+  if (cur >= i1) return false;
+  const int ps = cur / p.gh2;
+  r.hb0 = cur - ps * p.gh2;
+  r.pair = ps / p.nstrips;
+  r.strip = ps - r.pair * p.nstrips;
+  r.hb1 = min(p.gh2, r.hb0 + (i1 - cur));
+  cur += r.hb1 - r.hb0;
+  r.kfirst = (__ldg(p.vx + 28 * r.hb0) & ~3) / kChunkRows;
+  r.klast = min(p.nchunks, (__ldg(p.vx + 28 * r.hb1 - 1) + __ldg(p.vcnt + 28 * r.hb1 - 1) + kChunkRows - 1) / kChunkRows);
+  return true;
+}
+
+// Issue the TMA tensor copies of one 16-row chunk into a raw stage: per frame
+// of the pair, NX boxes of Y (BW x 16 rows) then NX boxes of UV (BW x 8 rows).
+// Lane 0 arms the full barrier with the stage's byte count first.
+__device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, int k, uint8_t* raw, uint64_t* bar,
+                                            int lane) {
+  const int boxes = 2 * 2 * p.NX;  // frames x planes x boxes
+  if (lane == 0) mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * 24 * p.BW * p.NX));
   __syncwarp();
-  // 2 frames x 24 rows = 48 copies spread over the warp
-  for (int i = lane; i < 48; i += 32) {
-    const int f = i / 24, rr = i % 24;
-    const FrameDesc fd = frs[f];
-    uint8_t* dst = raw + (f * 24 + rr) * p.SWP;
-    if (rr < kChunkRows) {
-      const int fy = max(min(p.SWP, fd.py - SX0), 0);
-      if (rr < rows_y && fy > 0)
-        bulk_g2s(dst, fd.y + static_cast<size_t>(r0 + rr) * fd.py + SX0, fy, bar);
-    } else {
-      const int u = rr - kChunkRows;
-      const int fuv = max(min(p.SWP, fd.puv - SX0), 0);
-      if (u < rows_uv && fuv > 0)
-        bulk_g2s(dst, fd.uv + static_cast<size_t>((r0 >> 1) + u) * fd.puv + SX0, fuv, bar);
-    }
+  if (lane < boxes) {
+    const int f = lane / (2 * p.NX), rest = lane % (2 * p.NX), pl = rest / p.NX, sub = rest % p.NX;
+    uint8_t* dst = raw + f * 24 * p.BW * p.NX + (pl ? 16 * p.BW * p.NX + sub * 8 * p.BW : sub * 16 * p.BW);
+    tma_load_2d(dst, &p.tm[2 * (2 * pair + f) + pl], SX0 + sub * p.BW, pl ? k * (kChunkRows / 2) : k * kChunkRows,
+                bar);
   }
 }
 
-template <int NW, int K>
-__global__ void __launch_bounds__(84 * K, 2) fc_fused_kernel(const __grid_constant__ Params p) {
-  constexpr int SW = 28 * K;       // output columns per strip
-  constexpr int NT = 3 * SW;       // threads: one per (channel, column) for the H pass
+// Persistent, warp-specialised fused kernel.
+//   warp 12      : TMA producer -- streams NV12 rows of the next chunk into a
+//                  double-buffered raw area (full/empty mbarriers).
+//   warps 0..11  : a5 colour (integer BT.601, dp2a) -> RGB planes;
+//                  a6 horizontal pass: warp w < 11 owns output tile w (8 columns)
+//                  of the strip; three chained int8 MMAs per 16 rows x 8 outputs
+//                  -> u8 ring (4 source rows per 32-bit word);
+//                  a7 vertical pass: warp w owns 8-row group (w&3) of the band and
+//                  planes {2(w>>2), 2(w>>2)+1}; one MMA tile per 14-column patch,
+//                  then a8 table + a9 patch-order stores.
+// Work items are (pair, strip, band) triples; CTA b takes [b*T/G, (b+1)*T/G).
+// Strips are whole merge blocks, so every token row is written by one CTA in
+// one band (no partial-sector merging across CTAs in L2).
+template <int KSH, int KSV>
+__global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_constant__ Params p) {
+  constexpr int SW = kStrip;
   constexpr int CH = kChunkRows;
-  constexpr int VWS = 1 + 3 * NW;  // words per vertical-table row in smem
+  constexpr int RS = kRingStride;
 
   extern __shared__ __align__(1024) uint8_t smem[];
-  float* lut = reinterpret_cast<float*>(smem);                        // 3 x 256 f32, 1 KB aligned
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 3072);          // 2 mbarriers
-  uint32_t* vws = reinterpret_cast<uint32_t*>(smem + 3072 + 16);      // 28 * VWS
-  uint8_t* raw = smem + 3072 + 16 + ((28 * VWS * 4 + 15) & ~15);      // [2 buf][2 f][24 rows][SWP]
-  uint8_t* rgb = raw + 2 * 48 * p.SWP;                                // [2 f][3 c][16 rows][SWP]
-  uint32_t* ring = reinterpret_cast<uint32_t*>(rgb + 6 * CH * p.SWP); // [2 f][3 c][SW][TRS]
+  float* lut = reinterpret_cast<float*>(smem);                    // 3 x 256 f32 at offset 0
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 3072);      // kStages full barriers
+  uint64_t* empty = full + kStages;                               // kStages empty barriers
+  const int RAWF = 24 * p.BW * p.NX;                              // raw bytes per frame per stage
+  uint8_t* raw = smem + 3072 + 128;                               // [kStages][2 f][Y boxes | UV boxes]
+  const int SWP = p.SWP;
+  uint8_t* rgb = raw + kStages * 2 * RAWF;                        // [2 f][3 c][16 rows][SWP]
+  uint32_t* ring = reinterpret_cast<uint32_t*>(rgb + 6 * CH * SWP);  // [TRW][RS] words: [w][f][c][x]
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int strip = blockIdx.x, pair = blockIdx.y;
-  const int X0 = strip * SW;
-  const int sw_act = min(SW, p.W2 - X0);
-  const int SX0 = __ldg(p.hx + X0) & ~15;
-  const int NQ = p.SWP >> 4;
-  const FrameDesc* frs = &p.fr[2 * pair];
+  const int g = lane >> 2, tq = lane & 3;
 
   if (tid == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kComputeWarps);
+    }
     fence_mbar_init();
   }
-  for (int i = tid; i < 768; i += NT) lut[i] = __ldg(p.lut + i);
+  for (int i = tid; i < 768; i += kThreads) lut[i] = __ldg(p.lut + i);
   __syncthreads();
-  if (warp == 0) issue_chunk(p, frs, SX0, 0, raw, &bars[0], lane);
 
-  // H pass: thread = (channel hc, column ho) for both frames; weights in registers
-  const int hc = tid / SW, ho = tid - hc * SW;
-  const bool hact = ho < sw_act;
-  uint32_t hw0[NW], hw1[NW], hw2[NW];
-  int hoff = 0;
-  {
-    const int oo = X0 + min(ho, sw_act - 1);
-    const uint32_t* w = p.hw + static_cast<size_t>(oo) * 3 * NW;
-#pragma unroll
-    for (int i = 0; i < NW; ++i) {
-      hw0[i] = __ldg(w + i);
-      hw1[i] = __ldg(w + NW + i);
-      hw2[i] = __ldg(w + 2 * NW + i);
-    }
-    hoff = __ldg(p.hx + oo) - SX0;
-  }
-  const int hsh = (hoff & 3) * 8;
-  const uint8_t* hsrc0 = rgb + (hc * CH) * p.SWP + (hoff & ~3);     // frame 0, row 0
-  const uint8_t* hsrc1 = hsrc0 + 3 * CH * p.SWP;                      // frame 1
-  uint32_t* hdst0 = ring + (hc * SW + ho) * p.TRS;
-  uint32_t* hdst1 = hdst0 + 3 * SW * p.TRS;
+  const int total = p.npairs * p.nstrips * p.gh2;
+  const int i0 = static_cast<int>((static_cast<long long>(blockIdx.x) * total) / gridDim.x);
+  const int i1 = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * total) / gridDim.x);
 
-  // V pass: thread = (channel vc, column pair vxp, half of the band vjh), both frames
-  const int vc = tid / SW, vrem = tid - vc * SW;
-  const int vxp = vrem % (SW / 2), vjh = vrem / (SW / 2);
-  const int vx = 2 * vxp;
-  const bool vact = vx < sw_act;
-  const uint32_t* vcol00 = ring + (vc * SW + vx) * p.TRS;   // frame 0, column vx
-  const uint32_t* vcol01 = vcol00 + p.TRS;                  // frame 0, column vx+1
-  const uint32_t* vcol10 = vcol00 + 3 * SW * p.TRS;         // frame 1
-  const uint32_t* vcol11 = vcol10 + p.TRS;
-  const uint32_t lutb = smem_u32(lut + vc * 256);
-  // token addressing of this thread's columns (R6): x = 28 wb + 14 wm + pw
-  const int gx = X0 + vx;
-  const int vwb = gx / 28, vwm = (gx / 14) & 1, vpw = gx % 14;
-
-  int next_k = 0;
-  for (int hb = 0; hb < p.gh2; ++hb) {
-    const int yo0 = hb * 28;
-    const int yend = __ldg(p.vx + yo0 + 27) + __ldg(p.vcnt + yo0 + 27);
-    const int kneed = min(p.nchunks, (yend + CH - 1) / CH);
-    for (; next_k < kneed; ++next_k) {
-      const int k = next_k, buf = k & 1;
-      uint8_t* rawb = raw + buf * 48 * p.SWP;
-      if (warp == 0 && k + 1 < p.nchunks) {
+  // ------------------------------------------------------------ producer warp
+  if (warp == kComputeWarps) {
+    uint32_t seq = 0;
+    int cur = i0;
+    Run r;
+    while (next_run(p, cur, i1, r)) {
+      const int SX0 = __ldg(p.hx + r.strip * p.sw) & ~15;
+      if (lane < 4) prefetch_tmap(&p.tm[2 * (2 * r.pair) + lane]);
+      for (int k = r.kfirst; k < r.klast; ++k, ++seq) {
+        const int buf = seq % kStages;
+        mbar_wait(&empty[buf], ((seq / kStages) & 1) ^ 1);
         fence_proxy_async();
-        issue_chunk(p, frs, SX0, k + 1, raw + (buf ^ 1) * 48 * p.SWP, &bars[buf ^ 1], lane);
+        issue_chunk(p, r.pair, SX0, k, raw + buf * 2 * RAWF, &full[buf], lane);
       }
-      mbar_wait(&bars[buf], (k >> 1) & 1);
-      // ---- a5: NV12 -> RGB planes, 16 pixels per item
-      const int r0 = k * CH;
-      for (int it = tid; it < 2 * CH * NQ; it += NT) {
-        const int q = it % NQ;
-        const int rr = (it / NQ) % CH;
-        const int f = it / (NQ * CH);
-        const uint4 Yv = *reinterpret_cast<const uint4*>(rawb + (f * 24 + rr) * p.SWP + 16 * q);
-        const uint4 UVv = *reinterpret_cast<const uint4*>(rawb + (f * 24 + CH + (rr >> 1)) * p.SWP + 16 * q);
-        uint4 Rv, Gv, Bv;
-        bt601_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x);
-        bt601_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y);
-        bt601_4(Yv.z, UVv.z, Rv.z, Gv.z, Bv.z);
-        bt601_4(Yv.w, UVv.w, Rv.w, Gv.w, Bv.w);
-        uint8_t* dst = rgb + ((f * 3) * CH + rr) * p.SWP + 16 * q;
-        *reinterpret_cast<uint4*>(dst) = Rv;
-        *reinterpret_cast<uint4*>(dst + CH * p.SWP) = Gv;
-        *reinterpret_cast<uint4*>(dst + 2 * CH * p.SWP) = Bv;
-        if (p.dbg_src != nullptr) {
-          const int y = r0 + rr, x = SX0 + 16 * q;
-          if (y < p.H) {
-            const uint32_t cw[3][4] = {{Rv.x, Rv.y, Rv.z, Rv.w}, {Gv.x, Gv.y, Gv.z, Gv.w}, {Bv.x, Bv.y, Bv.z, Bv.w}};
-            const size_t fi = static_cast<size_t>(p.frame_base + 2 * pair + f);
-            for (int i = 0; i < 16 && x + i < p.W; ++i)
-              for (int c = 0; c < 3; ++c)
-                p.dbg_src[((fi * p.H + y) * p.W + x + i) * 3 + c] = (cw[c][i >> 2] >> (8 * (i & 3))) & 0xFF;
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------ compute warps
+  const int NQ16 = p.SWPN >> 4;
+  const int citems = 2 * CH * NQ16;
+  const int cstep_q = kComputeThreads % NQ16, cstep_r = kComputeThreads / NQ16;
+  const uint32_t rgb_s = smem_u32(rgb);
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t lut_s = smem_u32(lut);
+  // V-pass role: row group vjg, planes {2 vsub, 2 vsub + 1}
+  const int vjg = warp & 3, vsub = warp >> 2;
+  const int j0 = 8 * vjg + 2 * tq;                 // output rows j0, j0+1 of the band
+  const bool jok0 = j0 < 28, jok1 = j0 + 1 < 28;   // group 3 covers rows 24..31
+  const bool xok1 = g < 6;                         // second column g+8 inside the 14-wide patch
+  // token offset of (row j, patch column 0) within a band's token block (R6):
+  // row part hm*2*1176 + ph*14
+  const int jo0 = (j0 / 14) * 2 * kCols + (j0 % 14) * 14;
+
+  uint32_t seq = 0;
+  int cur = i0;
+  Run r;
+  while (next_run(p, cur, i1, r)) {
+    const int X0 = r.strip * p.sw;
+    const int SX0 = __ldg(p.hx + X0) & ~15;
+    const int npatch = min(p.sw / 14, (p.W2 - X0) / 14);  // valid patches in this strip
+    const bool hact = warp < p.htiles;
+    // H-pass B fragments of this warp's output tile (constant over the strip)
+    const int htile = r.strip * p.htiles + min(warp, p.htiles - 1);
+    uint32_t hb[KSH][3][2];
+    {
+      const uint32_t* f = p.hfr + static_cast<size_t>(htile) * KSH * 3 * 64 + lane * 2;
+#pragma unroll
+      for (int k = 0; k < KSH; ++k)
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl) {
+          hb[k][pl][0] = __ldg(f + (k * 3 + pl) * 64);
+          hb[k][pl][1] = __ldg(f + (k * 3 + pl) * 64 + 1);
+        }
+    }
+    // A-fragment byte addresses in an RGB plane: rows g, g+8; columns xs + 4t (+16)
+    const uint32_t hA0 = rgb_s + g * SWP + (hact ? __ldg(p.hxs + htile) - SX0 : 0) + 4 * tq;
+    const uint32_t hA1 = hA0 + 8 * SWP;
+    // ring columns of this thread's outputs (2t, 2t+1 of the tile); masked past the strip / frame
+    const int ho = warp * kTileN + 2 * tq;
+    const bool hst0 = hact && ho < p.sw && X0 + ho < p.W2;
+    const bool hst1 = hact && ho + 1 < p.sw && X0 + ho + 1 < p.W2;
+
+    int next_k = r.kfirst;
+    // ring words of source rows kfirst*16 + g and + g + 8 (advanced per chunk)
+    int hwA = ((r.kfirst * CH) / 4 + (g >> 2)) % p.TRW;
+    int hwB = ((r.kfirst * CH) / 4 + 2 + (g >> 2)) % p.TRW;
+    for (int hb_ = r.hb0; hb_ < r.hb1; ++hb_) {
+      const int yo0 = hb_ * 28;
+      const int kneed = min(p.nchunks, (__ldg(p.vx + yo0 + 27) + __ldg(p.vcnt + yo0 + 27) + CH - 1) / CH);
+      for (; next_k < kneed; ++next_k, ++seq) {
+        const int k = next_k;
+        const int buf = seq % kStages;
+        const uint8_t* rawb = raw + buf * 2 * RAWF;
+        mbar_wait(&full[buf], (seq / kStages) & 1);
+        // ---- a5: NV12 -> RGB planes, 16 pixels per item
+        {
+          int q = tid % NQ16, rowi = tid / NQ16;  // rowi = f*CH + rr
+          for (int it = (p.skip & 1) ? citems : tid; it < citems; it += kComputeThreads) {
+            const int f = rowi >= CH, rr = rowi - f * CH;
+            const int xb = 16 * q, sub = xb / p.BW, xo = xb - sub * p.BW;
+            const uint8_t* fb = rawb + f * RAWF;
+            const uint4 Yv = *reinterpret_cast<const uint4*>(fb + (sub * 16 + rr) * p.BW + xo);
+            const uint4 UVv = *reinterpret_cast<const uint4*>(fb + 16 * p.BW * p.NX + (sub * 8 + (rr >> 1)) * p.BW + xo);
+            uint4 Rv, Gv, Bv;
+            bt601_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x);
+            bt601_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y);
+            bt601_4(Yv.z, UVv.z, Rv.z, Gv.z, Bv.z);
+            bt601_4(Yv.w, UVv.w, Rv.w, Gv.w, Bv.w);
+            uint8_t* dst = rgb + ((f * 3) * CH + rr) * SWP + 16 * q;
+            *reinterpret_cast<uint4*>(dst) = Rv;
+            *reinterpret_cast<uint4*>(dst + CH * SWP) = Gv;
+            *reinterpret_cast<uint4*>(dst + 2 * CH * SWP) = Bv;
+            if (p.dbg_src != nullptr) {
+              const int y = k * CH + rr, x = SX0 + 16 * q;
+              if (y < p.H) {
+                const uint32_t cw[3][4] = {{Rv.x, Rv.y, Rv.z, Rv.w}, {Gv.x, Gv.y, Gv.z, Gv.w}, {Bv.x, Bv.y, Bv.z, Bv.w}};
+                const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
+                for (int i = 0; i < 16 && x + i < p.W; ++i)
+                  for (int c = 0; c < 3; ++c)
+                    p.dbg_src[((fi * p.H + y) * p.W + x + i) * 3 + c] = (cw[c][i >> 2] >> (8 * (i & 3))) & 0xFF;
+              }
+            }
+            q += cstep_q;
+            rowi += cstep_r;
+            if (q >= NQ16) {
+              q -= NQ16;
+              ++rowi;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done reading the raw buffer
+        bar_sync(1, kComputeThreads);              // RGB planes complete
+        // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of 3 for ILP
+        if (hact && !(p.skip & 2)) {
+          const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + (g & 3);
+          const uint32_t dB = ring_s + (hwB * RS + ho) * 4 + (g & 3);
+          constexpr int HG = KSH == 1 ? 3 : 2;  // planes interleaved per group (ILP vs registers)
+#pragma unroll
+          for (int fg = 0; fg < 6; fg += HG) {
+            uint32_t a[HG][KSH][4];
+#pragma unroll
+            for (int e = 0; e < HG; ++e)
+#pragma unroll
+              for (int kk = 0; kk < KSH; ++kk) {
+                const uint32_t po = (fg + e) * CH * SWP + 32 * kk;
+                a[e][kk][0] = lds32(hA0 + po);
+                a[e][kk][1] = lds32(hA1 + po);
+                a[e][kk][2] = lds32(hA0 + po + 16);
+                a[e][kk][3] = lds32(hA1 + po + 16);
+              }
+            int d2[HG][4], d1[HG][4], d0[HG][4];
+#pragma unroll
+            for (int e = 0; e < HG; ++e) fir_mma_planes<KSH>(d2[e], d1[e], d0[e], a[e], hb);
+#pragma unroll
+            for (int e = 0; e < HG; ++e) {
+              // clip8 (R4): d0,d1 = row g, columns ho, ho+1; d2,d3 = row g+8
+              const uint32_t off = (fg + e) * SW * 4;
+              uint32_t q[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                q[i] = static_cast<uint32_t>(add_min_relu(combine_planes(d2[e][i], d1[e][i], d0[e][i]), 0,
+                                                          (1 << 30) - 1)) >> 22;
+              if (hst0) {
+                sts8(dA + off, q[0]);
+                sts8(dB + off, q[2]);
+              }
+              if (hst1) {
+                sts8(dA + off + 4, q[1]);
+                sts8(dB + off + 4, q[3]);
+              }
+            }
+          }
+        }
+        // advance this thread's two ring rows by one chunk (4 words), wrapping
+        hwA += 4;
+        hwA -= hwA >= p.TRW ? p.TRW : 0;
+        hwB += 4;
+        hwB -= hwB >= p.TRW ? p.TRW : 0;
+        bar_sync(1, kComputeThreads);  // ring rows complete, RGB planes free
+      }
+      // ---- a7 + a8 + a9: vertical pass (MMA), normalise, patchify
+      if (!(p.skip & 4)) {
+        const int grp = hb_ * 4 + vjg;
+        uint32_t vb[KSV][3][2];
+        const uint32_t* f = p.vfr + static_cast<size_t>(grp) * KSV * 3 * 64 + lane * 2;
+#pragma unroll
+        for (int kk = 0; kk < KSV; ++kk)
+#pragma unroll
+          for (int pl = 0; pl < 3; ++pl) {
+            vb[kk][pl][0] = __ldg(f + (kk * 3 + pl) * 64);
+            vb[kk][pl][1] = __ldg(f + (kk * 3 + pl) * 64 + 1);
+          }
+        const int ys = __ldg(p.vys + grp);
+        // A rows: columns (g, g+8) of a patch; k = source rows ys + 32kk + 4t (+16)
+        uint32_t rb[KSV][2];
+#pragma unroll
+        for (int kk = 0; kk < KSV; ++kk) {
+          rb[kk][0] = ring_s + ((((ys >> 2) + 8 * kk + tq) % p.TRW) * RS + 2 * vsub * SW + g) * 4;
+          rb[kk][1] = ring_s + ((((ys >> 2) + 8 * kk + 4 + tq) % p.TRW) * RS + 2 * vsub * SW + g) * 4;
+        }
+        // token block of this (pair, band, strip); patch q of the strip starts at
+        // column offset (X0 + 14 q): merge block wb = (X0/28) + q/2, sub-block wm = q&1
+        float* tb = p.tokens + ((static_cast<size_t>(r.pair) * p.gh2 + hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + g;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int fc = 2 * vsub + e, f = fc / 3, c = fc - 3 * (fc / 3);
+          const uint32_t lutc = lut_s + c * 1024;
+          float* tp = tb + (c * 2 + f) * 196;
+          constexpr int VG = KSV == 1 ? 2 : 1;  // patches interleaved per group
+#pragma unroll
+          for (int q0 = 0; q0 < 6; q0 += VG) {
+            if (q0 >= npatch) break;
+            uint32_t a[VG][KSV][4];
+#pragma unroll
+            for (int e2 = 0; e2 < VG; ++e2)
+#pragma unroll
+              for (int kk = 0; kk < KSV; ++kk) {
+                const uint32_t co = (e * SW + 14 * (q0 + e2)) * 4;
+                a[e2][kk][0] = lds32(rb[kk][0] + co);
+                a[e2][kk][1] = lds32(rb[kk][0] + co + 32);
+                a[e2][kk][2] = lds32(rb[kk][1] + co);
+                a[e2][kk][3] = lds32(rb[kk][1] + co + 32);
+              }
+            int d2[VG][4], d1[VG][4], d0[VG][4];
+#pragma unroll
+            for (int e2 = 0; e2 < VG; ++e2) fir_mma_planes<KSV>(d2[e2], d1[e2], d0[e2], a[e2], vb);
+#pragma unroll
+            for (int e2 = 0; e2 < VG; ++e2) {
+              const int q = q0 + e2;
+              if (q >= npatch) break;
+              // d0,d1: column g, rows j0, j0+1; d2,d3: column g+8
+              uint32_t sv[4];
+              float o[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                sv[i] = static_cast<uint32_t>(
+                    add_min_relu(combine_planes(d2[e2][i], d1[e2][i], d0[e2][i]), 0, (1 << 30) - 1));
+                o[i] = ldsf(lutc + ((sv[i] >> 20) & 0x3FCu));
+              }
+              float* op = tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
+              if (jok0) __stcs(op, o[0]);
+              if (jok1) __stcs(op + 14, o[1]);
+              if (xok1) {
+                if (jok0) __stcs(op + 8, o[2]);
+                if (jok1) __stcs(op + 22, o[3]);
+              }
+              if (p.dbg_rs != nullptr) {
+                const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
+                for (int ee = 0; ee < 4; ++ee) {
+                  const int x = X0 + 14 * q + g + ((ee >= 2) ? 8 : 0), j = j0 + (ee & 1);
+                  if ((ee < 2 || xok1) && x < p.W2 && j < 28)
+                    p.dbg_rs[((fi * p.H2 + yo0 + j) * p.W2 + x) * 3 + c] = sv[ee] >> 22;
+                }
+              }
+            }
           }
         }
       }
-      __syncthreads();
-      // ---- a6: horizontal pass -> ring (4 rows packed per word, column-major)
-      if (hact) {
-        const int wbase = ((r0 >> 2) % p.TRW);
-#pragma unroll 1
-        for (int g = 0; g < CH / 4; ++g) {
-          int qa[4], qb[4];
-#pragma unroll
-          for (int rr = 0; rr < 4; ++rr) {
-            const int row = 4 * g + rr;
-            const uint32_t* s0 = reinterpret_cast<const uint32_t*>(hsrc0 + row * p.SWP);
-            const uint32_t* s1 = reinterpret_cast<const uint32_t*>(hsrc1 + row * p.SWP);
-            uint32_t a[NW + 1], b[NW + 1], da[NW], db[NW];
-#pragma unroll
-            for (int i = 0; i <= NW; ++i) {
-              a[i] = s0[i];
-              b[i] = s1[i];
-            }
-#pragma unroll
-            for (int i = 0; i < NW; ++i) {
-              da[i] = __funnelshift_r(a[i], a[i + 1], hsh);
-              db[i] = __funnelshift_r(b[i], b[i + 1], hsh);
-            }
-            qa[rr] = fir_sum<NW>(da, hw0, hw1, hw2) >> 22;  // clip8 = saturating pack below
-            qb[rr] = fir_sum<NW>(db, hw0, hw1, hw2) >> 22;
-          }
-          const uint32_t word0 = pack_sat_u8(qa[1], qa[0], pack_sat_u8(qa[3], qa[2], 0));
-          const uint32_t word1 = pack_sat_u8(qb[1], qb[0], pack_sat_u8(qb[3], qb[2], 0));
-          int w = wbase + g;
-          if (w >= p.TRW) w -= p.TRW;
-          hdst0[w] = word0;
-          hdst1[w] = word1;
-        }
-      }
-      __syncthreads();
+      bar_sync(1, kComputeThreads);  // ring may be overwritten by the next chunks
     }
-    // ---- vertical tables of this band's 28 output rows -> smem
-    for (int i = tid; i < 28 * VWS; i += NT) {
-      const int j = i / VWS, kk = i - j * VWS;
-      const int yo = yo0 + j;
-      vws[i] = (kk == 0) ? static_cast<uint32_t>(__ldg(p.vx + yo) % p.TR)
-                         : __ldg(p.vw + static_cast<size_t>(yo) * 3 * NW + (kk - 1));
-    }
-    __syncthreads();
-    // ---- a7 + a8 + a9: vertical pass, normalise, patchify (float2 stores)
-    if (vact) {
-      const size_t trow = (static_cast<size_t>(pair) * p.gh2 + hb) * p.gw2 * 4 + vwb * 4 + vjh * 2 + vwm;
-      float* out0 = p.tokens + trow * kCols + (vc * 2 + 0) * 196 + vpw;
-      float* out1 = out0 + 196;
-#pragma unroll 1
-      for (int jj = 0; jj < 14; ++jj) {
-        const int j = vjh * 14 + jj;
-        const uint32_t* vj = vws + j * VWS;
-        const int ypos = static_cast<int>(vj[0]);
-        const int vsh = (ypos & 3) * 8;
-        uint32_t v0[NW], v1[NW], v2[NW];
-#pragma unroll
-        for (int i = 0; i < NW; ++i) {
-          v0[i] = vj[1 + i];
-          v1[i] = vj[1 + NW + i];
-          v2[i] = vj[1 + 2 * NW + i];
-        }
-        int widx[NW + 1];
-#pragma unroll
-        for (int i = 0; i <= NW; ++i) {
-          const int t = (ypos >> 2) + i;
-          widx[i] = t >= p.TRW ? t - p.TRW : t;
-        }
-        uint32_t a0[NW + 1], a1[NW + 1], b0[NW + 1], b1[NW + 1];
-#pragma unroll
-        for (int i = 0; i <= NW; ++i) {
-          a0[i] = vcol00[widx[i]];
-          a1[i] = vcol01[widx[i]];
-          b0[i] = vcol10[widx[i]];
-          b1[i] = vcol11[widx[i]];
-        }
-        uint32_t da0[NW], da1[NW], db0[NW], db1[NW];
-#pragma unroll
-        for (int i = 0; i < NW; ++i) {
-          da0[i] = __funnelshift_r(a0[i], a0[i + 1], vsh);
-          da1[i] = __funnelshift_r(a1[i], a1[i + 1], vsh);
-          db0[i] = __funnelshift_r(b0[i], b0[i + 1], vsh);
-          db1[i] = __funnelshift_r(b1[i], b1[i + 1], vsh);
-        }
-        // clip8 then table index: clamp S to [0, 2^30-1], byte = S >> 22
-        const uint32_t s00 = static_cast<uint32_t>(add_min_relu(fir_sum<NW>(da0, v0, v1, v2), 0, (1 << 30) - 1));
-        const uint32_t s01 = static_cast<uint32_t>(add_min_relu(fir_sum<NW>(da1, v0, v1, v2), 0, (1 << 30) - 1));
-        const uint32_t s10 = static_cast<uint32_t>(add_min_relu(fir_sum<NW>(db0, v0, v1, v2), 0, (1 << 30) - 1));
-        const uint32_t s11 = static_cast<uint32_t>(add_min_relu(fir_sum<NW>(db1, v0, v1, v2), 0, (1 << 30) - 1));
-        float o00, o01, o10, o11;
-        asm("ld.shared.f32 %0, [%1];" : "=f"(o00) : "r"(((s00 >> 20) & 0x3FCu) + lutb));
-        asm("ld.shared.f32 %0, [%1];" : "=f"(o01) : "r"(((s01 >> 20) & 0x3FCu) + lutb));
-        asm("ld.shared.f32 %0, [%1];" : "=f"(o10) : "r"(((s10 >> 20) & 0x3FCu) + lutb));
-        asm("ld.shared.f32 %0, [%1];" : "=f"(o11) : "r"(((s11 >> 20) & 0x3FCu) + lutb));
-        st_cs_f2(out0 + jj * 14, o00, o01);
-        st_cs_f2(out1 + jj * 14, o10, o11);
-        if (p.dbg_rs != nullptr) {
-          const size_t fi0 = static_cast<size_t>(p.frame_base + 2 * pair);
-          const int yo = yo0 + j;
-          uint8_t* d0 = p.dbg_rs + ((fi0 * p.H2 + yo) * p.W2 + gx) * 3 + vc;
-          uint8_t* d1 = d0 + static_cast<size_t>(p.H2) * p.W2 * 3;
-          d0[0] = s00 >> 22;
-          d0[3] = s01 >> 22;
-          d1[0] = s10 >> 22;
-          d1[3] = s11 >> 22;
-        }
-      }
-    }
-    __syncthreads();
   }
 }
 
 // ------------------------------------------------------------------ host side
-static const int kNW[] = {1, 2, 3, 4, 6, 8, 12, 16};
-
-static int pick_nw(int words) {
-  for (int w : kNW)
-    if (w >= words) return w;
-  return -1;
-}
-
 using KernelFn = void (*)(Params);
 
-template <int NW, int K>
-static KernelFn kfn() {
-  return fc_fused_kernel<NW, K>;
-}
+// Instances: k-steps (32 source pixels each) of the H-pass and V-pass MMA
+// windows.  8 consecutive outputs need KS*32 >= span + 3 (4-byte alignment).
+#define FC_INSTANCES(X) \
+  X(1, 1) X(1, 2) X(2, 1) X(2, 2) X(2, 3) X(3, 2) X(3, 3) X(4, 2) X(4, 3) X(4, 4) X(1, 3) X(3, 1) X(1, 4) X(4, 1) X(2, 4) X(3, 4)
 
-static KernelFn select_kernel(int nw, int K) {
-#define FC_CASE(NWV)                                  \
-  case NWV:                                           \
-    return K == 4 ? kfn<NWV, 4>() : kfn<NWV, 2>();
-  switch (nw) {
-    FC_CASE(1)
-    FC_CASE(2)
-    FC_CASE(3)
-    FC_CASE(4)
-    FC_CASE(6)
-    FC_CASE(8)
-    FC_CASE(12)
-    FC_CASE(16)
-  }
-#undef FC_CASE
-  return nullptr;
-}
+struct Instance {
+  int ksh, ksv;
+  KernelFn fn;
+};
+#define FC_INST(A, B) {A, B, fc_fused_kernel<A, B>},
+static const Instance kInstances[] = {FC_INSTANCES(FC_INST)};
+#undef FC_INST
+constexpr int kMaxKS = 4;
 
 static fc_status cuda_fail(cudaError_t e, const char* what) {
   return fail(FC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-// Re-pack an axis table's byte planes to the kernel's word count.
-static std::vector<uint32_t> planes_for(const AxisTable& t, int nw) {
-  std::vector<uint32_t> out(static_cast<size_t>(t.out) * 3 * nw, 0u);
-  for (int o = 0; o < t.out; ++o)
-    for (int pl = 0; pl < 3; ++pl)
-      for (int i = 0; i < t.words; ++i)
-        out[(static_cast<size_t>(o) * 3 + pl) * nw + i] = t.planes[(static_cast<size_t>(o) * 3 + pl) * t.words + i];
-  return out;
 }
 
 template <typename T>
@@ -378,99 +430,204 @@ static cudaError_t upload(T** dst, const std::vector<T>& v) {
   return cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
 }
 
-static int plan_nw(const fc_plan_s* P) { return pick_nw(std::max(P->th.words, P->tv.words)); }
+// Integer Pillow weight of output o at source index src (0 outside the window).
+static int32_t weight_at(const AxisTable& t, int o, int src) {
+  if (o < 0 || o >= t.out) return 0;
+  const int tap = src - t.xmin[o];
+  if (tap < 0 || tap >= t.cnt[o]) return 0;
+  return t.iw[static_cast<size_t>(o) * t.ksize + tap];
+}
+static uint32_t weight_byte(int32_t w, int plane) {
+  return plane == 2 ? static_cast<uint32_t>(w >> 16) & 0xFFu : (static_cast<uint32_t>(w) >> (8 * plane)) & 0xFFu;
+}
 
-// Process-wide cache of uploaded tables, keyed by everything the tables are
-// a function of (device, W->W', H->H', packing width, normalisation).  Plans
-// of equally shaped requests share one upload, so fc_plan + fc_preprocess
-// never touch the device synchronously after the first request of a shape.
-struct TableKey {
-  int dev, w, w2, h, h2, nw;
-  uint32_t lut_bits[768];
-  bool operator<(const TableKey& o) const {
-    return std::memcmp(this, &o, sizeof(TableKey)) < 0;
+// B fragments of m16n8k32 for a group of 8 outputs (H: 8 columns; V: 8 rows of
+// a band) whose windows start at source index xs: b_r (r = 0,1) of lane
+// (g = lane/4, t = lane%4) holds k = ks*32 + 16 r + 4 t + [0..3] of output g.
+static void frag_group(const AxisTable& t, const int (&outs)[8], int xs, int KS, uint32_t* dst) {
+  for (int ks = 0; ks < KS; ++ks)
+    for (int pl = 0; pl < 3; ++pl)
+      for (int lane = 0; lane < 32; ++lane)
+        for (int rr = 0; rr < 2; ++rr) {
+          const int g = lane >> 2, tq = lane & 3;
+          uint32_t word = 0;
+          for (int bb = 0; bb < 4; ++bb) {
+            const int k = ks * 32 + 16 * rr + 4 * tq + bb;
+            word |= weight_byte(weight_at(t, outs[g], xs + k), pl) << (8 * bb);
+          }
+          dst[((ks * 3 + pl) * 32 + lane) * 2 + rr] = word;
+        }
+}
+
+// Span (in k) that a group of outputs needs from its 4-aligned start.
+static int group_ks(const AxisTable& t, const int (&outs)[8], int xs) {
+  int end = xs;
+  for (int g = 0; g < 8; ++g)
+    if (outs[g] >= 0 && outs[g] < t.out) end = std::max(end, t.xmin[outs[g]] + t.cnt[outs[g]]);
+  return (end - xs + 31) / 32;
+}
+
+struct MmaTables {
+  int ksh = 1, ksv = 1;
+  std::vector<int32_t> hxs, vys;
+  std::vector<uint32_t> hfr, vfr;
+};
+
+// H: per strip of 84 columns, 11 tiles of 8 consecutive output columns (the
+// last tile's columns 84..87 belong to the next strip and carry no weights);
+// V: per band, 4 groups of 8 output rows (rows 28hb + 8gi + [0..8), those past
+// the band's 28 rows carry no weights).
+static void build_mma_tables(const fc_plan_s* P, int sw, MmaTables* m) {
+  const AxisTable& th = P->th;
+  const AxisTable& tv = P->tv;
+  const int nstrips = (th.out + sw - 1) / sw;
+  const int htiles = (sw + 7) / 8;
+  const int nth = nstrips * htiles;
+  const int gh2 = tv.out / 28;
+  m->hxs.resize(nth);
+  m->vys.resize(gh2 * 4);
+  auto h_outs = [&](int tt, int (&outs)[8]) {
+    const int s = tt / htiles, i = tt % htiles;
+    for (int g = 0; g < 8; ++g) {
+      const int o = s * sw + 8 * i + g;
+      outs[g] = (8 * i + g < sw && o < th.out) ? o : -1;
+    }
+  };
+  auto v_outs = [&](int grp, int (&outs)[8]) {
+    const int hb = grp / 4, gi = grp % 4;
+    for (int g = 0; g < 8; ++g) outs[g] = (8 * gi + g < 28) ? 28 * hb + 8 * gi + g : -1;
+  };
+  int ksh = 1, ksv = 1;
+  for (int tt = 0; tt < nth; ++tt) {
+    int outs[8];
+    h_outs(tt, outs);
+    const int first = std::min(tt / htiles * sw + 8 * (tt % htiles), th.out - 1);
+    m->hxs[tt] = th.xmin[first] & ~3;
+    ksh = std::max(ksh, group_ks(th, outs, m->hxs[tt]));
   }
+  for (int grp = 0; grp < gh2 * 4; ++grp) {
+    int outs[8];
+    v_outs(grp, outs);
+    m->vys[grp] = tv.xmin[28 * (grp / 4) + 8 * (grp % 4)] & ~3;
+    ksv = std::max(ksv, group_ks(tv, outs, m->vys[grp]));
+  }
+  m->ksh = ksh;
+  m->ksv = ksv;
+  m->hfr.assign(static_cast<size_t>(nth) * ksh * 3 * 64, 0u);
+  m->vfr.assign(static_cast<size_t>(gh2) * 4 * ksv * 3 * 64, 0u);
+  for (int tt = 0; tt < nth; ++tt) {
+    int outs[8];
+    h_outs(tt, outs);
+    frag_group(th, outs, m->hxs[tt], ksh, &m->hfr[static_cast<size_t>(tt) * ksh * 3 * 64]);
+  }
+  for (int grp = 0; grp < gh2 * 4; ++grp) {
+    int outs[8];
+    v_outs(grp, outs);
+    frag_group(tv, outs, m->vys[grp], ksv, &m->vfr[static_cast<size_t>(grp) * ksv * 3 * 64]);
+  }
+}
+
+// Process-wide cache of uploaded tables, keyed by everything the tables are a
+// function of (device, W->W', H->H', normalisation).  Plans of equally shaped
+// requests share one upload, so fc_plan + fc_preprocess never touch the device
+// synchronously after the first request of a shape.
+struct TableKey {
+  int dev, sw, w, w2, h, h2;
+  uint32_t lut_bits[768];
+  bool operator<(const TableKey& o) const { return std::memcmp(this, &o, sizeof(TableKey)) < 0; }
 };
 
 static std::mutex g_tables_mu;
 static std::map<TableKey, DeviceTables>* g_tables = new std::map<TableKey, DeviceTables>();  // never freed
 
-static fc_status device_tables(fc_plan_s* P, int dev, DeviceTables** out) {
+static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out) {
   std::lock_guard<std::mutex> lk(P->mu);
-  auto it = P->dev.find(dev);
+  const int pkey = dev * 1024 + sw;
+  auto it = P->dev.find(pkey);
   if (it != P->dev.end()) {
     *out = &it->second;
     return FC_OK;
   }
-  const int nw = plan_nw(P);
   TableKey key;
   std::memset(&key, 0, sizeof(key));
   key.dev = dev;
+  key.sw = sw;
   key.w = P->th.in;
   key.w2 = P->th.out;
   key.h = P->tv.in;
   key.h2 = P->tv.out;
-  key.nw = nw;
   std::memcpy(key.lut_bits, P->lut.data(), sizeof(key.lut_bits));
   std::lock_guard<std::mutex> gk(g_tables_mu);
   auto git = g_tables->find(key);
   if (git != g_tables->end()) {
-    *out = &(P->dev[dev] = git->second);
+    *out = &(P->dev[pkey] = git->second);
     return FC_OK;
   }
+  MmaTables m;
+  build_mma_tables(P, sw, &m);
+  if (m.ksh > kMaxKS || m.ksv > kMaxKS)
+    return fail(FC_ERR_UNSUPPORTED, "resize window wider than 128 source pixels per 8 outputs");
   DeviceTables t;
+  t.ksh = m.ksh;
+  t.ksv = m.ksv;
   cudaError_t e = cudaSuccess;
   if (e == cudaSuccess) e = upload(&t.hx, P->th.xmin);
-  if (e == cudaSuccess) e = upload(&t.hcnt, P->th.cnt);
-  if (e == cudaSuccess) e = upload(&t.hw, planes_for(P->th, nw));
+  if (e == cudaSuccess) e = upload(&t.hxs, m.hxs);
+  if (e == cudaSuccess) e = upload(&t.hfr, m.hfr);
   if (e == cudaSuccess) e = upload(&t.vx, P->tv.xmin);
   if (e == cudaSuccess) e = upload(&t.vcnt, P->tv.cnt);
-  if (e == cudaSuccess) e = upload(&t.vw, planes_for(P->tv, nw));
+  if (e == cudaSuccess) e = upload(&t.vys, m.vys);
+  if (e == cudaSuccess) e = upload(&t.vfr, m.vfr);
   if (e == cudaSuccess) e = upload(&t.lut, P->lut);
   if (e != cudaSuccess) {
-    cudaFree(t.hx); cudaFree(t.hcnt); cudaFree(t.hw); cudaFree(t.vx); cudaFree(t.vcnt); cudaFree(t.vw);
-    cudaFree(t.lut);
+    cudaFree(t.hx); cudaFree(t.hxs); cudaFree(t.hfr); cudaFree(t.vx); cudaFree(t.vcnt); cudaFree(t.vys);
+    cudaFree(t.vfr); cudaFree(t.lut);
     return e == cudaErrorMemoryAllocation ? fail(FC_ERR_OOM, "table upload: out of device memory")
                                           : cuda_fail(e, "table upload");
   }
   (*g_tables)[key] = t;
-  *out = &(P->dev[dev] = t);
+  *out = &(P->dev[pkey] = t);
   return FC_OK;
 }
 
 struct Geometry {
-  int K, nw, SWP, TR, TRW, TRS, nstrips, nchunks;
+  int sw, htiles, SWPN, SWP, BW, NX, TR, TRW, nstrips, nchunks;
+  KernelFn fn;
   size_t smem;
 };
 
-static size_t smem_bytes(int K, int nw, int SWP, int TRS) {
-  const int SW = 28 * K;
-  return 3072 + 16 + ((28 * (1 + 3 * nw) * 4 + 15) & ~15) + static_cast<size_t>(2) * 48 * SWP +
-         static_cast<size_t>(6) * kChunkRows * SWP + static_cast<size_t>(6) * SW * TRS * 4;
+static size_t smem_bytes(int SWP, int RAWW, int TRW) {
+  return 3072 + 128 + static_cast<size_t>(kStages) * 48 * RAWW + static_cast<size_t>(6) * kChunkRows * SWP +
+         static_cast<size_t>(TRW) * kRingStride * 4;
 }
 
-static bool geometry(const fc_plan_s* P, int K, Geometry* g) {
-  const int SW = 28 * K;
-  const int nw = plan_nw(P);
-  if (nw < 0) return false;
+static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int sw, int max_smem, Geometry* g) {
+  const int SW = sw;
+  g->sw = sw;
+  g->htiles = (sw + 7) / 8;
   const auto& th = P->th;
   const auto& tv = P->tv;
-  int swp = 16;
   const int nstrips = (P->w2 + SW - 1) / SW;
+  // source window per strip: every MMA tile's 32*KSH bytes from its start, and
+  // every tap of every output
+  int need = 16;
   for (int s = 0; s < nstrips; ++s) {
     const int X0 = s * SW, X1 = std::min(X0 + SW, P->w2);
     const int SX0 = th.xmin[X0] & ~15;
-    int need = 0;
-    for (int o = X0; o < X1; ++o) {
-      const int off = th.xmin[o] - SX0;
-      need = std::max(need, (off & ~3) + 4 * (nw + 1));
-      need = std::max(need, th.xmin[o] + th.cnt[o] - SX0);
-    }
-    swp = std::max(swp, (need + 15) & ~15);
+    for (int i = 0; i < g->htiles && X0 + 8 * i < X1; ++i)
+      need = std::max(need, (th.xmin[X0 + 8 * i] & ~3) - SX0 + 32 * dt->ksh);
+    for (int o = X0; o < X1; ++o) need = std::max(need, th.xmin[o] + th.cnt[o] - SX0);
   }
-  // ring: after the chunks a band needs (16-row granularity) the ring must
-  // still hold the band's first source row
-  int tr = 4 * (nw + 1);
+  // round to an odd multiple of 16 (bank-conflict-free MMA A-fragment loads)
+  int swp = (need + 15) / 16;
+  if (!(swp & 1)) ++swp;
+  g->SWPN = ((need + 15) / 16) * 16;
+  g->SWP = swp * 16;
+  g->NX = (g->SWPN + 255) / 256;                       // TMA boxes are at most 256 wide
+  g->BW = ((g->SWPN / g->NX + 15) / 16) * 16;
+  // ring depth: after the chunks a band needs (16-row granularity) the ring
+  // must still hold the first row of the band's MMA windows
+  int tr = 32 * dt->ksv + 16;
   int kmax = 0;
   for (int hb = 0; hb < P->h2 / 28; ++hb) {
     const int ylo = tv.xmin[hb * 28] & ~3;
@@ -479,27 +636,79 @@ static bool geometry(const fc_plan_s* P, int K, Geometry* g) {
     tr = std::max(tr, kneed * kChunkRows - ylo);
     kmax = std::max(kmax, kneed);
   }
-  tr = (tr + 3) & ~3;
-  g->K = K;
-  g->nw = nw;
-  g->SWP = swp;
-  g->TR = tr;
-  g->TRW = tr / 4;
-  g->TRS = (g->TRW & 1) ? g->TRW : g->TRW + 1;
+  g->TR = (tr + 3) & ~3;
+  g->TRW = g->TR / 4;
   g->nstrips = nstrips;
   g->nchunks = std::min(kmax, (P->meta.height + kChunkRows - 1) / kChunkRows);
-  g->smem = smem_bytes(K, nw, swp, g->TRS);
-  return true;
+  g->fn = nullptr;
+  for (const Instance& in : kInstances)
+    if (in.ksh == dt->ksh && in.ksv == dt->ksv) g->fn = in.fn;
+  if (!g->fn) return fail(FC_ERR_UNSUPPORTED, "no kernel instance for this resize window");
+  g->smem = smem_bytes(g->SWP, g->BW * g->NX, g->TRW);
+  if (g->smem > static_cast<size_t>(max_smem))
+    return fail(FC_ERR_UNSUPPORTED, "working set exceeds shared memory (resize window too wide)");
+  return FC_OK;
 }
 
-static fc_status choose_geometry(const fc_plan_s* P, int max_smem, Geometry* g) {
-  for (int K : {4, 2}) {
-    if (!geometry(P, K, g)) return fail(FC_ERR_UNSUPPORTED, "resize filter too wide");
-    // prefer K=4 only when two CTAs fit per SM
-    if (K == 4 && g->smem * 2 > static_cast<size_t>(max_smem)) continue;
-    if (g->smem <= static_cast<size_t>(max_smem)) return FC_OK;
+// ---- TMA tensor maps of the NV12 planes (host-encoded, cached per surface)
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<EncodeTiledFn>(nullptr);
+    return reinterpret_cast<EncodeTiledFn>(f);
+  }();
+  return fn;
+}
+
+struct MapKey {
+  uintptr_t ptr;
+  int64_t pitch, rows;
+  int bw, bh;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && pitch == o.pitch && rows == o.rows && bw == o.bw && bh == o.bh;
   }
-  return fail(FC_ERR_UNSUPPORTED, "working set exceeds shared memory (frame too wide for one strip)");
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    return std::hash<uintptr_t>()(k.ptr) ^ (std::hash<int64_t>()(k.pitch * 131 + k.rows) << 1) ^
+           (static_cast<size_t>(k.bw) << 20) ^ static_cast<size_t>(k.bh);
+  }
+};
+static std::mutex g_maps_mu;
+static std::unordered_map<MapKey, CUtensorMap, MapKeyHash>* g_maps =
+    new std::unordered_map<MapKey, CUtensorMap, MapKeyHash>();  // never freed
+
+// 2-D u8 tensor [rows][pitch] with a (bw x bh) box; out-of-bounds -> zeros.
+static fc_status tensor_map(const uint8_t* base, int64_t pitch, int64_t rows, int bw, int bh, CUtensorMap* out) {
+  const MapKey key{reinterpret_cast<uintptr_t>(base), pitch, rows, bw, bh};
+  std::lock_guard<std::mutex> lk(g_maps_mu);
+  auto it = g_maps->find(key);
+  if (it != g_maps->end()) {
+    *out = it->second;
+    return FC_OK;
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return fail(FC_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(pitch), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(pitch)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(bh)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUtensorMap m;
+  const CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(FC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+  if (g_maps->size() > (1u << 16)) g_maps->clear();
+  (*g_maps)[key] = m;
+  *out = m;
+  return FC_OK;
 }
 
 static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv12_surface* surfaces,
@@ -534,24 +743,33 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
-  int major = 0, max_smem = 0;
+  int major = 0, max_smem = 0, nsm = 0;
   cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   if (major != 10) return fail(FC_ERR_CUDA, "fc kernels are built for sm_100a only (no CPU/other-arch fallback)");
-  Geometry g;
-  fc_status st = choose_geometry(P, max_smem, &g);
-  if (st != FC_OK) return st;
+  // strips of 3 merge blocks; 1 merge block when a very wide resize window
+  // would not fit the working set in shared memory
   DeviceTables* dt = nullptr;
-  st = device_tables(P, dev, &dt);
+  Geometry g;
+  fc_status st = FC_OK;
+  for (int sw : {kStrip, 28}) {
+    st = device_tables(P, dev, sw, &dt);
+    if (st != FC_OK) return st;
+    st = choose_geometry(P, dt, sw, max_smem, &g);
+    if (st == FC_OK) break;
+  }
   if (st != FC_OK) return st;
-  KernelFn fn = select_kernel(g.nw, g.K);
-  if (!fn) return fail(FC_ERR_UNSUPPORTED, "no kernel instance for this filter width");
+  KernelFn fn = g.fn;
   e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(g.smem));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  int occ = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, g.smem);
+  if (e != cudaSuccess || occ < 1) return cuda_fail(e, "occupancy query");
 
-  static thread_local Params prm;  // ~30 KB: keep it off the stack
-  std::memset(&prm, 0, offsetof(Params, fr));
+  static thread_local Params prm;  // ~31 KB: keep it off the stack
+  std::memset(&prm, 0, offsetof(Params, tm));
   prm.W = W;
   prm.H = H;
   prm.W2 = P->w2;
@@ -559,18 +777,28 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
   prm.gh2 = static_cast<int>(P->gh / 2);
   prm.gw2 = static_cast<int>(P->gw / 2);
   prm.nstrips = g.nstrips;
+  prm.sw = g.sw;
+  prm.htiles = g.htiles;
   prm.SWP = g.SWP;
+  prm.SWPN = g.SWPN;
+  prm.BW = g.BW;
+  prm.NX = g.NX;
   prm.TR = g.TR;
   prm.TRW = g.TRW;
-  prm.TRS = g.TRS;
   prm.nchunks = g.nchunks;
   prm.hx = dt->hx;
-  prm.hw = dt->hw;
+  prm.hxs = dt->hxs;
+  prm.hfr = dt->hfr;
   prm.vx = dt->vx;
   prm.vcnt = dt->vcnt;
-  prm.vw = dt->vw;
+  prm.vys = dt->vys;
+  prm.vfr = dt->vfr;
   prm.lut = dt->lut;
   prm.dbg_src = dbg_src;
+  {
+    const char* sk = std::getenv("FC_PROFILE_SKIP");
+    prm.skip = sk ? std::atoi(sk) : 0;
+  }
   prm.dbg_rs = dbg_rs;
   const int64_t nf = static_cast<int64_t>(frames.size());
   const int64_t rows_per_pair = P->gh * P->gw;
@@ -582,10 +810,14 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
     prm.tokens = tokens + (f0 / 2) * rows_per_pair * kCols;
     for (int64_t i = 0; i < cnt; ++i) {
       const fc_nv12_surface& sf = surfaces[frames[f0 + i]];
-      prm.fr[i] = FrameDesc{sf.y, sf.uv, static_cast<int32_t>(sf.pitch_y), static_cast<int32_t>(sf.pitch_uv)};
+      st = tensor_map(sf.y, sf.pitch_y, H, g.BW, kChunkRows, &prm.tm[2 * i]);
+      if (st == FC_OK) st = tensor_map(sf.uv, sf.pitch_uv, H / 2, g.BW, kChunkRows / 2, &prm.tm[2 * i + 1]);
+      if (st != FC_OK) return st;
     }
-    dim3 grid(g.nstrips, static_cast<unsigned>(cnt / 2));
-    fn<<<grid, 84 * g.K, g.smem, s>>>(prm);
+    prm.npairs = static_cast<int>(cnt / 2);
+    const long long items = static_cast<long long>(prm.npairs) * g.nstrips * prm.gh2;
+    const int grid = static_cast<int>(std::min<long long>(items, static_cast<long long>(occ) * nsm));
+    fn<<<grid, kThreads, g.smem, s>>>(prm);
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   }
