@@ -221,6 +221,13 @@ __device__ __forceinline__ float ldsf(uint32_t addr) {
   return v;
 }
 
+// predicated streaming store (no branch)
+__device__ __forceinline__ void st_cs_pred(float* p, float v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.f32 [%0], %1;\n}" ::"l"(p), "f"(v),
+               "r"(static_cast<int>(pred))
+               : "memory");
+}
+
 __device__ __forceinline__ void st_cs_f2(float* p, float a, float b) {
   asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }

@@ -54,8 +54,9 @@ struct Params {
   int nstrips, npairs;
   int sw, htiles;      // strip width (84 or 28 output columns), H tiles per strip
   int SWP;            // RGB-plane row stride (odd multiple of 16)
-  int SWPN;           // source-window bytes needed per row
+  int SWPN;           // converted (and TMA-loaded) bytes per row: taps of the strip's outputs
   int BW, NX;         // TMA box width (<= 256) and boxes per row: NX*BW >= SWPN
+  int bwshift, bwmask;  // box index / offset of a byte column (NX == 1: 31 / ~0; else BW = 256: 8 / 255)
   int TR, TRW;        // ring rows / words
   int nchunks;        // chunks any band needs
   const int32_t* hx;    // H table: xmin per output column
@@ -151,6 +152,10 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
     fence_mbar_init();
   }
   for (int i = tid; i < 768; i += kThreads) lut[i] = __ldg(p.lut + i);
+  // bytes of the RGB planes past the converted width are only ever multiplied
+  // by zero weights (MMA read-ahead); keep them zero, never garbage
+  for (int i = tid; i < 6 * CH * SWP / 16; i += kThreads)
+    reinterpret_cast<uint4*>(rgb)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
 
   const int total = p.npairs * p.nstrips * p.gh2;
@@ -176,9 +181,20 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
   }
 
   // ------------------------------------------------------------ compute warps
+  // colour items (frame, row, 16-pixel group): at most 2 per thread; their
+  // offsets are launch constants (raw stage: Y / UV byte, RGB plane byte)
   const int NQ16 = p.SWPN >> 4;
   const int citems = 2 * CH * NQ16;
-  const int cstep_q = kComputeThreads % NQ16, cstep_r = kComputeThreads / NQ16;
+  int cy[2], cuv[2], crgb[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int it = tid + e * kComputeThreads;
+    const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
+    const int xb = 16 * q, sub = xb >> p.bwshift, xo = xb & p.bwmask;
+    cy[e] = f * RAWF + (sub * 16 + rr) * p.BW + xo;
+    cuv[e] = f * RAWF + 16 * p.BW * p.NX + (sub * 8 + (rr >> 1)) * p.BW + xo;
+    crgb[e] = ((f * 3) * CH + rr) * SWP + xb;
+  }
   const uint32_t rgb_s = smem_u32(rgb);
   const uint32_t ring_s = smem_u32(ring);
   const uint32_t lut_s = smem_u32(lut);
@@ -233,38 +249,30 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
         const uint8_t* rawb = raw + buf * 2 * RAWF;
         mbar_wait(&full[buf], (seq / kStages) & 1);
         // ---- a5: NV12 -> RGB planes, 16 pixels per item
-        {
-          int q = tid % NQ16, rowi = tid / NQ16;  // rowi = f*CH + rr
-          for (int it = (p.skip & 1) ? citems : tid; it < citems; it += kComputeThreads) {
-            const int f = rowi >= CH, rr = rowi - f * CH;
-            const int xb = 16 * q, sub = xb / p.BW, xo = xb - sub * p.BW;
-            const uint8_t* fb = rawb + f * RAWF;
-            const uint4 Yv = *reinterpret_cast<const uint4*>(fb + (sub * 16 + rr) * p.BW + xo);
-            const uint4 UVv = *reinterpret_cast<const uint4*>(fb + 16 * p.BW * p.NX + (sub * 8 + (rr >> 1)) * p.BW + xo);
-            uint4 Rv, Gv, Bv;
-            bt601_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x);
-            bt601_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y);
-            bt601_4(Yv.z, UVv.z, Rv.z, Gv.z, Bv.z);
-            bt601_4(Yv.w, UVv.w, Rv.w, Gv.w, Bv.w);
-            uint8_t* dst = rgb + ((f * 3) * CH + rr) * SWP + 16 * q;
-            *reinterpret_cast<uint4*>(dst) = Rv;
-            *reinterpret_cast<uint4*>(dst + CH * SWP) = Gv;
-            *reinterpret_cast<uint4*>(dst + 2 * CH * SWP) = Bv;
-            if (p.dbg_src != nullptr) {
-              const int y = k * CH + rr, x = SX0 + 16 * q;
-              if (y < p.H) {
-                const uint32_t cw[3][4] = {{Rv.x, Rv.y, Rv.z, Rv.w}, {Gv.x, Gv.y, Gv.z, Gv.w}, {Bv.x, Bv.y, Bv.z, Bv.w}};
-                const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
-                for (int i = 0; i < 16 && x + i < p.W; ++i)
-                  for (int c = 0; c < 3; ++c)
-                    p.dbg_src[((fi * p.H + y) * p.W + x + i) * 3 + c] = (cw[c][i >> 2] >> (8 * (i & 3))) & 0xFF;
-              }
-            }
-            q += cstep_q;
-            rowi += cstep_r;
-            if (q >= NQ16) {
-              q -= NQ16;
-              ++rowi;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (tid + e * kComputeThreads >= citems || (p.skip & 1)) break;
+          const uint4 Yv = *reinterpret_cast<const uint4*>(rawb + cy[e]);
+          const uint4 UVv = *reinterpret_cast<const uint4*>(rawb + cuv[e]);
+          uint4 Rv, Gv, Bv;
+          bt601_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x);
+          bt601_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y);
+          bt601_4(Yv.z, UVv.z, Rv.z, Gv.z, Bv.z);
+          bt601_4(Yv.w, UVv.w, Rv.w, Gv.w, Bv.w);
+          uint8_t* dst = rgb + crgb[e];
+          *reinterpret_cast<uint4*>(dst) = Rv;
+          *reinterpret_cast<uint4*>(dst + CH * SWP) = Gv;
+          *reinterpret_cast<uint4*>(dst + 2 * CH * SWP) = Bv;
+          if (p.dbg_src != nullptr) {
+            const int it = tid + e * kComputeThreads;
+            const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
+            const int y = k * CH + rr, x = SX0 + 16 * q;
+            if (y < p.H) {
+              const uint32_t cw[3][4] = {{Rv.x, Rv.y, Rv.z, Rv.w}, {Gv.x, Gv.y, Gv.z, Gv.w}, {Bv.x, Bv.y, Bv.z, Bv.w}};
+              const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
+              for (int i = 0; i < 16 && x + i < p.W; ++i)
+                for (int c = 0; c < 3; ++c)
+                  p.dbg_src[((fi * p.H + y) * p.W + x + i) * 3 + c] = (cw[c][i >> 2] >> (8 * (i & 3))) & 0xFF;
             }
           }
         }
@@ -334,19 +342,27 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
         const int ys = __ldg(p.vys + grp);
         // A rows: columns (g, g+8) of a patch; k = source rows ys + 32kk + 4t (+16)
         uint32_t rb[KSV][2];
+        {
+          int w = (ys >> 2) % p.TRW + tq;
 #pragma unroll
-        for (int kk = 0; kk < KSV; ++kk) {
-          rb[kk][0] = ring_s + ((((ys >> 2) + 8 * kk + tq) % p.TRW) * RS + 2 * vsub * SW + g) * 4;
-          rb[kk][1] = ring_s + ((((ys >> 2) + 8 * kk + 4 + tq) % p.TRW) * RS + 2 * vsub * SW + g) * 4;
+          for (int kk = 0; kk < KSV; ++kk) {
+            const int wa = w >= p.TRW ? w - p.TRW : w;
+            const int wb4 = wa + 4 >= p.TRW ? wa + 4 - p.TRW : wa + 4;
+            rb[kk][0] = ring_s + (wa * RS + 2 * vsub * SW + g) * 4;
+            rb[kk][1] = ring_s + (wb4 * RS + 2 * vsub * SW + g) * 4;
+            w = wa + 8;
+          }
         }
         // token block of this (pair, band, strip); patch q of the strip starts at
         // column offset (X0 + 14 q): merge block wb = (X0/28) + q/2, sub-block wm = q&1
         float* tb = p.tokens + ((static_cast<size_t>(r.pair) * p.gh2 + hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + g;
+        const int fc0 = 2 * vsub;
+        float* tpe[2] = {tb + ((fc0 % 3) * 2 + fc0 / 3) * 196, tb + (((fc0 + 1) % 3) * 2 + (fc0 + 1) / 3) * 196};
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int fc = 2 * vsub + e, f = fc / 3, c = fc - 3 * (fc / 3);
+          const int fc = fc0 + e, f = fc / 3, c = fc - 3 * (fc / 3);
           const uint32_t lutc = lut_s + c * 1024;
-          float* tp = tb + (c * 2 + f) * 196;
+          float* tp = tpe[e];
           constexpr int VG = KSV == 1 ? 2 : 1;  // patches interleaved per group
 #pragma unroll
           for (int q0 = 0; q0 < 6; q0 += VG) {
@@ -379,12 +395,10 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
                 o[i] = ldsf(lutc + ((sv[i] >> 20) & 0x3FCu));
               }
               float* op = tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
-              if (jok0) __stcs(op, o[0]);
-              if (jok1) __stcs(op + 14, o[1]);
-              if (xok1) {
-                if (jok0) __stcs(op + 8, o[2]);
-                if (jok1) __stcs(op + 22, o[3]);
-              }
+              st_cs_pred(op, o[0], jok0);
+              st_cs_pred(op + 14, o[1], jok1);
+              st_cs_pred(op + 8, o[2], jok0 && xok1);
+              st_cs_pred(op + 22, o[3], jok1 && xok1);
               if (p.dbg_rs != nullptr) {
                 const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
                 for (int ee = 0; ee < 4; ++ee) {
@@ -608,23 +622,24 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
   const auto& th = P->th;
   const auto& tv = P->tv;
   const int nstrips = (P->w2 + SW - 1) / SW;
-  // source window per strip: every MMA tile's 32*KSH bytes from its start, and
-  // every tap of every output
-  int need = 16;
+  // per strip: converted width = the taps of its outputs (SWPN); RGB-plane
+  // stride = also every MMA tile's 32*KSH-byte read window (SWP)
+  int need = 16, taps = 16;
   for (int s = 0; s < nstrips; ++s) {
     const int X0 = s * SW, X1 = std::min(X0 + SW, P->w2);
     const int SX0 = th.xmin[X0] & ~15;
     for (int i = 0; i < g->htiles && X0 + 8 * i < X1; ++i)
       need = std::max(need, (th.xmin[X0 + 8 * i] & ~3) - SX0 + 32 * dt->ksh);
-    for (int o = X0; o < X1; ++o) need = std::max(need, th.xmin[o] + th.cnt[o] - SX0);
+    for (int o = X0; o < X1; ++o) taps = std::max(taps, th.xmin[o] + th.cnt[o] - SX0);
   }
+  need = std::max(need, taps);
   // round to an odd multiple of 16 (bank-conflict-free MMA A-fragment loads)
   int swp = (need + 15) / 16;
   if (!(swp & 1)) ++swp;
-  g->SWPN = ((need + 15) / 16) * 16;
+  g->SWPN = ((taps + 15) / 16) * 16;
   g->SWP = swp * 16;
   g->NX = (g->SWPN + 255) / 256;                       // TMA boxes are at most 256 wide
-  g->BW = ((g->SWPN / g->NX + 15) / 16) * 16;
+  g->BW = g->NX == 1 ? g->SWPN : 256;
   // ring depth: after the chunks a band needs (16-row granularity) the ring
   // must still hold the first row of the band's MMA windows
   int tr = 32 * dt->ksv + 16;
@@ -644,6 +659,8 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
   for (const Instance& in : kInstances)
     if (in.ksh == dt->ksh && in.ksv == dt->ksv) g->fn = in.fn;
   if (!g->fn) return fail(FC_ERR_UNSUPPORTED, "no kernel instance for this resize window");
+  if (2 * kChunkRows * (g->SWPN / 16) > 2 * kComputeThreads)
+    return fail(FC_ERR_UNSUPPORTED, "strip too wide for the colour stage");
   g->smem = smem_bytes(g->SWP, g->BW * g->NX, g->TRW);
   if (g->smem > static_cast<size_t>(max_smem))
     return fail(FC_ERR_UNSUPPORTED, "working set exceeds shared memory (resize window too wide)");
@@ -702,7 +719,7 @@ static fc_status tensor_map(const uint8_t* base, int64_t pitch, int64_t rows, in
   const cuuint32_t estr[2] = {1, 1};
   CUtensorMap m;
   const CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(FC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
   if (g_maps->size() > (1u << 16)) g_maps->clear();
@@ -783,6 +800,8 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
   prm.SWPN = g.SWPN;
   prm.BW = g.BW;
   prm.NX = g.NX;
+  prm.bwshift = g.NX == 1 ? 31 : 8;
+  prm.bwmask = g.NX == 1 ? -1 : 255;
   prm.TR = g.TR;
   prm.TRW = g.TRW;
   prm.nchunks = g.nchunks;
