@@ -1,0 +1,107 @@
+"""Multi-process host logic of the N>1 path on CPU (gloo, world size 2/3).
+
+One process per rank, as bench.py runs under torchrun.  Each rank builds the
+plan independently (it must be identical on every rank: no coordination is
+needed, the plan is a pure function of the request), computes ITS shard -- here
+with the CPU oracle, since this box has no GPU -- and the shards are gathered
+to the encoder rank over the process group at the row offsets the plan
+assigns.  The encoder checks the P:339 invariant: the gathered result equals
+the single-GPU result bit for bit.  The device path of the same exchange
+(fc_gather, NCCL send/recv) is the same row arithmetic.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, case, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2512_17574_b200 as fc
+    import synth
+    from oracle import oracle
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        W, H, N, gops, cfg = case
+        plan = fc.Plan(fc.VideoMeta(W, H, N, (30, 1), gops), fc.ModelCfg(world_size=world, **cfg))
+        # 1) every rank derived the same plan
+        digest = hashlib.sha256(repr((plan.sampled_indices, plan.ranks(), plan.grid_thw)).encode()).digest()
+        mine = torch.tensor(list(digest), dtype=torch.uint8)
+        allg = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(allg, mine)
+        assert all(torch.equal(a, mine) for a in allg), "plans differ between ranks"
+        # 2) this rank's shard (oracle stands in for the device kernel on CPU)
+        rp = plan.rank(rank)
+        idx = plan.sampled_indices
+        frames = idx[rp["sampled_begin"]:rp["sampled_begin"] + rp["sampled_count"]]
+        frames += [frames[-1]] * rp["pad_frames"] if frames else []
+        h2, w2 = plan.resized
+        host = {i: synth.frame_nv12(W, H, i, "natural", 21) for i in set(frames)}
+        rows = rp["row_end"] - rp["row_begin"]
+        shard = (oracle.preprocess([host[f] for f in frames], W, H, w2, h2) if frames
+                 else np.zeros((0, 1176), np.float32))
+        assert shard.shape[0] == rows
+        # 3) gather to the encoder rank at the planned row offsets
+        maxrows = max(r["row_end"] - r["row_begin"] for r in plan.ranks())
+        buf = torch.zeros((maxrows, 1176), dtype=torch.float32)
+        buf[:rows] = torch.from_numpy(shard)
+        enc = plan.cfg.encoder_rank
+        gathered = [torch.empty_like(buf) for _ in range(world)] if rank == enc else None
+        dist.gather(buf, gathered, dst=enc)
+        if rank == enc:
+            full = np.zeros((plan.token_rows, 1176), np.float32)
+            for r, rp_r in enumerate(plan.ranks()):
+                n = rp_r["row_end"] - rp_r["row_begin"]
+                full[rp_r["row_begin"]:rp_r["row_end"]] = gathered[r][:n].numpy()
+            host_all = {i: synth.frame_nv12(W, H, i, "natural", 21) for i in idx}
+            ref = oracle.preprocess([host_all[i] for i in idx], W, H, w2, h2)
+            assert full.view(np.uint32).tobytes() == ref.view(np.uint32).tobytes(), "gathered != single-GPU result"
+        q.put((rank, "ok"))
+    except Exception as e:  # report to the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+CASES = [
+    (320, 240, 300, list(range(0, 300, 30)), dict(sample_fps=2.0)),
+    (256, 144, 100, list(range(0, 100, 10)),
+     dict(sampling="explicit", explicit_indices=[0, 3, 12, 13, 14, 25, 41, 42, 57, 70, 81])),
+    (320, 240, 120, [0], dict(sample_fps=2.0)),  # single GOP: all on the encoder, other ranks idle
+]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_gloo_gather_equals_single_gpu(world, case):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES[case], q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    assert res == {r: "ok" for r in range(world)}, res

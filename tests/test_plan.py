@@ -1,0 +1,199 @@
+"""Host planner (fc_plan, through the C ABI) vs the oracle -- CPU only.
+
+Covers rows a1-a4 and b of SURVEY §8: sampling indices and grid_thw
+bit-exact against the oracle, the GOP partition's invariants (P:339-340,
+method b), optimality of the DP against brute force
+on tiny inputs, structured errors, and that libfc.so
+loads and exports every symbol include/fc.h declares.
+"""
+import ctypes
+import os
+import random
+import re
+
+import pytest
+
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def plan_of(fc, W, H, N, gops, fps=(30, 1), **cfg):
+    return fc.Plan(fc.VideoMeta(W, H, N, fps, gops), fc.ModelCfg(**cfg))
+
+
+def test_abi_exports_every_declared_symbol(fc):
+    hdr = open(os.path.join(ROOT, "include", "fc.h")).read()
+    names = set(re.findall(r"\b(fc_[a-z0-9_]+)\s*\(", hdr))
+    assert len(names) >= 15
+    lib = ctypes.CDLL(fc._native.LIB_PATH)
+    missing = [n for n in sorted(names) if not hasattr(lib, n)]
+    assert not missing, missing
+    assert fc.lib().fc_abi_version() == 1
+
+
+@pytest.mark.parametrize("name", sorted(synth.CONFIGS))
+def test_config_plans_match_oracle(fc, oracle, name):
+    wl = synth.CONFIGS[name]
+    for world in (1, 2, 4, 8):
+        p = plan_of(fc, wl.width, wl.height, wl.num_frames, wl.gop_start, wl.fps, world_size=world,
+                    sample_fps=wl.sample_fps)
+        idx = oracle.sample_indices(wl.num_frames, wl.fps[0] / wl.fps[1], wl.sample_fps)
+        assert p.sampled_indices == idx
+        h2, w2 = oracle.smart_resize(wl.height, wl.width)
+        assert p.resized == (h2, w2)
+        assert p.grid_thw == oracle.grid_thw(len(idx), h2, w2)
+        gt, gh, gw = p.grid_thw
+        oracle.check_rank_plans(wl.gop_start, wl.num_frames, idx, world, p.ranks(), gh, gw)
+
+
+def test_paper_scale_bottlenecks(fc):
+    """Per-rank pairs at W=8: c2 8, c3 38, c4 4."""
+    for name, want in (("c2", 8), ("c3", 38), ("c4", 4)):
+        wl = synth.CONFIGS[name]
+        p = plan_of(fc, wl.width, wl.height, wl.num_frames, wl.gop_start, wl.fps, world_size=8,
+                    sample_fps=wl.sample_fps)
+        pairs = [(r["sampled_count"] + r["pad_frames"]) // 2 for r in p.ranks()]
+        assert max(pairs) == want, pairs
+
+
+def test_single_gop_stays_on_encoder_rank(fc):
+    # a GOP is indivisible; one GOP -> one rank (the encoder rank 0)
+    wl = synth.CONFIGS["c1"]
+    p = plan_of(fc, wl.width, wl.height, wl.num_frames, wl.gop_start, world_size=8)
+    rs = p.ranks()
+    assert rs[0]["sampled_count"] == 8 and all(r["sampled_count"] == 0 for r in rs[1:])
+    assert p.ranks_used == 1
+
+
+def _random_video(rng):
+    G = rng.randint(1, 12)
+    sizes = [rng.randint(1, 9) for _ in range(G)]
+    N = sum(sizes)
+    starts = [sum(sizes[:i]) for i in range(G)]
+    return N, starts
+
+
+def test_random_plans_invariants_and_optimality(fc, oracle):
+    """1000 random (meta, selection, W): invariants hold; the max
+    per-rank pairs equals the brute-force optimum."""
+    rng = random.Random(1234)
+    checked = 0
+    for _ in range(1000):
+        N, starts = _random_video(rng)
+        k = rng.randint(1, N)
+        explicit = sorted(rng.sample(range(N), k))
+        world = rng.randint(1, 5)
+        p = plan_of(fc, 64, 48, N, starts, world_size=world, sampling="explicit", explicit_indices=explicit)
+        assert p.sampled_indices == explicit
+        gt, gh, gw = p.grid_thw
+        oracle.check_rank_plans(starts, N, explicit, world, p.ranks(), gh, gw)
+        if len(starts) <= 8:
+            per_gop = [sum(1 for f in explicit if oracle.gop_of(f, starts) == g) for g in range(len(starts))]
+            best = oracle.brute_force_min_max_pairs(per_gop, world)
+            got = max((r["sampled_count"] + r["pad_frames"] + 1) // 2 for r in p.ranks())
+            assert got == best, (per_gop, world, got, best)
+            checked += 1
+    assert checked > 300
+
+
+def test_monotone_in_world_size(fc):
+    # more ranks never increase the bottleneck
+    wl = synth.CONFIGS["c3"]
+    prev = None
+    for world in range(1, 9):
+        p = plan_of(fc, wl.width, wl.height, wl.num_frames, wl.gop_start, world_size=world, sample_fps=1.0)
+        m = max((r["sampled_count"] + r["pad_frames"]) // 2 for r in p.ranks())
+        assert prev is None or m <= prev
+        prev = m
+
+
+def test_method_b_moves_frames_up_never_down(fc, oracle):
+    # Fig. 8 / P:340: odd ranks take the next frame; only the last rank pads
+    p = plan_of(fc, 64, 48, 30, [0, 10, 20], world_size=3, sampling="explicit",
+                explicit_indices=[0, 3, 6, 10, 13, 16, 20, 23, 26])
+    rs = p.ranks()
+    assert [r["sampled_count"] for r in rs] == [4, 2, 3] or sum(r["pad_frames"] for r in rs) == 1
+    assert all(r["pad_frames"] == 0 for r in rs[:-1] if r["sampled_count"])
+    assert sum(r["sampled_count"] for r in rs) == 9
+    for r in rs:
+        if r["tail_frame"] >= 0:
+            assert r["tail_gop"] >= r["gop_end"]
+
+
+def test_est_decode_frames(fc):
+    # decode from the keyframe through the last target of each GOP
+    p = plan_of(fc, 64, 48, 30, [0, 10, 20], world_size=1, sampling="explicit", explicit_indices=[2, 5, 12, 25])
+    assert p.rank(0)["est_decode_frames"] == (5 + 1) + (2 + 1) + (5 + 1)
+
+
+def test_determinism(fc):
+    wl = synth.CONFIGS["c2"]
+    a = plan_of(fc, wl.width, wl.height, wl.num_frames, wl.gop_start, world_size=8)
+    b = plan_of(fc, wl.width, wl.height, wl.num_frames, wl.gop_start, world_size=8)
+    assert a.ranks() == b.ranks() and a.sampled_indices == b.sampled_indices
+
+
+def test_encoder_rank_takes_a_full_share(fc):
+    wl = synth.CONFIGS["c2"]
+    p = plan_of(fc, wl.width, wl.height, wl.num_frames, wl.gop_start, world_size=8)
+    pairs = [(r["sampled_count"] + r["pad_frames"]) // 2 for r in p.ranks()]
+    assert pairs[0] == max(pairs)  # tie-break: maximise the encoder's share (fewer gather bytes)
+
+
+def test_fixed_resize_paper_224(fc):
+    # the serving evaluation resizes everything to 224x224
+    p = plan_of(fc, 1920, 1080, 1800, list(range(0, 1800, 30)), resized_height=224, resized_width=224)
+    assert p.resized == (224, 224) and p.grid_thw == (60, 16, 16)
+    assert p.token_rows // p.grid_thw[0] == 256  # 128 patch rows per frame (R14)
+
+
+@pytest.mark.parametrize("kwargs,code", [
+    (dict(W=63, H=48), "FC_ERR_UNSUPPORTED"),           # odd width (NV12)
+    (dict(W=64, H=48, N=1, gops=[0]), "FC_ERR_EMPTY_SELECTION"),  # n = 0
+    (dict(W=4000, H=4, N=100), "FC_ERR_ASPECT_RATIO"),  # > 200:1
+    (dict(gops=[0, 5, 5]), "FC_ERR_INVALID_ARG"),       # not strictly increasing
+    (dict(gops=[1, 5]), "FC_ERR_INVALID_ARG"),          # first GOP must start at 0
+    (dict(gops=[0, 500]), "FC_ERR_INVALID_ARG"),        # GOP start past the end
+    (dict(cfg=dict(world_size=2, encoder_rank=2)), "FC_ERR_RANK"),
+    (dict(cfg=dict(resized_height=100, resized_width=224)), "FC_ERR_INVALID_ARG"),
+    (dict(cfg=dict(sampling="explicit", explicit_indices=[3, 2])), "FC_ERR_INVALID_ARG"),
+])
+def test_structured_errors(fc, kwargs, code):
+    W, H, N = kwargs.get("W", 64), kwargs.get("H", 48), kwargs.get("N", 100)
+    gops = kwargs.get("gops", [0, 50])
+    with pytest.raises(fc.FcError) as e:
+        plan_of(fc, W, H, N, gops, **kwargs.get("cfg", {}))
+    assert e.value.name == code
+
+
+def test_rank_out_of_range(fc):
+    p = plan_of(fc, 64, 48, 100, [0, 50], world_size=2)
+    with pytest.raises(fc.FcError) as e:
+        p.rank(2)
+    assert e.value.name == "FC_ERR_RANK"
+
+
+def test_no_cpu_fallback(fc):
+    """fc_preprocess must fail loudly (not compute on the CPU) without an sm_100 device."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    p = plan_of(fc, 64, 48, 100, [0, 50], sampling="explicit", explicit_indices=[0, 10])
+    buf = (ctypes.c_uint8 * (48 * 64 * 2 + 64))()
+    base = (ctypes.addressof(buf) + 15) & ~15
+    surf = fc.SurfaceTable(100)
+    for i in (0, 10):
+        surf.arr[i] = fc._native.Nv12SurfaceC(base, base + 48 * 64, 64, 64)
+    out = (ctypes.c_float * (p.token_rows * 1176))()
+    st = fc.lib().fc_preprocess(p.handle, 0, surf.arr, 100, ctypes.cast(out, ctypes.c_void_p), None, None)
+    assert fc._native.STATUS[st] == "FC_ERR_CUDA"
+    assert b"sm_100" in fc.lib().fc_last_error() or b"cuda" in fc.lib().fc_last_error().lower()
+
+
+def test_missing_surface_reported(fc):
+    p = plan_of(fc, 64, 48, 100, [0, 50], sampling="explicit", explicit_indices=[0, 10])
+    surf = fc.SurfaceTable(100)  # all NULL
+    out = (ctypes.c_float * (p.token_rows * 1176))()
+    st = fc.lib().fc_preprocess(p.handle, 0, surf.arr, 100, ctypes.cast(out, ctypes.c_void_p), None, None)
+    assert fc._native.STATUS[st] == "FC_ERR_MISSING_SURFACE"
