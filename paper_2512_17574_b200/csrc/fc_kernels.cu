@@ -43,7 +43,7 @@ constexpr int kTileN = 8;                  // outputs per H-pass MMA tile (N of 
 constexpr int kStrip = 84;                 // output columns per strip: 3 merge blocks = 6 patches
 constexpr int kComputeWarps = 12;
 constexpr int kComputeThreads = 32 * kComputeWarps;
-constexpr int kThreads = kComputeThreads + 32;  // + 1 TMA producer warp
+constexpr int kThreads = kComputeThreads;  // thread 0 also issues the TMA copies
 constexpr int kMaxFramesPerLaunch = 120;   // TMA tensor maps (2 per frame) passed by value
 constexpr int kRingStride = 6 * kStrip + 16;  // ring row stride (words): == 8 mod 32, conflict-free A loads
 constexpr int kStages = 4;                 // raw NV12 chunk buffers (TMA runs kStages-1 chunks ahead)
@@ -95,20 +95,19 @@ __device__ __forceinline__ bool next_run(const Params& p, int& cur, int i1, Run&
   return true;
 }
 
-// Issue the TMA tensor copies of one 16-row chunk into a raw stage: per frame
-// of the pair, NX boxes of Y (BW x 16 rows) then NX boxes of UV (BW x 8 rows).
-// Lane 0 arms the full barrier with the stage's byte count first.
-__device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, int k, uint8_t* raw, uint64_t* bar,
-                                            int lane) {
-  const int boxes = 2 * 2 * p.NX;  // frames x planes x boxes
-  if (lane == 0) mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * 24 * p.BW * p.NX));
-  __syncwarp();
-  if (lane < boxes) {
-    const int f = lane / (2 * p.NX), rest = lane % (2 * p.NX), pl = rest / p.NX, sub = rest % p.NX;
-    uint8_t* dst = raw + f * 24 * p.BW * p.NX + (pl ? 16 * p.BW * p.NX + sub * 8 * p.BW : sub * 16 * p.BW);
-    tma_load_2d(dst, &p.tm[2 * (2 * pair + f) + pl], SX0 + sub * p.BW, pl ? k * (kChunkRows / 2) : k * kChunkRows,
-                bar);
-  }
+// Issue the TMA tensor copies of one 16-row chunk into a raw stage (one
+// thread): per frame of the pair, NX boxes of Y (BW x 16 rows) then NX boxes
+// of UV (BW x 8 rows), after arming the stage's full barrier with their bytes.
+__device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, int k, uint8_t* raw, uint64_t* bar) {
+  fence_proxy_async();
+  mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * 24 * p.BW * p.NX));
+  for (int f = 0; f < 2; ++f)
+    for (int pl = 0; pl < 2; ++pl)
+      for (int sub = 0; sub < p.NX; ++sub) {
+        uint8_t* dst = raw + f * 24 * p.BW * p.NX + (pl ? 16 * p.BW * p.NX + sub * 8 * p.BW : sub * 16 * p.BW);
+        tma_load_2d(dst, &p.tm[2 * (2 * pair + f) + pl], SX0 + sub * p.BW,
+                    pl ? k * (kChunkRows / 2) : k * kChunkRows, bar);
+      }
 }
 
 // Persistent, warp-specialised fused kernel.
@@ -133,7 +132,6 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
   extern __shared__ __align__(1024) uint8_t smem[];
   float* lut = reinterpret_cast<float*>(smem);                    // 3 x 256 f32 at offset 0
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + 3072);      // kStages full barriers
-  uint64_t* empty = full + kStages;                               // kStages empty barriers
   const int RAWF = 24 * p.BW * p.NX;                              // raw bytes per frame per stage
   uint8_t* raw = smem + 3072 + 128;                               // [kStages][2 f][Y boxes | UV boxes]
   const int SWP = p.SWP;
@@ -145,10 +143,7 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
   const int g = lane >> 2, tq = lane & 3;
 
   if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kComputeWarps);
-    }
+    for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
   for (int i = tid; i < 768; i += kThreads) lut[i] = __ldg(p.lut + i);
@@ -161,24 +156,6 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
   const int total = p.npairs * p.nstrips * p.gh2;
   const int i0 = static_cast<int>((static_cast<long long>(blockIdx.x) * total) / gridDim.x);
   const int i1 = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * total) / gridDim.x);
-
-  // ------------------------------------------------------------ producer warp
-  if (warp == kComputeWarps) {
-    uint32_t seq = 0;
-    int cur = i0;
-    Run r;
-    while (next_run(p, cur, i1, r)) {
-      const int SX0 = __ldg(p.hx + r.strip * p.sw) & ~15;
-      if (lane < 4) prefetch_tmap(&p.tm[2 * (2 * r.pair) + lane]);
-      for (int k = r.kfirst; k < r.klast; ++k, ++seq) {
-        const int buf = seq % kStages;
-        mbar_wait(&empty[buf], ((seq / kStages) & 1) ^ 1);
-        fence_proxy_async();
-        issue_chunk(p, r.pair, SX0, k, raw + buf * 2 * RAWF, &full[buf], lane);
-      }
-    }
-    return;
-  }
 
   // ------------------------------------------------------------ compute warps
   // colour items (frame, row, 16-pixel group): at most 2 per thread; their
@@ -237,6 +214,7 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
     const bool hst1 = hact && ho + 1 < p.sw && X0 + ho + 1 < p.W2;
 
     int next_k = r.kfirst;
+    int iss_k = r.kfirst;  // next chunk of this run to issue (thread 0)
     // ring words of source rows kfirst*16 + g and + g + 8 (advanced per chunk)
     int hwA = ((r.kfirst * CH) / 4 + (g >> 2)) % p.TRW;
     int hwB = ((r.kfirst * CH) / 4 + 2 + (g >> 2)) % p.TRW;
@@ -247,6 +225,14 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
         const int k = next_k;
         const int buf = seq % kStages;
         const uint8_t* rawb = raw + buf * 2 * RAWF;
+        // keep kStages chunks in flight: chunk seq+j goes to stage (seq+j) % kStages,
+        // whose previous chunk was converted before the last barrier
+        if (tid == 0) {
+          for (; iss_k < r.klast && iss_k - next_k < kStages; ++iss_k) {
+            const uint32_t s2 = seq + (iss_k - next_k);
+            issue_chunk(p, r.pair, SX0, iss_k, raw + (s2 % kStages) * 2 * RAWF, &full[s2 % kStages]);
+          }
+        }
         mbar_wait(&full[buf], (seq / kStages) & 1);
         // ---- a5: NV12 -> RGB planes, 16 pixels per item
 #pragma unroll
@@ -276,9 +262,7 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
             }
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[buf]);  // this warp is done reading the raw buffer
-        bar_sync(1, kComputeThreads);              // RGB planes complete
+        bar_sync(1, kComputeThreads);              // RGB planes complete; raw stage free
         // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of 3 for ILP
         if (hact && !(p.skip & 2)) {
           const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + (g & 3);
