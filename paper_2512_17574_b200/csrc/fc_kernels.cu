@@ -40,12 +40,14 @@ namespace fc {
 
 constexpr int kChunkRows = 16;             // source rows per chunk
 constexpr int kTileN = 8;                  // outputs per H-pass MMA tile (N of m16n8k32)
-constexpr int kStrip = 84;                 // output columns per strip: 3 merge blocks = 6 patches
-constexpr int kComputeWarps = 12;
+constexpr int kStrip = 56;                 // output columns per strip: 2 merge blocks = 4 patches
+constexpr int kComputeWarps = 8;
+constexpr int kPlanesPerWarp = 24 / kComputeWarps;  // V pass: (4 row groups x 6 planes) / warps
 constexpr int kComputeThreads = 32 * kComputeWarps;
 constexpr int kThreads = kComputeThreads;  // thread 0 also issues the TMA copies
 constexpr int kMaxFramesPerLaunch = 120;   // TMA tensor maps (2 per frame) passed by value
-constexpr int kRingStride = 6 * kStrip + 16;  // ring row stride (words): == 8 mod 32, conflict-free A loads
+constexpr int kRingStride = 6 * kStrip + 24;  // ring row stride (words): == 8 mod 32, conflict-free A loads
+static_assert(kRingStride % 32 == 8, "ring stride must be 8 mod 32");
 constexpr int kStages = 4;                 // raw NV12 chunk buffers (TMA runs kStages-1 chunks ahead)
 
 struct Params {
@@ -124,7 +126,7 @@ __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, 
 // Strips are whole merge blocks, so every token row is written by one CTA in
 // one band (no partial-sector merging across CTAs in L2).
 template <int KSH, int KSV>
-__global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_constant__ Params p) {
   constexpr int SW = kStrip;
   constexpr int CH = kChunkRows;
   constexpr int RS = kRingStride;
@@ -175,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
   const uint32_t rgb_s = smem_u32(rgb);
   const uint32_t ring_s = smem_u32(ring);
   const uint32_t lut_s = smem_u32(lut);
-  // V-pass role: row group vjg, planes {2 vsub, 2 vsub + 1}
+  // V-pass role: row group vjg, planes [kPlanesPerWarp*vsub, +kPlanesPerWarp)
   const int vjg = warp & 3, vsub = warp >> 2;
   const int j0 = 8 * vjg + 2 * tq;                 // output rows j0, j0+1 of the band
   const bool jok0 = j0 < 28, jok1 = j0 + 1 < 28;   // group 3 covers rows 24..31
@@ -235,30 +237,44 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
         }
         mbar_wait(&full[buf], (seq / kStages) & 1);
         // ---- a5: NV12 -> RGB planes, 16 pixels per item
+        auto convert = [&](int oy, int ouv, int orgb, int e) {
+            const uint4 Yv = *reinterpret_cast<const uint4*>(rawb + oy);
+            const uint4 UVv = *reinterpret_cast<const uint4*>(rawb + ouv);
+            uint4 Rv, Gv, Bv;
+            bt601_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x);
+            bt601_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y);
+            bt601_4(Yv.z, UVv.z, Rv.z, Gv.z, Bv.z);
+            bt601_4(Yv.w, UVv.w, Rv.w, Gv.w, Bv.w);
+            uint8_t* dst = rgb + orgb;
+            *reinterpret_cast<uint4*>(dst) = Rv;
+            *reinterpret_cast<uint4*>(dst + CH * SWP) = Gv;
+            *reinterpret_cast<uint4*>(dst + 2 * CH * SWP) = Bv;
+            if (p.dbg_src != nullptr) {
+              const int it = tid + e * kComputeThreads;
+              const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
+              const int y = k * CH + rr, x = SX0 + 16 * q;
+              if (y < p.H) {
+                const uint32_t cw[3][4] = {{Rv.x, Rv.y, Rv.z, Rv.w}, {Gv.x, Gv.y, Gv.z, Gv.w}, {Bv.x, Bv.y, Bv.z, Bv.w}};
+                const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
+                for (int i = 0; i < 16 && x + i < p.W; ++i)
+                  for (int c = 0; c < 3; ++c)
+                    p.dbg_src[((fi * p.H + y) * p.W + x + i) * 3 + c] = (cw[c][i >> 2] >> (8 * (i & 3))) & 0xFF;
+              }
+            }
+        };
+        if (!(p.skip & 1)) {
+          if constexpr (KSH <= 2) {  // <= 2 items per thread (host-checked), offsets precomputed
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          if (tid + e * kComputeThreads >= citems || (p.skip & 1)) break;
-          const uint4 Yv = *reinterpret_cast<const uint4*>(rawb + cy[e]);
-          const uint4 UVv = *reinterpret_cast<const uint4*>(rawb + cuv[e]);
-          uint4 Rv, Gv, Bv;
-          bt601_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x);
-          bt601_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y);
-          bt601_4(Yv.z, UVv.z, Rv.z, Gv.z, Bv.z);
-          bt601_4(Yv.w, UVv.w, Rv.w, Gv.w, Bv.w);
-          uint8_t* dst = rgb + crgb[e];
-          *reinterpret_cast<uint4*>(dst) = Rv;
-          *reinterpret_cast<uint4*>(dst + CH * SWP) = Gv;
-          *reinterpret_cast<uint4*>(dst + 2 * CH * SWP) = Bv;
-          if (p.dbg_src != nullptr) {
-            const int it = tid + e * kComputeThreads;
-            const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
-            const int y = k * CH + rr, x = SX0 + 16 * q;
-            if (y < p.H) {
-              const uint32_t cw[3][4] = {{Rv.x, Rv.y, Rv.z, Rv.w}, {Gv.x, Gv.y, Gv.z, Gv.w}, {Bv.x, Bv.y, Bv.z, Bv.w}};
-              const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
-              for (int i = 0; i < 16 && x + i < p.W; ++i)
-                for (int c = 0; c < 3; ++c)
-                  p.dbg_src[((fi * p.H + y) * p.W + x + i) * 3 + c] = (cw[c][i >> 2] >> (8 * (i & 3))) & 0xFF;
+            for (int e = 0; e < 2; ++e) {
+              if (tid + e * kComputeThreads >= citems) break;
+              convert(cy[e], cuv[e], crgb[e], e);
+            }
+          } else {  // very wide resize windows: any number of items
+            for (int it = tid; it < citems; it += kComputeThreads) {
+              const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
+              const int xb = 16 * q, sub = xb >> p.bwshift, xo = xb & p.bwmask;
+              convert(f * RAWF + (sub * 16 + rr) * p.BW + xo, f * RAWF + 16 * p.BW * p.NX + (sub * 8 + (rr >> 1)) * p.BW + xo,
+                      ((f * 3) * CH + rr) * SWP + xb, (it - tid) / kComputeThreads);
             }
           }
         }
@@ -332,24 +348,23 @@ __global__ void __launch_bounds__(kThreads, 2) fc_fused_kernel(const __grid_cons
           for (int kk = 0; kk < KSV; ++kk) {
             const int wa = w >= p.TRW ? w - p.TRW : w;
             const int wb4 = wa + 4 >= p.TRW ? wa + 4 - p.TRW : wa + 4;
-            rb[kk][0] = ring_s + (wa * RS + 2 * vsub * SW + g) * 4;
-            rb[kk][1] = ring_s + (wb4 * RS + 2 * vsub * SW + g) * 4;
+            rb[kk][0] = ring_s + (wa * RS + kPlanesPerWarp * vsub * SW + g) * 4;
+            rb[kk][1] = ring_s + (wb4 * RS + kPlanesPerWarp * vsub * SW + g) * 4;
             w = wa + 8;
           }
         }
         // token block of this (pair, band, strip); patch q of the strip starts at
         // column offset (X0 + 14 q): merge block wb = (X0/28) + q/2, sub-block wm = q&1
         float* tb = p.tokens + ((static_cast<size_t>(r.pair) * p.gh2 + hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + g;
-        const int fc0 = 2 * vsub;
-        float* tpe[2] = {tb + ((fc0 % 3) * 2 + fc0 / 3) * 196, tb + (((fc0 + 1) % 3) * 2 + (fc0 + 1) / 3) * 196};
+        const int fc0 = kPlanesPerWarp * vsub;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
+        for (int e = 0; e < kPlanesPerWarp; ++e) {
           const int fc = fc0 + e, f = fc / 3, c = fc - 3 * (fc / 3);
           const uint32_t lutc = lut_s + c * 1024;
-          float* tp = tpe[e];
+          float* tp = tb + (c * 2 + f) * 196;
           constexpr int VG = KSV == 1 ? 2 : 1;  // patches interleaved per group
 #pragma unroll
-          for (int q0 = 0; q0 < 6; q0 += VG) {
+          for (int q0 = 0; q0 < kStrip / 14; q0 += VG) {
             if (q0 >= npatch) break;
             uint32_t a[VG][KSV][4];
 #pragma unroll
@@ -643,8 +658,8 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
   for (const Instance& in : kInstances)
     if (in.ksh == dt->ksh && in.ksv == dt->ksv) g->fn = in.fn;
   if (!g->fn) return fail(FC_ERR_UNSUPPORTED, "no kernel instance for this resize window");
-  if (2 * kChunkRows * (g->SWPN / 16) > 2 * kComputeThreads)
-    return fail(FC_ERR_UNSUPPORTED, "strip too wide for the colour stage");
+  if (dt->ksh <= 2 && 2 * kChunkRows * (g->SWPN / 16) > 2 * kComputeThreads)
+    return fail(FC_ERR_UNSUPPORTED, "colour stage: more than 2 items per thread");
   g->smem = smem_bytes(g->SWP, g->BW * g->NX, g->TRW);
   if (g->smem > static_cast<size_t>(max_smem))
     return fail(FC_ERR_UNSUPPORTED, "working set exceeds shared memory (resize window too wide)");
