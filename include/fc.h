@@ -185,9 +185,15 @@ fc_status fc_preprocess_debug(const fc_plan_t* plan, int32_t rank, const fc_nv12
                               int64_t num_surfaces, float* tokens, int64_t grid_thw[3], void* stream,
                               uint8_t* rgb_src, uint8_t* rgb_resized);
 
-/* Throughput mode (config 5): `count` independent (plan, rank) jobs in ONE
- * launch on `stream`.  surfaces[i] / num_surfaces[i] / tokens[i] as in
- * fc_preprocess for job i.  All plans must share resized size and taps class. */
+/* Throughput mode (config 5): `count` independent (plan, rank) jobs on
+ * `stream`.  surfaces[i] / num_surfaces[i] / tokens[i] as in fc_preprocess
+ * for job i (tokens[i] may be NULL for a job whose rank has no rows).  Every
+ * job is validated before anything is launched.  Consecutive jobs with equal
+ * source size, resized size and frame count form ONE persistent launch (the
+ * work list spans all their pairs; per-job token bases and the NV12 tensor
+ * maps travel in a small stream-ordered device descriptor), so a batch of
+ * same-shape clips is a single kernel launch.  Jobs of other shapes start a
+ * new launch.  Results equal per-job fc_preprocess calls bit for bit. */
 fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* ranks, int32_t count,
                               const fc_nv12_surface* const* surfaces, const int64_t* num_surfaces,
                               float* const* tokens, void* stream);
@@ -215,6 +221,11 @@ fc_status fc_gather(const fc_plan_t* plan, int32_t rank, void* comm, const float
 const char* fc_status_string(fc_status s);
 const char* fc_last_error(void);
 int32_t fc_abi_version(void);
+
+/* Process-wide count of kernels this library has launched successfully
+ * (fused preprocess kernels; NCCL's own kernels and memcpys not included).
+ * Monotone; safe to call from any thread; no CUDA call. */
+uint64_t fc_kernel_launches(void);
 
 #ifdef __cplusplus
 }

@@ -209,7 +209,9 @@ def preprocess_debug(plan: Plan, rank: int, surfaces: SurfaceTable, stream=None)
 
 
 def preprocess_batch(jobs: Sequence[tuple[Plan, int, SurfaceTable]], outs=None, stream=None):
-    """fc_preprocess_batch: several independent (plan, rank) jobs on one stream."""
+    """fc_preprocess_batch: several independent (plan, rank) jobs on one stream;
+    consecutive jobs of equal geometry and pair count share ONE launch (a
+    config-5 batch of same-shape clips is a single persistent launch)."""
     import torch
     n = len(jobs)
     if outs is None:

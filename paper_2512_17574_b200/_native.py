@@ -68,7 +68,7 @@ class Nv12SurfaceC(ctypes.Structure):
 EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_get", "fc_plan_sampled_indices",
            "fc_plan_rank", "fc_preprocess", "fc_preprocess_debug", "fc_preprocess_batch", "fc_nccl_unique_id",
            "fc_nccl_comm_init", "fc_nccl_comm_destroy", "fc_gather", "fc_status_string", "fc_last_error",
-           "fc_abi_version"]
+           "fc_abi_version", "fc_kernel_launches"]
 
 _lib = None
 
@@ -106,10 +106,12 @@ def lib() -> ctypes.CDLL:
     L.fc_last_error.restype = ctypes.c_char_p
     L.fc_abi_version.argtypes = []
     L.fc_abi_version.restype = ctypes.c_int32
+    L.fc_kernel_launches.argtypes = []
+    L.fc_kernel_launches.restype = ctypes.c_uint64
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("fc_model_cfg_default", "fc_plan_destroy", "fc_status_string", "fc_last_error",
-                        "fc_abi_version"):
+                        "fc_abi_version", "fc_kernel_launches"):
             fn.restype = ctypes.c_int
     _lib = L
     return L

@@ -2,6 +2,7 @@
 // the CUDA launcher of libfc.so.  Not part of the ABI (include/fc.h is).
 #pragma once
 #include <cstdint>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -64,7 +65,8 @@ struct fc_plan_s {
   double sampled_fps = 0, second_per_grid = 0;
   int32_t world = 1, ranks_used = 0;
   std::vector<fc::RankPlan> ranks;
-  fc::AxisTable th, tv;      // horizontal (W -> W'), vertical (H -> H')
+  // horizontal (W -> W'), vertical (H -> H'); shared, immutable, cached per (in, out)
+  std::shared_ptr<const fc::AxisTable> th, tv;
   std::vector<float> lut;    // 3 x 256 (R5)
   std::mutex mu;             // guards dev
   std::unordered_map<int, fc::DeviceTables> dev;
@@ -74,4 +76,5 @@ namespace fc {
 void set_error(const std::string& msg);
 fc_status fail(fc_status s, const std::string& msg);
 fc_status build_axis(int in, int out, AxisTable* t);
+fc_status axis_cached(int in, int out, std::shared_ptr<const AxisTable>* t);
 }  // namespace fc

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <atomic>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -45,7 +46,7 @@ constexpr int kComputeWarps = 8;
 constexpr int kPlanesPerWarp = 24 / kComputeWarps;  // V pass: (4 row groups x 6 planes) / warps
 constexpr int kComputeThreads = 32 * kComputeWarps;
 constexpr int kThreads = kComputeThreads;  // thread 0 also issues the TMA copies
-constexpr int kMaxFramesPerLaunch = 120;   // TMA tensor maps (2 per frame) passed by value
+constexpr int kMaxInlineFrames = 120;      // tensor maps (2 per frame) passed by value up to this many frames
 constexpr int kRingStride = 6 * kStrip + 24;  // ring row stride (words): == 8 mod 32, conflict-free A loads
 static_assert(kRingStride % 32 == 8, "ring stride must be 8 mod 32");
 constexpr int kStages = 4;                 // raw NV12 chunk buffers (TMA runs kStages-1 chunks ahead)
@@ -75,7 +76,10 @@ struct Params {
   int frame_base;     // index of fr[0] within the rank's frame list (debug dumps)
   int skip;           // profiling only (FC_PROFILE_SKIP): 1 = colour, 2 = H pass, 4 = V pass
   int nframes;
-  CUtensorMap tm[2 * kMaxFramesPerLaunch];  // per frame: Y plane (box BW x 16), UV plane (box BW x 8)
+  int ppj;            // pairs per job (batch launches; == npairs for one job)
+  float* const* tokj; // device: per-job token base (batch launches) or null -> tokens
+  const CUtensorMap* tmg;  // device copy of the maps (launches past kMaxInlineFrames frames) or null -> tm
+  CUtensorMap tm[2 * kMaxInlineFrames];  // per frame: Y plane (box BW x 16), UV plane (box BW x 8)
 };
 
 // Walk of one CTA's work: contiguous (pair, strip, band) items, split into
@@ -101,13 +105,14 @@ __device__ __forceinline__ bool next_run(const Params& p, int& cur, int i1, Run&
 // thread): per frame of the pair, NX boxes of Y (BW x 16 rows) then NX boxes
 // of UV (BW x 8 rows), after arming the stage's full barrier with their bytes.
 __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, int k, uint8_t* raw, uint64_t* bar) {
+  const CUtensorMap* tm = p.tmg != nullptr ? p.tmg : p.tm;
   fence_proxy_async();
   mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * 24 * p.BW * p.NX));
   for (int f = 0; f < 2; ++f)
     for (int pl = 0; pl < 2; ++pl)
       for (int sub = 0; sub < p.NX; ++sub) {
         uint8_t* dst = raw + f * 24 * p.BW * p.NX + (pl ? 16 * p.BW * p.NX + sub * 8 * p.BW : sub * 16 * p.BW);
-        tma_load_2d(dst, &p.tm[2 * (2 * pair + f) + pl], SX0 + sub * p.BW,
+        tma_load_2d(dst, &tm[2 * (2 * pair + f) + pl], SX0 + sub * p.BW,
                     pl ? k * (kChunkRows / 2) : k * kChunkRows, bar);
       }
 }
@@ -214,7 +219,6 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
     const int ho = warp * kTileN + 2 * tq;
     const bool hst0 = hact && ho < p.sw && X0 + ho < p.W2;
     const bool hst1 = hact && ho + 1 < p.sw && X0 + ho + 1 < p.W2;
-
     int next_k = r.kfirst;
     int iss_k = r.kfirst;  // next chunk of this run to issue (thread 0)
     // ring words of source rows kfirst*16 + g and + g + 8 (advanced per chunk)
@@ -355,7 +359,16 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
         }
         // token block of this (pair, band, strip); patch q of the strip starts at
         // column offset (X0 + 14 q): merge block wb = (X0/28) + q/2, sub-block wm = q&1
-        float* tb = p.tokens + ((static_cast<size_t>(r.pair) * p.gh2 + hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + g;
+        // first token row of this pair (R6: a job's pairs are consecutive gh*gw-row blocks)
+        const size_t pair_rows = static_cast<size_t>(p.gh2) * p.gw2 * 4;
+        float* tpair;
+        if (p.tokj != nullptr) {
+          const int job = r.pair / p.ppj;
+          tpair = p.tokj[job] + static_cast<size_t>(r.pair - job * p.ppj) * pair_rows * kCols;
+        } else {
+          tpair = p.tokens + static_cast<size_t>(r.pair) * pair_rows * kCols;
+        }
+        float* tb = tpair + (static_cast<size_t>(hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + g;
         const int fc0 = kPlanesPerWarp * vsub;
 #pragma unroll
         for (int e = 0; e < kPlanesPerWarp; ++e) {
@@ -491,8 +504,8 @@ struct MmaTables {
 // V: per band, 4 groups of 8 output rows (rows 28hb + 8gi + [0..8), those past
 // the band's 28 rows carry no weights).
 static void build_mma_tables(const fc_plan_s* P, int sw, MmaTables* m) {
-  const AxisTable& th = P->th;
-  const AxisTable& tv = P->tv;
+  const AxisTable& th = *P->th;
+  const AxisTable& tv = *P->tv;
   const int nstrips = (th.out + sw - 1) / sw;
   const int htiles = (sw + 7) / 8;
   const int nth = nstrips * htiles;
@@ -565,10 +578,10 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
   std::memset(&key, 0, sizeof(key));
   key.dev = dev;
   key.sw = sw;
-  key.w = P->th.in;
-  key.w2 = P->th.out;
-  key.h = P->tv.in;
-  key.h2 = P->tv.out;
+  key.w = P->th->in;
+  key.w2 = P->th->out;
+  key.h = P->tv->in;
+  key.h2 = P->tv->out;
   std::memcpy(key.lut_bits, P->lut.data(), sizeof(key.lut_bits));
   std::lock_guard<std::mutex> gk(g_tables_mu);
   auto git = g_tables->find(key);
@@ -584,11 +597,11 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
   t.ksh = m.ksh;
   t.ksv = m.ksv;
   cudaError_t e = cudaSuccess;
-  if (e == cudaSuccess) e = upload(&t.hx, P->th.xmin);
+  if (e == cudaSuccess) e = upload(&t.hx, P->th->xmin);
   if (e == cudaSuccess) e = upload(&t.hxs, m.hxs);
   if (e == cudaSuccess) e = upload(&t.hfr, m.hfr);
-  if (e == cudaSuccess) e = upload(&t.vx, P->tv.xmin);
-  if (e == cudaSuccess) e = upload(&t.vcnt, P->tv.cnt);
+  if (e == cudaSuccess) e = upload(&t.vx, P->tv->xmin);
+  if (e == cudaSuccess) e = upload(&t.vcnt, P->tv->cnt);
   if (e == cudaSuccess) e = upload(&t.vys, m.vys);
   if (e == cudaSuccess) e = upload(&t.vfr, m.vfr);
   if (e == cudaSuccess) e = upload(&t.lut, P->lut);
@@ -618,8 +631,8 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
   const int SW = sw;
   g->sw = sw;
   g->htiles = (sw + 7) / 8;
-  const auto& th = P->th;
-  const auto& tv = P->tv;
+  const auto& th = *P->th;
+  const auto& tv = *P->tv;
   const int nstrips = (P->w2 + SW - 1) / SW;
   // per strip: converted width = the taps of its outputs (SWPN); RGB-plane
   // stride = also every MMA tile's 32*KSH-byte read window (SWP)
@@ -727,26 +740,21 @@ static fc_status tensor_map(const uint8_t* base, int64_t pitch, int64_t rows, in
   return FC_OK;
 }
 
-static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv12_surface* surfaces,
-                                 int64_t num_surfaces, float* tokens, int64_t grid_thw[3], void* stream,
-                                 uint8_t* dbg_src, uint8_t* dbg_rs) {
-  if (!Pc) return fail(FC_ERR_INVALID_ARG, "plan is NULL");
-  fc_plan_s* P = const_cast<fc_plan_s*>(Pc);
+// The rank's frame list (its sampled frames, then pad copies of the last),
+// after validating every surface it reads.  Empty for a rank with no rows.
+static std::atomic<uint64_t> g_launches{0};
+
+static fc_status rank_frames(const fc_plan_s* P, int32_t rank, const fc_nv12_surface* surfaces, int64_t num_surfaces,
+                             std::vector<int64_t>* frames) {
+  frames->clear();
   if (rank < 0 || rank >= P->world) return fail(FC_ERR_RANK, "rank outside [0, world_size)");
   const fc_rank_plan& rp = P->ranks[rank].p;
-  if (grid_thw) {
-    grid_thw[0] = P->gt;
-    grid_thw[1] = P->gh;
-    grid_thw[2] = P->gw;
-  }
   if (rp.row_end == rp.row_begin) return FC_OK;
-  if (!surfaces || !tokens) return fail(FC_ERR_INVALID_ARG, "surfaces/tokens is NULL");
-  // the rank's frame list: its sampled frames, then pad copies of the last
-  std::vector<int64_t> frames;
-  for (int64_t i = 0; i < rp.sampled_count; ++i) frames.push_back(P->sampled[rp.sampled_begin + i]);
-  for (int64_t i = 0; i < rp.pad_frames; ++i) frames.push_back(frames.back());
-  const int W = P->meta.width, H = P->meta.height;
-  for (int64_t f : frames) {
+  if (!surfaces) return fail(FC_ERR_INVALID_ARG, "surfaces is NULL");
+  for (int64_t i = 0; i < rp.sampled_count; ++i) frames->push_back(P->sampled[rp.sampled_begin + i]);
+  for (int64_t i = 0; i < rp.pad_frames; ++i) frames->push_back(frames->back());
+  const int W = P->meta.width;
+  for (int64_t f : *frames) {
     if (f >= num_surfaces) return fail(FC_ERR_MISSING_SURFACE, "surface array too short for frame " + std::to_string(f));
     const fc_nv12_surface& s = surfaces[f];
     if (!s.y || !s.uv) return fail(FC_ERR_MISSING_SURFACE, "NULL surface for frame " + std::to_string(f));
@@ -756,6 +764,24 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
         s.pitch_uv > INT32_MAX)
       return fail(FC_ERR_UNSUPPORTED, "pitches must be multiples of 16 and >= width");
   }
+  return FC_OK;
+}
+
+// One launch job: a (plan, rank)'s frame list, its surfaces and its token buffer.
+struct Job {
+  std::vector<int64_t> frames;
+  const fc_nv12_surface* surfaces;
+  float* tokens;
+};
+
+// ONE persistent launch over every pair of `jobs` (all of P's geometry and
+// pair count).  Up to kMaxInlineFrames frames of a single job, the tensor maps
+// travel in the kernel parameters (nothing to upload; graph-capturable);
+// beyond that, or for several jobs, a descriptor [maps | per-job token bases]
+// is copied to a stream-ordered device allocation (cudaMallocAsync, freed
+// after the launch in stream order).
+static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, uint8_t* dbg_src,
+                             uint8_t* dbg_rs) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -764,7 +790,8 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   if (major != 10) return fail(FC_ERR_CUDA, "fc kernels are built for sm_100a only (no CPU/other-arch fallback)");
-  // strips of 3 merge blocks; 1 merge block when a very wide resize window
+  const int W = P->meta.width, H = P->meta.height;
+  // strips of 2 merge blocks; 1 merge block when a very wide resize window
   // would not fit the working set in shared memory
   DeviceTables* dt = nullptr;
   Geometry g;
@@ -813,33 +840,78 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
   prm.vfr = dt->vfr;
   prm.lut = dt->lut;
   prm.dbg_src = dbg_src;
+  prm.dbg_rs = dbg_rs;
   {
     const char* sk = std::getenv("FC_PROFILE_SKIP");
     prm.skip = sk ? std::atoi(sk) : 0;
   }
-  prm.dbg_rs = dbg_rs;
-  const int64_t nf = static_cast<int64_t>(frames.size());
-  const int64_t rows_per_pair = P->gh * P->gw;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  for (int64_t f0 = 0; f0 < nf; f0 += kMaxFramesPerLaunch) {
-    const int64_t cnt = std::min<int64_t>(kMaxFramesPerLaunch, nf - f0);
-    prm.frame_base = static_cast<int>(f0);
-    prm.nframes = static_cast<int>(cnt);
-    prm.tokens = tokens + (f0 / 2) * rows_per_pair * kCols;
-    for (int64_t i = 0; i < cnt; ++i) {
-      const fc_nv12_surface& sf = surfaces[frames[f0 + i]];
-      st = tensor_map(sf.y, sf.pitch_y, H, g.BW, kChunkRows, &prm.tm[2 * i]);
-      if (st == FC_OK) st = tensor_map(sf.uv, sf.pitch_uv, H / 2, g.BW, kChunkRows / 2, &prm.tm[2 * i + 1]);
+  const int64_t nfj = static_cast<int64_t>(jobs[0].frames.size());
+  const int64_t nf = nfj * static_cast<int64_t>(jobs.size());
+  const long long items = (nf / 2) * static_cast<long long>(g.nstrips) * prm.gh2;
+  if (items > INT32_MAX) return fail(FC_ERR_UNSUPPORTED, "launch too large (> 2^31 work items)");
+  prm.frame_base = 0;
+  prm.nframes = static_cast<int>(nf);
+  prm.npairs = static_cast<int>(nf / 2);
+  prm.ppj = static_cast<int>(nfj / 2);
+  prm.tokens = jobs[0].tokens;
+  const bool inline_maps = jobs.size() == 1 && nf <= kMaxInlineFrames;
+  std::vector<CUtensorMap> maps(inline_maps ? 0 : 2 * nf);
+  CUtensorMap* mp = inline_maps ? prm.tm : maps.data();
+  for (size_t j = 0; j < jobs.size(); ++j)
+    for (int64_t i = 0; i < nfj; ++i) {
+      const fc_nv12_surface& sf = jobs[j].surfaces[jobs[j].frames[i]];
+      const int64_t fi = static_cast<int64_t>(j) * nfj + i;
+      st = tensor_map(sf.y, sf.pitch_y, H, g.BW, kChunkRows, &mp[2 * fi]);
+      if (st == FC_OK) st = tensor_map(sf.uv, sf.pitch_uv, H / 2, g.BW, kChunkRows / 2, &mp[2 * fi + 1]);
       if (st != FC_OK) return st;
     }
-    prm.npairs = static_cast<int>(cnt / 2);
-    const long long items = static_cast<long long>(prm.npairs) * g.nstrips * prm.gh2;
-    const int grid = static_cast<int>(std::min<long long>(items, static_cast<long long>(occ) * nsm));
-    fn<<<grid, kThreads, g.smem, s>>>(prm);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  void* desc = nullptr;
+  if (!inline_maps) {
+    const size_t mbytes = maps.size() * sizeof(CUtensorMap);
+    const size_t bytes = mbytes + (jobs.size() > 1 ? jobs.size() * sizeof(float*) : 0);
+    std::vector<uint8_t> host(bytes);
+    std::memcpy(host.data(), maps.data(), mbytes);
+    if (jobs.size() > 1)
+      for (size_t j = 0; j < jobs.size(); ++j) std::memcpy(host.data() + mbytes + j * sizeof(float*), &jobs[j].tokens, sizeof(float*));
+    e = cudaMallocAsync(&desc, bytes, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (launch descriptor)");
+    // pageable source: returns once the bytes are staged, so `host` may die
+    e = cudaMemcpyAsync(desc, host.data(), bytes, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(desc, s);
+      return cuda_fail(e, "descriptor upload");
+    }
+    prm.tmg = reinterpret_cast<const CUtensorMap*>(desc);
+    if (jobs.size() > 1) prm.tokj = reinterpret_cast<float* const*>(static_cast<uint8_t*>(desc) + mbytes);
   }
+  const int grid = static_cast<int>(std::min<long long>(items, static_cast<long long>(occ) * nsm));
+  fn<<<grid, kThreads, g.smem, s>>>(prm);
+  e = cudaGetLastError();
+  if (desc) cudaFreeAsync(desc, s);
+  if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   return FC_OK;
+}
+
+static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv12_surface* surfaces,
+                                 int64_t num_surfaces, float* tokens, int64_t grid_thw[3], void* stream,
+                                 uint8_t* dbg_src, uint8_t* dbg_rs) {
+  if (!Pc) return fail(FC_ERR_INVALID_ARG, "plan is NULL");
+  fc_plan_s* P = const_cast<fc_plan_s*>(Pc);
+  if (rank < 0 || rank >= P->world) return fail(FC_ERR_RANK, "rank outside [0, world_size)");
+  if (grid_thw) {
+    grid_thw[0] = P->gt;
+    grid_thw[1] = P->gh;
+    grid_thw[2] = P->gw;
+  }
+  std::vector<Job> jobs(1);
+  fc_status st = rank_frames(P, rank, surfaces, num_surfaces, &jobs[0].frames);
+  if (st != FC_OK || jobs[0].frames.empty()) return st;
+  if (!tokens) return fail(FC_ERR_INVALID_ARG, "tokens is NULL");
+  jobs[0].surfaces = surfaces;
+  jobs[0].tokens = tokens;
+  return launch_jobs(P, jobs, stream, dbg_src, dbg_rs);
 }
 
 }  // namespace fc
@@ -864,14 +936,45 @@ fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* rank
                               float* const* tokens, void* stream) {
   if (count < 0 || (count > 0 && (!plans || !ranks || !surfaces || !num_surfaces || !tokens)))
     return fail(FC_ERR_INVALID_ARG, "batch arguments");
-  // v0: one launch per job (a single work-list launch is on the roadmap)
+  // validate every job before any launch; then one launch per maximal run of
+  // consecutive jobs sharing source size, resized size and pair count (a
+  // homogeneous batch -- config 5 -- is one launch)
+  std::vector<Job> jobs(count);
+  std::vector<fc_plan_s*> jp(count);
   for (int32_t i = 0; i < count; ++i) {
-    fc_status st = preprocess_impl(plans[i], ranks[i], surfaces[i], num_surfaces[i], tokens[i], nullptr, stream,
-                                   nullptr, nullptr);
+    if (!plans[i]) return fail(FC_ERR_INVALID_ARG, "batch: plan " + std::to_string(i) + " is NULL");
+    jp[i] = const_cast<fc_plan_s*>(plans[i]);
+    fc_status st = rank_frames(jp[i], ranks[i], surfaces[i], num_surfaces[i], &jobs[i].frames);
     if (st != FC_OK) return st;
+    if (!jobs[i].frames.empty() && !tokens[i]) return fail(FC_ERR_INVALID_ARG, "batch: tokens is NULL");
+    jobs[i].surfaces = surfaces[i];
+    jobs[i].tokens = tokens[i];
+  }
+  auto same = [&](int a, int b) {
+    const fc_plan_s &A = *jp[a], &B = *jp[b];
+    return A.meta.width == B.meta.width && A.meta.height == B.meta.height && A.w2 == B.w2 && A.h2 == B.h2 &&
+           jobs[a].frames.size() == jobs[b].frames.size();
+  };
+  std::vector<Job> group;
+  for (int32_t i = 0; i < count;) {
+    if (jobs[i].frames.empty()) {
+      ++i;
+      continue;
+    }
+    int32_t j = i;
+    group.clear();
+    while (j < count && (jobs[j].frames.empty() || same(i, j))) {
+      if (!jobs[j].frames.empty()) group.push_back(jobs[j]);
+      ++j;
+    }
+    fc_status st = launch_jobs(jp[i], group, stream, nullptr, nullptr);
+    if (st != FC_OK) return st;
+    i = j;
   }
   return FC_OK;
 }
+
+uint64_t fc_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 void fc_plan_destroy(fc_plan_t* P) {
   // device tables belong to the process-wide cache (shared by equal shapes)

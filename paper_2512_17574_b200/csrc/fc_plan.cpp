@@ -12,6 +12,8 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <map>
+#include <memory>
 #include <cstring>
 #include <limits>
 #include <new>
@@ -101,6 +103,30 @@ fc_status build_axis(int in, int out, AxisTable* t) {
       p[1 * W + word] |= b1 << sh;
       p[2 * W + word] |= b2 << sh;
     }
+  return FC_OK;
+}
+
+// Axis tables depend only on (in, out): requests of one resolution share them
+// (a serving process sees few distinct shapes).  Bounded; evicted tables stay
+// alive while a plan holds them.
+fc_status axis_cached(int in, int out, std::shared_ptr<const AxisTable>* t) {
+  static std::mutex mu;
+  static auto* cache = new std::map<std::pair<int, int>, std::shared_ptr<const AxisTable>>();  // never freed
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache->find({in, out});
+    if (it != cache->end()) {
+      *t = it->second;
+      return FC_OK;
+    }
+  }
+  auto a = std::make_shared<AxisTable>();
+  fc_status st = build_axis(in, out, a.get());
+  if (st != FC_OK) return st;
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache->size() >= 256) cache->clear();
+  (*cache)[{in, out}] = a;
+  *t = a;
   return FC_OK;
 }
 
@@ -454,8 +480,8 @@ fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t*
     P->second_per_grid = kTps / P->sampled_fps;
     st = partition(P);
   }
-  if (st == FC_OK) st = build_axis(m.width, P->w2, &P->th);
-  if (st == FC_OK) st = build_axis(m.height, P->h2, &P->tv);
+  if (st == FC_OK) st = axis_cached(m.width, P->w2, &P->th);
+  if (st == FC_OK) st = axis_cached(m.height, P->h2, &P->tv);
   if (st == FC_OK) {
     P->lut.resize(3 * 256);
     for (int ch = 0; ch < 3; ++ch)
@@ -488,8 +514,8 @@ fc_status fc_plan_info_get(const fc_plan_t* P, fc_plan_info* info) {
   info->second_per_grid = P->second_per_grid;
   info->ranks_used = P->ranks_used;
   info->world_size = P->world;
-  info->max_taps_h = P->th.max_cnt;
-  info->max_taps_v = P->tv.max_cnt;
+  info->max_taps_h = P->th->max_cnt;
+  info->max_taps_v = P->tv->max_cnt;
   return FC_OK;
 }
 

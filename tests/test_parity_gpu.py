@@ -171,3 +171,98 @@ def test_full_c5_clip(fc, oracle, cuda):
     plan, e, s = _full_config(fc, oracle, cuda, "c5", lambda gt: range(gt), kind="uniform", clip=17)
     assert plan.grid_thw == (10, 34, 60)
     assert e == s
+
+
+# ------------------------------------------------------------ batch launches
+def _clip_inputs(fc, wl, clip, kind, plan):
+    host = synth.frames_nv12(wl, plan.sampled_indices, kind, clip=clip)
+    dev = synth.to_device(host)
+    return host, dev, fc.SurfaceTable.from_tensors(dev, wl.num_frames)
+
+
+def test_batch_homogeneous_matches_oracle(fc, oracle, cuda):
+    """fc_preprocess_batch, config-5 shape: 6 clips with different content in
+    ONE launch (per-job token bases, tensor maps in device memory); every
+    clip equals the oracle on its own frames."""
+    import torch
+    wl = synth.CONFIGS["c5"]
+    jobs, hosts = [], []
+    for clip in range(6):
+        plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
+                       fc.ModelCfg(sampling="explicit", explicit_indices=[3 * clip, 40 + clip, 100, 299 - clip]))
+        host, dev, surf = _clip_inputs(fc, wl, clip, "natural" if clip % 2 else "uniform", plan)
+        jobs.append((plan, 0, surf, dev))
+        hosts.append(host)
+    outs = fc.preprocess_batch([(p, r, s) for p, r, s, _ in jobs])
+    torch.cuda.synchronize()
+    h2, w2 = jobs[0][0].resized
+    for (plan, _, _, _), host, out in zip(jobs, hosts, outs):
+        ref = oracle.preprocess([host[i] for i in plan.sampled_indices], wl.width, wl.height, w2, h2)
+        assert tol_check(out.cpu().numpy(), ref, "batch clip") == ref.size
+
+
+def test_batch_heterogeneous_equals_single_calls(fc, oracle, cuda):
+    """Mixed shapes, pair counts, a rank with no rows and a job past the
+    inline tensor-map limit in one batch call: each job's tokens equal its own
+    fc_preprocess call bit for bit (runs of equal geometry share a launch)."""
+    import torch
+    specs = [  # (W, H, N, gops, cfg, rank)
+        (320, 240, 120, [0], dict(sample_fps=2.0), 0),
+        (320, 240, 120, [0], dict(sample_fps=2.0), 0),
+        (320, 240, 120, [0], dict(sample_fps=2.0, world_size=2), 1),   # no rows
+        (320, 240, 120, [0], dict(sampling="explicit", explicit_indices=[1, 7, 9]), 0),
+        (200, 120, 16, [0], dict(sampling="explicit", explicit_indices=list(range(16))), 0),
+        (64, 48, 300, list(range(0, 300, 30)), dict(sampling="explicit", explicit_indices=list(range(0, 300, 2))), 0),
+    ]
+    jobs, singles = [], []
+    for k, (W, H, N, gops, cfg, rank) in enumerate(specs):
+        plan = fc.Plan(fc.VideoMeta(W, H, N, (30, 1), gops), fc.ModelCfg(**cfg))
+        host = {i: synth.frame_nv12(W, H, i, "uniform", 50 + k) for i in plan.sampled_indices}
+        dev = synth.to_device(host)
+        surf = fc.SurfaceTable.from_tensors(dev, N)
+        jobs.append((plan, rank, surf, dev))
+        singles.append(fc.preprocess(plan, rank, surf) if plan.rank(rank)["row_end"] > plan.rank(rank)["row_begin"]
+                       else None)
+    outs = fc.preprocess_batch([(p, r, s) for p, r, s, _ in jobs])
+    torch.cuda.synchronize()
+    for k, (single, out) in enumerate(zip(singles, outs)):
+        if single is None:
+            assert out.shape[0] == 0
+            continue
+        assert torch.equal(out.view(torch.int32), single.view(torch.int32)), f"job {k}"
+    # the long job (150 frames > inline limit) against the oracle on two pairs
+    plan, _, _, _ = jobs[-1]
+    W, H = 64, 48
+    h2, w2 = plan.resized
+    rpp = plan.grid_thw[1] * plan.grid_thw[2]
+    idx = plan.sampled_indices
+    for t in (0, plan.grid_thw[0] - 1):
+        fr = [idx[2 * t], idx[2 * t + 1]]
+        ref = oracle.preprocess([synth.frame_nv12(W, H, f, "uniform", 55) for f in fr], W, H, w2, h2)
+        tol_check(outs[-1][t * rpp:(t + 1) * rpp].cpu().numpy(), ref, f"long job pair {t}")
+
+
+def test_full_c5_batch_64_clips(fc, oracle, cuda):
+    """Config 5 as the bench runs it: 64 clips, one fc_preprocess_batch call;
+    sampled clips checked pair by pair against the oracle."""
+    import torch
+    wl = synth.CONFIGS["c5"]
+    meta = fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start)
+    plan = fc.Plan(meta, fc.ModelCfg(sample_fps=wl.sample_fps))
+    idx = plan.sampled_indices
+    hosts, jobs = {}, []
+    for clip in range(wl.clips):
+        host = synth.frames_nv12(wl, idx, "natural", clip=clip)
+        if clip in (0, 31, 63):
+            hosts[clip] = host
+        dev = synth.to_device(host)
+        jobs.append((plan, 0, fc.SurfaceTable.from_tensors(dev, wl.num_frames), dev))
+    outs = fc.preprocess_batch([(p, r, s) for p, r, s, _ in jobs])
+    torch.cuda.synchronize()
+    h2, w2 = plan.resized
+    rpp = plan.grid_thw[1] * plan.grid_thw[2]
+    for clip, host in hosts.items():
+        for t in (0, 4, plan.grid_thw[0] - 1):
+            ref = oracle.preprocess([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2)
+            got = outs[clip][t * rpp:(t + 1) * rpp].cpu().numpy()
+            assert tol_check(got, ref, f"c5 clip {clip} pair {t}") == ref.size
