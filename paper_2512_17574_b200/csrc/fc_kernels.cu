@@ -50,6 +50,8 @@ constexpr int kMaxInlineFrames = 120;      // tensor maps (2 per frame) passed b
 constexpr int kRingStride = 6 * kStrip + 24;  // ring row stride (words): == 8 mod 32, conflict-free A loads
 static_assert(kRingStride % 32 == 8, "ring stride must be 8 mod 32");
 constexpr int kStages = 4;                 // raw NV12 chunk buffers (TMA runs kStages-1 chunks ahead)
+constexpr int kIssueWarp = kComputeWarps - 1;  // owns no H-pass tile (7 tiles of 8 cover a 56-column strip)
+static_assert((kStrip + kTileN - 1) / kTileN < kComputeWarps, "the TMA issuing warp must own no H tile");
 
 struct Params {
   int W, H, W2, H2;
@@ -148,6 +150,7 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, tq = lane & 3;
+  const bool issuer = tid == kIssueWarp * 32;  // lane 0 of the warp without an H tile issues the TMA copies
 
   if (tid == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
@@ -220,10 +223,14 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
     const bool hst0 = hact && ho < p.sw && X0 + ho < p.W2;
     const bool hst1 = hact && ho + 1 < p.sw && X0 + ho + 1 < p.W2;
     int next_k = r.kfirst;
-    int iss_k = r.kfirst;  // next chunk of this run to issue (thread 0)
     // ring words of source rows kfirst*16 + g and + g + 8 (advanced per chunk)
     int hwA = ((r.kfirst * CH) / 4 + (g >> 2)) % p.TRW;
     int hwB = ((r.kfirst * CH) / 4 + 2 + (g >> 2)) % p.TRW;
+    // prefill: the run's first kStages chunks (every stage is free: the previous
+    // run consumed all it issued, before the barrier that ended its last band)
+    if (issuer)
+      for (int j = 0; j < kStages && r.kfirst + j < r.klast; ++j)
+        issue_chunk(p, r.pair, SX0, r.kfirst + j, raw + ((seq + j) % kStages) * 2 * RAWF, &full[(seq + j) % kStages]);
     for (int hb_ = r.hb0; hb_ < r.hb1; ++hb_) {
       const int yo0 = hb_ * 28;
       const int kneed = min(p.nchunks, (__ldg(p.vx + yo0 + 27) + __ldg(p.vcnt + yo0 + 27) + CH - 1) / CH);
@@ -231,14 +238,6 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
         const int k = next_k;
         const int buf = seq % kStages;
         const uint8_t* rawb = raw + buf * 2 * RAWF;
-        // keep kStages chunks in flight: chunk seq+j goes to stage (seq+j) % kStages,
-        // whose previous chunk was converted before the last barrier
-        if (tid == 0) {
-          for (; iss_k < r.klast && iss_k - next_k < kStages; ++iss_k) {
-            const uint32_t s2 = seq + (iss_k - next_k);
-            issue_chunk(p, r.pair, SX0, iss_k, raw + (s2 % kStages) * 2 * RAWF, &full[s2 % kStages]);
-          }
-        }
         mbar_wait(&full[buf], (seq / kStages) & 1);
         // ---- a5: NV12 -> RGB planes, 16 pixels per item
         auto convert = [&](int oy, int ouv, int orgb, int e) {
@@ -283,6 +282,9 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
           }
         }
         bar_sync(1, kComputeThreads);              // RGB planes complete; raw stage free
+        // refill the stage just converted with chunk k + kStages; the issuing
+        // warp owns no H tile, so this runs beside the H pass, off the critical path
+        if (issuer && k + kStages < r.klast) issue_chunk(p, r.pair, SX0, k + kStages, raw + buf * 2 * RAWF, &full[buf]);
         // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of 3 for ILP
         if (hact && !(p.skip & 2)) {
           const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + (g & 3);
