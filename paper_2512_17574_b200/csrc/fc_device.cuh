@@ -159,15 +159,26 @@ __device__ __forceinline__ void bt601_4(uint32_t yw, uint32_t uvw, uint32_t& R, 
 template <bool kSignedB>
 __device__ __forceinline__ void mma_u8(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   if constexpr (kSignedB) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+    asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
         : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
   } else {
-    asm volatile(
-        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+    asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
         : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+  }
+}
+// Same with a uniform constant accumulator input (d = A*B + c).
+template <bool kSignedB>
+__device__ __forceinline__ void mma_u8c(int (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1, int c) {
+  if constexpr (kSignedB) {
+    asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%10,%10,%10};"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(c));
+  } else {
+    asm("mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%10,%10,%10,%10};"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "r"(c));
   }
 }
 
@@ -179,14 +190,14 @@ __device__ __forceinline__ void mma_u8(int (&d)[4], const uint32_t (&a)[4], uint
 template <int KS>
 __device__ __forceinline__ void fir_mma_planes(int (&d2)[4], int (&d1)[4], int (&d0)[4], const uint32_t (&a)[KS][4],
                                                const uint32_t (&bf)[KS][3][2]) {
+  // k-step 0 takes its accumulator from constants (32 = Pillow's 2^21
+  // rounding term in units of plane 2; 0 for the others), so no register
+  // re-initialisation is needed per tile
+  mma_u8c<true>(d2, a[0], bf[0][2][0], bf[0][2][1], 32);
+  mma_u8c<false>(d1, a[0], bf[0][1][0], bf[0][1][1], 0);
+  mma_u8c<false>(d0, a[0], bf[0][0][0], bf[0][0][1], 0);
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    d2[i] = 32;
-    d1[i] = 0;
-    d0[i] = 0;
-  }
-#pragma unroll
-  for (int k = 0; k < KS; ++k) {
+  for (int k = 1; k < KS; ++k) {
     mma_u8<true>(d2, a[k], bf[k][2][0], bf[k][2][1]);
     mma_u8<false>(d1, a[k], bf[k][1][0], bf[k][1][1]);
     mma_u8<false>(d0, a[k], bf[k][0][0], bf[k][0][1]);

@@ -44,6 +44,7 @@ constexpr int kTileN = 8;                  // outputs per H-pass MMA tile (N of 
 constexpr int kStrip = 56;                 // output columns per strip: 2 merge blocks = 4 patches
 constexpr int kComputeWarps = 8;
 constexpr int kPlanesPerWarp = 24 / kComputeWarps;  // V pass: (4 row groups x 6 planes) / warps
+static_assert(kPlanesPerWarp == 3, "V pass: each warp owns the 3 channels of one frame");
 constexpr int kComputeThreads = 32 * kComputeWarps;
 constexpr int kThreads = kComputeThreads;  // thread 0 also issues the TMA copies
 constexpr int kMaxInlineFrames = 120;      // tensor maps (2 per frame) passed by value up to this many frames
@@ -76,7 +77,7 @@ struct Params {
   uint8_t* dbg_src;   // [nframes_total, H, W, 3] or null
   uint8_t* dbg_rs;    // [nframes_total, H2, W2, 3] or null
   int frame_base;     // index of fr[0] within the rank's frame list (debug dumps)
-  int skip;           // profiling only (FC_PROFILE_SKIP): 1 = colour, 2 = H pass, 4 = V pass
+  uint32_t trw_magic;  // ceil(2^32 / TRW): x mod TRW = x - TRW * umulhi(x, magic) for the row words used
   int nframes;
   int ppj;            // pairs per job (batch launches; == npairs for one job)
   float* const* tokj; // device: per-job token base (batch launches) or null -> tokens
@@ -132,7 +133,7 @@ __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, 
 // Work items are (pair, strip, band) triples; CTA b takes [b*T/G, (b+1)*T/G).
 // Strips are whole merge blocks, so every token row is written by one CTA in
 // one band (no partial-sector merging across CTAs in L2).
-template <int KSH, int KSV>
+template <int KSH, int KSV, bool DBG>
 __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_constant__ Params p) {
   constexpr int SW = kStrip;
   constexpr int CH = kChunkRows;
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
             *reinterpret_cast<uint4*>(dst) = Rv;
             *reinterpret_cast<uint4*>(dst + CH * SWP) = Gv;
             *reinterpret_cast<uint4*>(dst + 2 * CH * SWP) = Bv;
-            if (p.dbg_src != nullptr) {
+            if (DBG && p.dbg_src != nullptr) {
               const int it = tid + e * kComputeThreads;
               const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
               const int y = k * CH + rr, x = SX0 + 16 * q;
@@ -265,7 +266,7 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
               }
             }
         };
-        if (!(p.skip & 1)) {
+        {
           if constexpr (KSH <= 2) {  // <= 2 items per thread (host-checked), offsets precomputed
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
         // warp owns no H tile, so this runs beside the H pass, off the critical path
         if (issuer && k + kStages < r.klast) issue_chunk(p, r.pair, SX0, k + kStages, raw + buf * 2 * RAWF, &full[buf]);
         // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of 3 for ILP
-        if (hact && !(p.skip & 2)) {
+        if (hact) {
           const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + (g & 3);
           const uint32_t dB = ring_s + (hwB * RS + ho) * 4 + (g & 3);
           constexpr int HG = KSH == 1 ? 3 : 2;  // planes interleaved per group (ILP vs registers)
@@ -334,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
         bar_sync(1, kComputeThreads);  // ring rows complete, RGB planes free
       }
       // ---- a7 + a8 + a9: vertical pass (MMA), normalise, patchify
-      if (!(p.skip & 4)) {
+      {
         const int grp = hb_ * 4 + vjg;
         uint32_t vb[KSV][3][2];
         const uint32_t* f = p.vfr + static_cast<size_t>(grp) * KSV * 3 * 64 + lane * 2;
@@ -349,7 +350,8 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
         // A rows: columns (g, g+8) of a patch; k = source rows ys + 32kk + 4t (+16)
         uint32_t rb[KSV][2];
         {
-          int w = (ys >> 2) % p.TRW + tq;
+          const uint32_t yw = static_cast<uint32_t>(ys) >> 2;
+          int w = static_cast<int>(yw - p.TRW * __umulhi(yw, p.trw_magic)) + tq;  // (ys/4) mod TRW
 #pragma unroll
           for (int kk = 0; kk < KSV; ++kk) {
             const int wa = w >= p.TRW ? w - p.TRW : w;
@@ -371,10 +373,10 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
           tpair = p.tokens + static_cast<size_t>(r.pair) * pair_rows * kCols;
         }
         float* tb = tpair + (static_cast<size_t>(hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + g;
-        const int fc0 = kPlanesPerWarp * vsub;
 #pragma unroll
         for (int e = 0; e < kPlanesPerWarp; ++e) {
-          const int fc = fc0 + e, f = fc / 3, c = fc - 3 * (fc / 3);
+          // this warp's planes are frame f = vsub, channels c = e (plane index 3f + c)
+          const int f = vsub, c = e;
           const uint32_t lutc = lut_s + c * 1024;
           float* tp = tb + (c * 2 + f) * 196;
           constexpr int VG = KSV == 1 ? 2 : 1;  // patches interleaved per group
@@ -413,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
               st_cs_pred(op + 14, o[1], jok1);
               st_cs_pred(op + 8, o[2], jok0 && xok1);
               st_cs_pred(op + 22, o[3], jok1 && xok1);
-              if (p.dbg_rs != nullptr) {
+              if (DBG && p.dbg_rs != nullptr) {
                 const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
                 for (int ee = 0; ee < 4; ++ee) {
                   const int x = X0 + 14 * q + g + ((ee >= 2) ? 8 : 0), j = j0 + (ee & 1);
@@ -440,9 +442,9 @@ using KernelFn = void (*)(Params);
 
 struct Instance {
   int ksh, ksv;
-  KernelFn fn;
+  KernelFn fn, fn_dbg;  // production / with the parity-test dumps of fc_preprocess_debug
 };
-#define FC_INST(A, B) {A, B, fc_fused_kernel<A, B>},
+#define FC_INST(A, B) {A, B, fc_fused_kernel<A, B, false>, fc_fused_kernel<A, B, true>},
 static const Instance kInstances[] = {FC_INSTANCES(FC_INST)};
 #undef FC_INST
 constexpr int kMaxKS = 4;
@@ -620,7 +622,7 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
 
 struct Geometry {
   int sw, htiles, SWPN, SWP, BW, NX, TR, TRW, nstrips, nchunks;
-  KernelFn fn;
+  KernelFn fn, fn_dbg;
   size_t smem;
 };
 
@@ -671,7 +673,10 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
   g->nchunks = std::min(kmax, (P->meta.height + kChunkRows - 1) / kChunkRows);
   g->fn = nullptr;
   for (const Instance& in : kInstances)
-    if (in.ksh == dt->ksh && in.ksv == dt->ksv) g->fn = in.fn;
+    if (in.ksh == dt->ksh && in.ksv == dt->ksv) {
+      g->fn = in.fn;
+      g->fn_dbg = in.fn_dbg;
+    }
   if (!g->fn) return fail(FC_ERR_UNSUPPORTED, "no kernel instance for this resize window");
   if (dt->ksh <= 2 && 2 * kChunkRows * (g->SWPN / 16) > 2 * kComputeThreads)
     return fail(FC_ERR_UNSUPPORTED, "colour stage: more than 2 items per thread");
@@ -805,7 +810,7 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
     if (st == FC_OK) break;
   }
   if (st != FC_OK) return st;
-  KernelFn fn = g.fn;
+  KernelFn fn = (dbg_src || dbg_rs) ? g.fn_dbg : g.fn;
   e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(g.smem));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
@@ -843,10 +848,7 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   prm.lut = dt->lut;
   prm.dbg_src = dbg_src;
   prm.dbg_rs = dbg_rs;
-  {
-    const char* sk = std::getenv("FC_PROFILE_SKIP");
-    prm.skip = sk ? std::atoi(sk) : 0;
-  }
+  prm.trw_magic = static_cast<uint32_t>(((1ull << 32) + g.TRW - 1) / g.TRW);
   const int64_t nfj = static_cast<int64_t>(jobs[0].frames.size());
   const int64_t nf = nfj * static_cast<int64_t>(jobs.size());
   const long long items = (nf / 2) * static_cast<long long>(g.nstrips) * prm.gh2;
