@@ -9,7 +9,10 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfc.so")
+# FC_LIB_VARIANT (kernel A/B experiments only): load libfc_<variant>.so, a
+# build of the same sources with a change under test, from this directory
+LIB_PATH = os.path.join(HERE, f"libfc_{os.environ['FC_LIB_VARIANT']}.so" if os.environ.get("FC_LIB_VARIANT")
+                        else "libfc.so")
 
 FC_TOKEN_COLS = 1176
 STATUS = {0: "FC_OK", 1: "FC_ERR_INVALID_ARG", 2: "FC_ERR_EMPTY_SELECTION", 3: "FC_ERR_ASPECT_RATIO",

@@ -10,4 +10,5 @@ for c in c1 c3 c4 c5; do timeout 300 python bench.py --config $c --steps 20 --wa
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/$tag/bench_ref.json 2>/dev/null
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 30 --csv --log-file gpurun_out/$tag/ncu_launches_c2.csv python bench.py --steps 10 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:fc_fused -s 3 -c 1 -o gpurun_out/$tag/ncu_full_c2 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:fc_fused -s 3 -c 1 -o gpurun_out/$tag/ncu_full_c4 python bench.py --config c4 --steps 2 --warmup 3 --no-cpu-baseline > /dev/null 2>&1
 ls -la gpurun_out/$tag
