@@ -1,0 +1,37 @@
+# Copy a recorded round (gpurun_out/<tag>, from tools/record.sh <tag>) into profiles/:
+# bench lines, launch list, ncu summaries (+ per-phase/per-line views), traffic JSON.
+set -e
+tag=${1:-r01}
+src=gpurun_out/$tag
+for f in bench_c1 bench_c2 bench_c3 bench_c4 bench_c5 bench_ref; do cp $src/$f.json profiles/${tag}_$f.json; done
+cp $src/ncu_launches_c2.csv profiles/${tag}_ncu_launches_c2.csv
+cp $src/pytest_gpu.txt profiles/${tag}_pytest_gpu.txt
+cp $src/smoke.txt profiles/${tag}_smoke.txt
+cp $src/gpu.txt profiles/${tag}_gpu.txt
+for c in c2 c4; do
+  python tools/ncu_summary.py $src/ncu_full_$c.ncu-rep > profiles/${tag}_ncu_full_${c}_summary.txt
+  python tools/ncu_lines.py $src/ncu_full_$c.ncu-rep 40 > profiles/${tag}_ncu_full_${c}_lines.txt
+  ncu -i $src/ncu_full_$c.ncu-rep --page details --csv > profiles/${tag}_ncu_full_${c}_details.csv
+done
+python - "$tag" <<'PY'
+import csv, io, json, subprocess, sys
+tag = sys.argv[1]
+out = {}
+for c in ("c2", "c4"):
+    rep = f"gpurun_out/{tag}/ncu_full_{c}.ncu-rep"
+    raw = list(csv.reader(io.StringIO(subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"],
+                                                     capture_output=True, text=True).stdout)))
+    h, v, u = raw[0], raw[2], raw[1]
+    def get(n):
+        x = float(v[h.index(n)].replace(",", ""))
+        unit = u[h.index(n)]
+        return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+    b = json.load(open(f"gpurun_out/{tag}/bench_{c}.json"))
+    rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
+    out[c] = {"dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
+              "algorithmic_bytes_per_launch": b["roofline"]["algorithmic_bytes_per_launch"],
+              "kernel_us_under_ncu": get("gpu__time_duration.sum") / (1e3 if u[h.index("gpu__time_duration.sum")] == "nsecond" else 1),
+              "source": f"profiles/{tag}_ncu_full_{c}_summary.txt (ncu --set full --clock-control none, 1 launch)"}
+json.dump(out, open("profiles/ncu_traffic.json", "w"), indent=1)
+print(json.dumps(out, indent=1))
+PY
