@@ -119,20 +119,20 @@ def workload_meta(fc, wl):
     return fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start)
 
 
-def algorithmic_bytes(plan, wl, rank_plan=None):
-    """1.5*W*H read per sampled frame + 12*W'*H' written
-    per frame of the padded sequence (4704 B per token row)."""
+def algorithmic_bytes(plan, wl, rank_plan=None, tok_bytes=4):
+    """1.5*W*H read per sampled frame + 1176 tokens
+    written per token row (4704 B fp32, 2352 B bf16)."""
     if rank_plan is None:
         n = plan.num_sampled
         rows = plan.token_rows
     else:
         n = rank_plan["sampled_count"]
         rows = rank_plan["row_end"] - rank_plan["row_begin"]
-    return int(n * 1.5 * wl.width * wl.height + rows * 1176 * 4)
+    return int(n * 1.5 * wl.width * wl.height + rows * 1176 * tok_bytes)
 
 
 # ------------------------------------------------------------ CPU oracle arm
-def oracle_sample(wl, pairs, nthreads):
+def oracle_sample(wl, pairs, nthreads, matrix="bt601"):
     """Run the oracle (as it stands) on `pairs` temporal pairs of workload wl.
     Returns (seconds, frames)."""
     from oracle import oracle
@@ -141,7 +141,7 @@ def oracle_sample(wl, pairs, nthreads):
     host = synth.frames_nv12(wl, take, "natural")
     h2, w2 = oracle.smart_resize(wl.height, wl.width)
     t0 = time.perf_counter()
-    oracle.preprocess([host[i] for i in take], wl.width, wl.height, w2, h2, nthreads=nthreads)
+    oracle.preprocess([host[i] for i in take], wl.width, wl.height, w2, h2, nthreads=nthreads, matrix=matrix)
     return time.perf_counter() - t0, len(take)
 
 
@@ -190,7 +190,8 @@ def run_ours(args):
     wl = synth.CONFIGS[args.config]
     clips = wl.clips                              # c5: 64 independent requests per step
     meta = workload_meta(fc, wl)
-    cfg = fc.ModelCfg(world_size=world, sample_fps=wl.sample_fps)
+    cfg = fc.ModelCfg(world_size=world, sample_fps=wl.sample_fps, token_dtype=args.tokens, color=args.color)
+    tok_bytes = 2 if args.tokens == "bf16" else 4
     plan0 = fc.Plan(meta, cfg)
     rp = plan0.rank(rank)
     n_all = plan0.num_sampled * clips
@@ -200,10 +201,11 @@ def run_ours(args):
     devs = [synth.to_device(h) for h in hosts]
     surfs = [fc.SurfaceTable.from_tensors(d, wl.num_frames) for d in devs]
     rows = rp["row_end"] - rp["row_begin"]
-    outs = [torch.empty((max(rows, 1), 1176), dtype=torch.float32, device="cuda") for _ in range(clips)]
+    tdt = torch.bfloat16 if args.tokens == "bf16" else torch.float32
+    outs = [torch.empty((max(rows, 1), 1176), dtype=tdt, device="cuda") for _ in range(clips)]
     comm = fc.NcclComm(rank, world) if world > 1 else None
     enc = cfg.encoder_rank
-    fulls = [torch.empty((plan0.token_rows, 1176), dtype=torch.float32, device="cuda")
+    fulls = [torch.empty((plan0.token_rows, 1176), dtype=tdt, device="cuda")
              if (world > 1 and rank == enc) else None for _ in range(clips)]
     stream = torch.cuda.current_stream()
 
@@ -268,7 +270,8 @@ def run_ours(args):
         torch.cuda.synchronize()
         gms = torch.tensor([g0.elapsed_time(g1) / max(3, args.steps // 4)], dtype=torch.float64, device="cuda")
         dist.all_reduce(gms, op=dist.ReduceOp.MAX)
-        gbytes = clips * sum((r["row_end"] - r["row_begin"]) * 1176 * 4 for i, r in enumerate(plan0.ranks()) if i != enc)
+        gbytes = clips * sum((r["row_end"] - r["row_begin"]) * 1176 * tok_bytes for i, r in enumerate(plan0.ranks())
+                             if i != enc)
         gather = {"ms": round(gms.item(), 4), "bytes_into_encoder": gbytes,
                   "GB/s": round(gbytes / (gms.item() * 1e-3) / 1e9, 1), "nvlink_nominal_GB/s": 900,
                   "nvlink_measured_peer_GB/s": 770}
@@ -276,7 +279,7 @@ def run_ours(args):
     # e2e: same step from pinned host buffers through the public API
     pinned = [{k: (torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()) for k, (a, b) in h.items()}
               for h in hosts]
-    res_host = torch.empty((clips, 1176), dtype=torch.float32).pin_memory()
+    res_host = torch.empty((clips, 1176), dtype=tdt).pin_memory()
     h2d = sum(a.numel() + b.numel() for pc in pinned for a, b in pc.values())
     e2e_steps = max(3, min(args.steps, 10))
 
@@ -317,21 +320,22 @@ def run_ours(args):
     if rank == 0:
         peak, peak_kind = load_peaks()
         if world == 1:
-            abytes = clips * algorithmic_bytes(plan0, wl)
+            abytes = clips * algorithmic_bytes(plan0, wl, tok_bytes=tok_bytes)
             kern_for_roof = kern_avg
         else:  # dominant kernel = this rank's launch; bytes of the largest shard
-            abytes = clips * max(algorithmic_bytes(plan0, wl, r) for r in plan0.ranks())
+            abytes = clips * max(algorithmic_bytes(plan0, wl, r, tok_bytes) for r in plan0.ranks())
             kern_for_roof = kern_max
         achieved = abytes / (kern_for_roof * 1e-3) / 1e9
-        traffic = load_traffic(args.config) if world == 1 else None
+        traffic = load_traffic(args.config) if (world == 1 and args.tokens == "f32" and args.color == "bt601") else None
         line = {
             "metric": METRIC, "value": round(n_all / (ms_per_step * 1e-3), 2), "unit": "frames/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8->f32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": f"u8->{args.tokens}",
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {wl.note}", "frames": n_all, "requests": clips,
                        "resized_hw": list(plan0.resized), "grid_thw": list(plan0.grid_thw),
-                       "token_bytes": clips * plan0.token_rows * 1176 * 4, "parallelism": f"gop-dp{world}",
+                       "token_bytes": clips * plan0.token_rows * 1176 * tok_bytes, "parallelism": f"gop-dp{world}",
+                       "color": args.color,
                        "l2": "per-step inputs+outputs (1.19 GB for c2) exceed the 126 MB L2; no flush",
                        "kernel_ms_avg": round(kern_max if world > 1 else kern_avg, 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -339,7 +343,7 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": abytes},
             "gpu_launches": int(launches),  # fc_kernel_launches() delta over the timed region (this rank)
             "e2e": {"value": round(n_all / (e2e_ms * 1e-3), 2), "unit": "frames/s", "ms_per_step": round(e2e_ms, 3),
-                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4704 * clips},
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 1176 * tok_bytes * clips},
             "clocks": clk.summary(),
         }
         if gather is not None:
@@ -347,7 +351,7 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             cores = len(os.sched_getaffinity(0))
             pairs = min(plan0.grid_thw[0], 60)
-            dt, f = oracle_sample(wl, pairs, cores)
+            dt, f = oracle_sample(wl, pairs, cores, args.color)
             line["cpu_baseline"] = {"value": round(f / dt, 3), "unit": "frames/s", "cores": cores,
                                     "kind": "oracle",
                                     "sample": f"{f} sampled frames ({pairs} temporal pairs) of {args.config}, "
@@ -368,6 +372,10 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tokens", default="f32", choices=["f32", "bf16"],
+                    help="token dtype (NEXT-4 variant; the BASELINE metric is f32)")
+    ap.add_argument("--color", default="bt601", choices=["bt601", "bt709", "bt601_full", "bt709_full"],
+                    help="YUV->RGB matrix (NEXT-4 variant; the BASELINE metric is bt601)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define FC_ABI_VERSION 1
+#define FC_ABI_VERSION 2  /* 2: token_dtype + color in fc_model_cfg; tokens as void* */
 #define FC_TOKEN_COLS 1176 /* 3 channels * 2 (temporal patch) * 14 * 14 */
 
 typedef enum {
@@ -76,6 +76,24 @@ typedef struct {
  * EXPLICIT = caller-given strictly increasing list (odd counts are padded). */
 typedef enum { FC_SAMPLE_FPS_STRIDE = 0, FC_SAMPLE_LINSPACE = 1, FC_SAMPLE_EXPLICIT = 2 } fc_sampling;
 
+/* Token element type.  F32 is the HF processor's output
+ * (the default, and what every BASELINE config measures).  BF16 is the fp32
+ * token rounded to nearest-even bfloat16 -- exactly torch's
+ * `.to(torch.bfloat16)` of the F32 result -- for encoders that consume bf16;
+ * it halves the token bytes written (reading R16). */
+typedef enum { FC_TOKENS_F32 = 0, FC_TOKENS_BF16 = 1 } fc_token_dtype;
+
+/* YUV -> RGB matrix (reading R3 for the default; R15 for the variants):
+ * 8-bit fixed point, out = clamp((cY*(Y - y0) + cU*(U-128) + cV*(V-128) + 128) >> 8)
+ * with the coefficients round(256 * the standard matrix entry), the limited
+ * ("TV", Y in [16,235]) or full ("PC", JPEG) range, nearest 2x2 chroma. */
+typedef enum {
+  FC_COLOR_BT601_LIMITED = 0, /* 298, 409 / -100, -208 / 516 (default, R3) */
+  FC_COLOR_BT709_LIMITED = 1, /* 298, 459 / -55, -136 / 541 */
+  FC_COLOR_BT601_FULL = 2,    /* 256, 359 / -88, -183 / 454 */
+  FC_COLOR_BT709_FULL = 3     /* 256, 403 / -48, -120 / 475 */
+} fc_color;
+
 /* Model / preprocessing configuration (Qwen2-VL video processor defaults,
  * filled by fc_model_cfg_default). */
 typedef struct {
@@ -99,6 +117,8 @@ typedef struct {
   double rescale_factor;       /* 1/255 */
   int32_t world_size;          /* W >= 1: GPUs the request is partitioned over */
   int32_t encoder_rank;        /* rank that receives the gathered tokens (default 0) */
+  fc_token_dtype token_dtype;  /* FC_TOKENS_F32 (default) or FC_TOKENS_BF16 */
+  fc_color color;              /* FC_COLOR_BT601_LIMITED (default) */
 } fc_model_cfg;
 
 void fc_model_cfg_default(fc_model_cfg* cfg);
@@ -163,26 +183,27 @@ typedef struct {
 
 /* fc_preprocess -- Alg. 1 l.21-22 (convert_AVframes_to_tensor_and_resize)
  * for rank `rank`: one fused kernel launch on `stream` computing, for the
- * rank's sampled frames, NV12 -> BT.601 RGB (R3) -> Pillow bicubic resize (R4)
- * -> rescale + normalise (R5) -> temporal pad + 14x14x2 patchify in 2x2 merge
- * order (R6).
+ * rank's sampled frames, NV12 -> RGB (cfg.color; BT.601 limited by default,
+ * R3) -> Pillow bicubic resize (R4) -> rescale + normalise (R5) -> temporal
+ * pad + 14x14x2 patchify in 2x2 merge order (R6).
  *   surfaces:     host array of num_surfaces descriptors indexed by GLOBAL
  *                 frame index (0..N-1); entries this rank does not read may
  *                 have NULL pointers (FC_ERR_MISSING_SURFACE otherwise).
- *   tokens:       device pointer, (row_end-row_begin) x 1176 fp32, contiguous.
+ *   tokens:       device pointer, (row_end-row_begin) x 1176 elements of
+ *                 cfg.token_dtype (fp32 by default, or bf16), contiguous.
  *   grid_thw:     host out (3 values) or NULL.
  *   stream:       cudaStream_t (0 = legacy default stream).
  * Asynchronous: returns after enqueueing.  Validation happens before any
  * launch.  A rank with no rows returns FC_OK without launching. */
 fc_status fc_preprocess(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
-                        int64_t num_surfaces, float* tokens, int64_t grid_thw[3], void* stream);
+                        int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream);
 
 /* Same, additionally dumping the integer intermediates for parity tests:
  *   rgb_src:     device u8 [n_r, H, W, 3]  (BT.601 output) or NULL
  *   rgb_resized: device u8 [n_r, H', W', 3] (resize output)  or NULL
  * where n_r = the rank's frames including padding, in order. */
 fc_status fc_preprocess_debug(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
-                              int64_t num_surfaces, float* tokens, int64_t grid_thw[3], void* stream,
+                              int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream,
                               uint8_t* rgb_src, uint8_t* rgb_resized);
 
 /* Throughput mode (config 5): `count` independent (plan, rank) jobs on
@@ -196,7 +217,7 @@ fc_status fc_preprocess_debug(const fc_plan_t* plan, int32_t rank, const fc_nv12
  * new launch.  Results equal per-job fc_preprocess calls bit for bit. */
 fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* ranks, int32_t count,
                               const fc_nv12_surface* const* surfaces, const int64_t* num_surfaces,
-                              float* const* tokens, void* stream);
+                              void* const* tokens, void* stream);
 
 /* ---- exchange: gather row shards to the encoder rank ---- */
 
@@ -210,12 +231,13 @@ fc_status fc_nccl_comm_destroy(void* comm);
 
 /* fc_gather -- gatherv of every rank's contiguous row shard into the encoder
  * rank's full token buffer (grouped ncclSend/ncclRecv, R9):
- *   shard: device pointer, this rank's (row_end-row_begin) x 1176 fp32
- *   full:  encoder rank: device pointer token_rows x 1176 fp32 (its own shard
+ *   shard: device pointer, this rank's (row_end-row_begin) x 1176 tokens
+ *          (element type cfg.token_dtype)
+ *   full:  encoder rank: device pointer token_rows x 1176 tokens (its own shard
  *          is copied in with cudaMemcpyAsync unless shard already aliases
  *          full + row_begin*1176); other ranks: ignored (may be NULL).
  * Collective: every rank of the plan's world must call it.  Async on stream. */
-fc_status fc_gather(const fc_plan_t* plan, int32_t rank, void* comm, const float* shard, float* full,
+fc_status fc_gather(const fc_plan_t* plan, int32_t rank, void* comm, const void* shard, void* full,
                     void* stream);
 
 const char* fc_status_string(fc_status s);

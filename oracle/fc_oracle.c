@@ -16,6 +16,10 @@
  *   oracle_nv12_to_rgb      O7  integer BT.601 limited range.
  *                               Pinned: exhaustive 2^24 closed-form check
  *                               against float BT.601 (<=1 LSB) + colour bars.
+ *   oracle_yuv_pixel        R15 variants (BT.709, full range; NEXT-4).
+ *                               Pinned: exhaustive 2^24 vs the float matrix
+ *                               from (Kr, Kb) (<=2 LSB), black/white/grey
+ *                               points, matrix 0 == oracle_bt601_pixel.
  *   oracle_resize_bicubic   O8  Pillow 12 ImagingResample BICUBIC, 8bpc path
  *                               (SURVEY D4).  Pinned: bit-exact vs
  *                               PIL.Image.resize on many shapes.
@@ -57,15 +61,61 @@ void oracle_bt601_pixel(int Y, int U, int V, uint8_t* rgb) {
   rgb[2] = (uint8_t)clamp255(floor_div256(298 * C + 516 * D + 128));
 }
 
-void oracle_nv12_to_rgb(const uint8_t* y, int64_t pitch_y, const uint8_t* uv, int64_t pitch_uv,
-                        int width, int height, uint8_t* rgb /* height*width*3 */) {
+/* Reading R15 (SURVEY 8(f) NEXT-4 variants; the paper is silent): the same
+ * 8-bit fixed-point form for other matrices.  From the standard's luma
+ * weights (Kr, Kb), Kg = 1-Kr-Kb, and the range (limited: Y scale 255/219,
+ * chroma scale 255/224, Y offset 16; full: 1, 1, 0):
+ *   R = Y + 2(1-Kr) E,  G = Y - 2(1-Kb)Kb/Kg D - 2(1-Kr)Kr/Kg E,  B = Y + 2(1-Kb) D,
+ * every coefficient scaled by 256 and rounded to the nearest integer, then
+ *   out = clamp((cY*(Y-y0) + cU*(U-128) + cV*(V-128) + 128) >> 8).
+ * matrix: 0 BT.601 limited (== oracle_bt601_pixel), 1 BT.709 limited,
+ * 2 BT.601 full, 3 BT.709 full. */
+void oracle_yuv_coeffs(int matrix, int* k /* cY, y0, cRV, cGU, cGV, cBU */) {
+  const double kr = (matrix == 1 || matrix == 3) ? 0.2126 : 0.299;
+  const double kb = (matrix == 1 || matrix == 3) ? 0.0722 : 0.114;
+  const double kg = 1.0 - kr - kb;
+  const int limited = matrix <= 1;
+  const double ys = limited ? 255.0 / 219.0 : 1.0;
+  const double cs = limited ? 255.0 / 224.0 : 1.0;
+  k[0] = (int)lround(256.0 * ys);
+  k[1] = limited ? 16 : 0;
+  k[2] = (int)lround(256.0 * 2.0 * (1.0 - kr) * cs);
+  k[3] = (int)lround(-256.0 * 2.0 * (1.0 - kb) * kb / kg * cs);
+  k[4] = (int)lround(-256.0 * 2.0 * (1.0 - kr) * kr / kg * cs);
+  k[5] = (int)lround(256.0 * 2.0 * (1.0 - kb) * cs);
+}
+
+void oracle_yuv_pixel(int Y, int U, int V, int matrix, uint8_t* rgb) {
+  int k[6];
+  oracle_yuv_coeffs(matrix, k);
+  int C = Y - k[1], D = U - 128, E = V - 128;
+  rgb[0] = (uint8_t)clamp255(floor_div256(k[0] * C + k[2] * E + 128));
+  rgb[1] = (uint8_t)clamp255(floor_div256(k[0] * C + k[3] * D + k[4] * E + 128));
+  rgb[2] = (uint8_t)clamp255(floor_div256(k[0] * C + k[5] * D + 128));
+}
+
+/* every (Y, U, V) -> out[((Y*256 + U)*256 + V)*3 + c], for the exhaustive pins */
+void oracle_yuv_table(int matrix, uint8_t* out) {
+  for (int Y = 0; Y < 256; ++Y)
+    for (int U = 0; U < 256; ++U)
+      for (int V = 0; V < 256; ++V) oracle_yuv_pixel(Y, U, V, matrix, out + (((size_t)Y * 256 + U) * 256 + V) * 3);
+}
+
+void oracle_nv12_to_rgb_m(const uint8_t* y, int64_t pitch_y, const uint8_t* uv, int64_t pitch_uv,
+                          int width, int height, int matrix, uint8_t* rgb /* height*width*3 */) {
   for (int r = 0; r < height; ++r)
     for (int c = 0; c < width; ++c) {
       int Y = y[(int64_t)r * pitch_y + c];
       int U = uv[(int64_t)(r / 2) * pitch_uv + 2 * (c / 2) + 0];
       int V = uv[(int64_t)(r / 2) * pitch_uv + 2 * (c / 2) + 1];
-      oracle_bt601_pixel(Y, U, V, rgb + ((int64_t)r * width + c) * 3);
+      if (matrix == 0) oracle_bt601_pixel(Y, U, V, rgb + ((int64_t)r * width + c) * 3);
+      else oracle_yuv_pixel(Y, U, V, matrix, rgb + ((int64_t)r * width + c) * 3);
     }
+}
+
+void oracle_nv12_to_rgb(const uint8_t* y, int64_t pitch_y, const uint8_t* uv, int64_t pitch_uv,
+                        int width, int height, uint8_t* rgb /* height*width*3 */) {
+  oracle_nv12_to_rgb_m(y, pitch_y, uv, pitch_uv, width, height, 0, rgb);
 }
 
 /* ------------------------------------------------------------------ O8 -- */
@@ -249,6 +299,7 @@ typedef struct {
   uint8_t* rgb_src; /* optional n*h*w*3 */
   uint8_t* rgb_rs;  /* n*h2*w2*3 */
   int nthreads, tid;
+  int matrix;
   int status;
 } job_t;
 
@@ -257,7 +308,7 @@ static void* frame_worker(void* arg) {
   uint8_t* src = (uint8_t*)malloc((size_t)j->h * j->w * 3);
   if (!src) { j->status = -1; return NULL; }
   for (int64_t f = j->tid; f < j->n; f += j->nthreads) {
-    oracle_nv12_to_rgb(j->y[f], j->pitch_y[f], j->uv[f], j->pitch_uv[f], j->w, j->h, src);
+    oracle_nv12_to_rgb_m(j->y[f], j->pitch_y[f], j->uv[f], j->pitch_uv[f], j->w, j->h, j->matrix, src);
     if (j->rgb_src) memcpy(j->rgb_src + (size_t)f * j->h * j->w * 3, src, (size_t)j->h * j->w * 3);
     if (oracle_resize_bicubic(src, j->w, j->h, j->w2, j->h2, j->rgb_rs + (size_t)f * j->h2 * j->w2 * 3) != 0)
       j->status = -1;
@@ -270,7 +321,7 @@ static void* frame_worker(void* arg) {
 int oracle_preprocess(const uint8_t* const* y, const uint8_t* const* uv, const int64_t* pitch_y,
                       const int64_t* pitch_uv, int64_t n, int w, int h, int w2, int h2,
                       const float* mean, const float* std, double rescale, float* tokens,
-                      uint8_t* rgb_src, uint8_t* rgb_rs, int nthreads) {
+                      uint8_t* rgb_src, uint8_t* rgb_rs, int nthreads, int matrix) {
   if (n <= 0 || w2 % 28 || h2 % 28) return -1;
   if (nthreads < 1) nthreads = 1;
   uint8_t* rs = rgb_rs ? rgb_rs : (uint8_t*)malloc((size_t)n * h2 * w2 * 3);
@@ -279,7 +330,7 @@ int oracle_preprocess(const uint8_t* const* y, const uint8_t* const* uv, const i
   pthread_t* th = (pthread_t*)calloc(nthreads, sizeof(pthread_t));
   int status = 0;
   for (int i = 0; i < nthreads; ++i) {
-    job_t j = {y, uv, pitch_y, pitch_uv, n, w, h, w2, h2, rgb_src, rs, nthreads, i, 0};
+    job_t j = {y, uv, pitch_y, pitch_uv, n, w, h, w2, h2, rgb_src, rs, nthreads, i, matrix, 0};
     jobs[i] = j;
     if (nthreads == 1) frame_worker(&jobs[i]);
     else pthread_create(&th[i], NULL, frame_worker, &jobs[i]);

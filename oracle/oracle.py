@@ -76,7 +76,10 @@ def lib():
         L.oracle_preprocess.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p,
-                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+        L.oracle_yuv_coeffs.argtypes = [ctypes.c_int, ctypes.c_void_p]
+        L.oracle_yuv_pixel.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p]
+        L.oracle_yuv_table.argtypes = [ctypes.c_int, ctypes.c_void_p]
         L.oracle_preprocess.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -269,6 +272,30 @@ def bt601_pixel(Y: int, U: int, V: int) -> tuple[int, int, int]:
     return tuple(o)
 
 
+MATRICES = {"bt601": 0, "bt709": 1, "bt601_full": 2, "bt709_full": 3}
+
+
+def yuv_coeffs(matrix: str) -> tuple[int, ...]:
+    """R15: (cY, y0, cRV, cGU, cGV, cBU) of a colour matrix."""
+    k = np.empty(6, np.int32)
+    lib().oracle_yuv_coeffs(MATRICES[matrix], _ptr(k))
+    return tuple(int(x) for x in k)
+
+
+def yuv_table(matrix: str) -> np.ndarray:
+    """Every (Y, U, V) through oracle_yuv_pixel: [256, 256, 256, 3] u8."""
+    out = np.empty((256, 256, 256, 3), np.uint8)
+    lib().oracle_yuv_table(MATRICES[matrix], _ptr(out))
+    return out
+
+
+def to_bf16(x: np.ndarray) -> np.ndarray:
+    """R16: fp32 -> bfloat16 bits, round to nearest, ties to even (finite
+    inputs): keep the top 16 bits of b + 0x7FFF + (bit 16 of b)."""
+    b = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
+    return ((b + 0x7FFF + ((b >> 16) & 1)) >> 16).astype(np.uint16)
+
+
 def resize_bicubic(rgb: np.ndarray, w2: int, h2: int) -> np.ndarray:
     """O8 Pillow-exact bicubic on an [H, W, 3] u8 image."""
     rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
@@ -308,7 +335,7 @@ def tokens_from_resized(rs: np.ndarray, mean=CLIP_MEAN, std=CLIP_STD, rescale: f
 
 def preprocess(frames: list[tuple[np.ndarray, np.ndarray]], width: int, height: int, w2: int, h2: int,
                mean=CLIP_MEAN, std=CLIP_STD, rescale: float = 1 / 255, want_rgb: bool = False,
-               nthreads: int = 1):
+               nthreads: int = 1, matrix: str = "bt601"):
     """O7..O11 end to end on the *sampled* frames (in order), each a pair
     (y [H, pitch_y] u8, uv [H/2, pitch_uv] u8).  Returns tokens
     [ceil(n/2)*gh*gw, 1176] f32 (and the RGB dumps if ``want_rgb``)."""
@@ -327,7 +354,7 @@ def preprocess(frames: list[tuple[np.ndarray, np.ndarray]], width: int, height: 
     s = np.array(std, np.float32)
     st = lib().oracle_preprocess(yp, uvp, _ptr(py), _ptr(puv), n, width, height, w2, h2, _ptr(m), _ptr(s),
                                  rescale, _ptr(tokens), _ptr(rgb_src) if want_rgb else None, _ptr(rgb_rs),
-                                 nthreads)
+                                 nthreads, MATRICES[matrix])
     if st != 0:
         raise RuntimeError("oracle_preprocess failed")
     if want_rgb:

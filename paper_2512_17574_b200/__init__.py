@@ -62,6 +62,8 @@ class ModelCfg:
     image_mean: tuple[float, float, float] | None = None
     image_std: tuple[float, float, float] | None = None
     rescale_factor: float | None = None
+    token_dtype: str = "f32"        # "f32" (HF output) | "bf16" (R16: RNE of the f32 token)
+    color: str = "bt601"            # "bt601" (R3) | "bt709" | "bt601_full" | "bt709_full" (R15)
 
     def to_c(self):
         c = _native.ModelCfgC()
@@ -69,6 +71,8 @@ class ModelCfg:
         c.world_size = self.world_size
         c.encoder_rank = self.encoder_rank
         c.sampling = _native.SAMPLING[self.sampling]
+        c.token_dtype = _native.TOKEN_DTYPES[self.token_dtype]
+        c.color = _native.COLORS[self.color]
         c.sample_fps = self.sample_fps
         c.num_frames = self.num_frames
         c.min_frames = self.min_frames
@@ -171,6 +175,11 @@ def _stream_ptr(stream) -> ctypes.c_void_p:
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def _tok_dtype(plan: Plan):
+    import torch
+    return torch.bfloat16 if plan.cfg.token_dtype == "bf16" else torch.float32
+
+
 def _rank_rows(plan: Plan, rank: int) -> int:
     rp = plan.rank(rank)
     return rp["row_end"] - rp["row_begin"]
@@ -183,7 +192,7 @@ def preprocess(plan: Plan, rank: int, surfaces: SurfaceTable, out=None, stream=N
     import torch
     rows = _rank_rows(plan, rank)
     if out is None:
-        out = torch.empty((rows, FC_TOKEN_COLS), dtype=torch.float32, device="cuda")
+        out = torch.empty((rows, FC_TOKEN_COLS), dtype=_tok_dtype(plan), device="cuda")
     grid = (ctypes.c_int64 * 3)()
     check(lib().fc_preprocess(plan.handle, rank, surfaces.arr, surfaces.n, ctypes.c_void_p(out.data_ptr()), grid,
                               _stream_ptr(stream)), "fc_preprocess")
@@ -215,7 +224,7 @@ def preprocess_batch(jobs: Sequence[tuple[Plan, int, SurfaceTable]], outs=None, 
     import torch
     n = len(jobs)
     if outs is None:
-        outs = [torch.empty((_rank_rows(p, r), FC_TOKEN_COLS), dtype=torch.float32, device="cuda")
+        outs = [torch.empty((_rank_rows(p, r), FC_TOKEN_COLS), dtype=_tok_dtype(p), device="cuda")
                 for p, r, _ in jobs]
     plans = (ctypes.c_void_p * n)(*[p.handle.value for p, _, _ in jobs])
     ranks = (ctypes.c_int32 * n)(*[r for _, r, _ in jobs])
@@ -260,7 +269,7 @@ def gather(plan: Plan, rank: int, comm: NcclComm | None, shard, full=None, strea
     import torch
     enc = plan.cfg.encoder_rank
     if rank == enc and full is None:
-        full = torch.empty((plan.token_rows, FC_TOKEN_COLS), dtype=torch.float32, device="cuda")
+        full = torch.empty((plan.token_rows, FC_TOKEN_COLS), dtype=_tok_dtype(plan), device="cuda")
     check(lib().fc_gather(plan.handle, rank, comm.handle if comm else None,
                           ctypes.c_void_p(shard.data_ptr()) if shard is not None else None,
                           ctypes.c_void_p(full.data_ptr()) if full is not None else None,

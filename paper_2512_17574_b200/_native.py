@@ -19,6 +19,8 @@ STATUS = {0: "FC_OK", 1: "FC_ERR_INVALID_ARG", 2: "FC_ERR_EMPTY_SELECTION", 3: "
           4: "FC_ERR_UNSUPPORTED", 5: "FC_ERR_MISSING_SURFACE", 6: "FC_ERR_RANK", 7: "FC_ERR_OOM",
           8: "FC_ERR_CUDA", 9: "FC_ERR_NCCL"}
 SAMPLING = {"fps_stride": 0, "linspace": 1, "explicit": 2}
+TOKEN_DTYPES = {"f32": 0, "bf16": 1}
+COLORS = {"bt601": 0, "bt709": 1, "bt601_full": 2, "bt709_full": 3}
 
 
 class FcError(RuntimeError):
@@ -46,7 +48,7 @@ class ModelCfgC(ctypes.Structure):
                 ("resized_height", ctypes.c_int32), ("resized_width", ctypes.c_int32),
                 ("image_mean", ctypes.c_float * 3), ("image_std", ctypes.c_float * 3),
                 ("rescale_factor", ctypes.c_double), ("world_size", ctypes.c_int32),
-                ("encoder_rank", ctypes.c_int32)]
+                ("encoder_rank", ctypes.c_int32), ("token_dtype", ctypes.c_int), ("color", ctypes.c_int)]
 
 
 class PlanInfoC(ctypes.Structure):

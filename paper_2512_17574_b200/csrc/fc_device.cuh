@@ -118,31 +118,30 @@ __device__ __forceinline__ int fir_sum(const uint32_t (&d)[NW], const uint32_t (
   return static_cast<int>(s);
 }
 
-// Integer BT.601 limited range (R3) on 4 pixels.  yw = Y0..Y3 bytes, uvw =
+// Integer YUV -> RGB (R3 BT.601 limited by default; R15 variants) on 4 pixels.  yw = Y0..Y3 bytes, uvw =
 // U0 V0 U1 V1 (the chroma samples of pixels {0,1} and {2,3}).  With the
 // constants folding C=Y-16, D=U-128, E=V-128 and the +128 rounding:
 //   R = (298Y + 409V - 56992) >> 8, G = (298Y - 100U - 208V + 34784) >> 8,
 //   B = (298Y + 516U - 70688) >> 8, each saturated to [0,255].
 // dp2a forms the two-term dot products straight from byte lanes; the
 // saturating pack does the clamp.  Returns one word per channel.
-__device__ __forceinline__ void bt601_4(uint32_t yw, uint32_t uvw, uint32_t& R, uint32_t& G, uint32_t& B) {
-  const uint32_t kR = (409u << 16) | 298u;
-  const uint32_t kB = (516u << 16) | 298u;
-  const uint32_t kG = ((0x10000u - 100u) << 16) | 298u;   // (298, -100)
-  const uint32_t kGv = (0x10000u - 208u) << 16;           // (0, -208)
+__device__ __forceinline__ void yuv2rgb_4(uint32_t yw, uint32_t uvw, uint32_t& R, uint32_t& G, uint32_t& B,
+                                          uint32_t kR, uint32_t kG, uint32_t kGv, uint32_t kB, int bR, int bG,
+                                          int bB) {
+  // kR = (cRV << 16) | cY, kB = (cBU << 16) | cY, kG = (cGU << 16) | cY, kGv = cGV << 16 (s16 halves)
   // byte words: [Y0 V0 Y1 V0], [Y2 V1 Y3 V1], [Y0 U0 Y1 U0], [Y2 U1 Y3 U1]
   const uint32_t yv01 = __byte_perm(yw, uvw, 0x5150);
   const uint32_t yv23 = __byte_perm(yw, uvw, 0x7372);
   const uint32_t yu01 = __byte_perm(yw, uvw, 0x4140);
   const uint32_t yu23 = __byte_perm(yw, uvw, 0x6362);
-  const int g0 = dp2a_lo(kGv, yv01, 34784);  // -208*V0 + 34784
-  const int g1 = dp2a_lo(kGv, yv23, 34784);
+  const int g0 = dp2a_lo(kGv, yv01, bG);  // cGV*V0 + bias
+  const int g1 = dp2a_lo(kGv, yv23, bG);
   // t -> clamp(t >> 8, 0, 255) == byte 1 of sat_u16(t): pack two saturated
   // halves, then gather the high bytes of four values with one PRMT.
-  const uint32_t r01 = pack_sat_u16(dp2a_hi(kR, yv01, -56992), dp2a_lo(kR, yv01, -56992));
-  const uint32_t r23 = pack_sat_u16(dp2a_hi(kR, yv23, -56992), dp2a_lo(kR, yv23, -56992));
-  const uint32_t b01 = pack_sat_u16(dp2a_hi(kB, yu01, -70688), dp2a_lo(kB, yu01, -70688));
-  const uint32_t b23 = pack_sat_u16(dp2a_hi(kB, yu23, -70688), dp2a_lo(kB, yu23, -70688));
+  const uint32_t r01 = pack_sat_u16(dp2a_hi(kR, yv01, bR), dp2a_lo(kR, yv01, bR));
+  const uint32_t r23 = pack_sat_u16(dp2a_hi(kR, yv23, bR), dp2a_lo(kR, yv23, bR));
+  const uint32_t b01 = pack_sat_u16(dp2a_hi(kB, yu01, bB), dp2a_lo(kB, yu01, bB));
+  const uint32_t b23 = pack_sat_u16(dp2a_hi(kB, yu23, bB), dp2a_lo(kB, yu23, bB));
   const uint32_t g01 = pack_sat_u16(dp2a_hi(kG, yu01, g0), dp2a_lo(kG, yu01, g0));
   const uint32_t g23 = pack_sat_u16(dp2a_hi(kG, yu23, g1), dp2a_lo(kG, yu23, g1));
   R = __byte_perm(r01, r23, 0x7531);
@@ -232,10 +231,15 @@ __device__ __forceinline__ float ldsf(uint32_t addr) {
   return v;
 }
 
-// predicated streaming store (no branch)
-__device__ __forceinline__ void st_cs_pred(float* p, float v, bool pred) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.f32 [%0], %1;\n}" ::"l"(p), "f"(v),
+// predicated streaming stores (no branch) of one token: fp32 bits / bf16 bits
+__device__ __forceinline__ void st_cs_pred(float* p, uint32_t v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.cs.b32 [%0], %1;\n}" ::"l"(p), "r"(v),
                "r"(static_cast<int>(pred))
+               : "memory");
+}
+__device__ __forceinline__ void st_cs_pred(uint16_t* p, uint32_t v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\t.reg .b16 h;\n\tsetp.ne.b32 q, %2, 0;\n\tcvt.u16.u32 h, %1;\n\t@q st.global.cs.b16 [%0], h;\n}" ::"l"(p),
+               "r"(v), "r"(static_cast<int>(pred))
                : "memory");
 }
 

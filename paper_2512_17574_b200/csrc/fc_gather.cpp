@@ -50,20 +50,23 @@ fc_status fc_nccl_comm_destroy(void* comm) {
   return FC_OK;
 }
 
-fc_status fc_gather(const fc_plan_t* P, int32_t rank, void* comm, const float* shard, float* full, void* stream) {
+fc_status fc_gather(const fc_plan_t* P, int32_t rank, void* comm, const void* shard, void* full, void* stream) {
   if (!P) return fail(FC_ERR_INVALID_ARG, "plan is NULL");
   if (rank < 0 || rank >= P->world) return fail(FC_ERR_RANK, "rank outside [0, world_size)");
   const int e = P->cfg.encoder_rank;
   const fc_rank_plan& me = P->ranks[rank].p;
-  const size_t my_elems = static_cast<size_t>(me.row_end - me.row_begin) * kCols;
+  // rows are exchanged as bytes: 1176 tokens x (4 B fp32 | 2 B bf16)
+  const size_t row_bytes = static_cast<size_t>(kCols) * (P->cfg.token_dtype == FC_TOKENS_BF16 ? 2 : 4);
+  const size_t my_bytes = static_cast<size_t>(me.row_end - me.row_begin) * row_bytes;
+  uint8_t* fullb = static_cast<uint8_t*>(full);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (rank == e && !full) return fail(FC_ERR_INVALID_ARG, "encoder rank needs the full buffer");
-  if (my_elems && !shard) return fail(FC_ERR_INVALID_ARG, "shard is NULL");
+  if (my_bytes && !shard) return fail(FC_ERR_INVALID_ARG, "shard is NULL");
   if (P->world > 1 && !comm) return fail(FC_ERR_INVALID_ARG, "comm is NULL with world_size > 1");
-  if (rank == e && my_elems) {
-    float* dst = full + static_cast<size_t>(me.row_begin) * kCols;
+  if (rank == e && my_bytes) {
+    uint8_t* dst = fullb + static_cast<size_t>(me.row_begin) * row_bytes;
     if (dst != shard) {
-      cudaError_t ce = cudaMemcpyAsync(dst, shard, my_elems * sizeof(float), cudaMemcpyDeviceToDevice, s);
+      cudaError_t ce = cudaMemcpyAsync(dst, shard, my_bytes, cudaMemcpyDeviceToDevice, s);
       if (ce != cudaSuccess) return fail(FC_ERR_CUDA, std::string("own shard copy: ") + cudaGetErrorString(ce));
     }
   }
@@ -75,13 +78,13 @@ fc_status fc_gather(const fc_plan_t* P, int32_t rank, void* comm, const float* s
     for (int p = 0; p < P->world; ++p) {
       if (p == e) continue;
       const fc_rank_plan& rp = P->ranks[p].p;
-      const size_t n = static_cast<size_t>(rp.row_end - rp.row_begin) * kCols;
+      const size_t n = static_cast<size_t>(rp.row_end - rp.row_begin) * row_bytes;
       if (!n) continue;
-      r = ncclRecv(full + static_cast<size_t>(rp.row_begin) * kCols, n, ncclFloat, p, c, s);
+      r = ncclRecv(fullb + static_cast<size_t>(rp.row_begin) * row_bytes, n, ncclUint8, p, c, s);
       if (r != ncclSuccess) break;
     }
-  } else if (my_elems) {
-    r = ncclSend(shard, my_elems, ncclFloat, e, c, s);
+  } else if (my_bytes) {
+    r = ncclSend(shard, my_bytes, ncclUint8, e, c, s);
   }
   ncclResult_t r2 = ncclGroupEnd();
   if (r != ncclSuccess) return nccl_fail(r, "ncclSend/ncclRecv");

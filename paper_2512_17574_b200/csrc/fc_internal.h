@@ -49,7 +49,7 @@ struct DeviceTables {
   int32_t* vcnt = nullptr;     // V taps per output row
   int32_t* vys = nullptr;      // V window start per (band, 8-row group)
   uint32_t* vfr = nullptr;     // V B fragments
-  float* lut = nullptr;        // 3 x 256 normalisation table (R5)
+  uint32_t* lut = nullptr;     // 3 x 256 normalisation table (R5), token-dtype bits
 };
 
 }  // namespace fc
@@ -68,6 +68,7 @@ struct fc_plan_s {
   // horizontal (W -> W'), vertical (H -> H'); shared, immutable, cached per (in, out)
   std::shared_ptr<const fc::AxisTable> th, tv;
   std::vector<float> lut;    // 3 x 256 (R5)
+  std::vector<uint32_t> lut_dev;  // what the kernel stores: fp32 bits, or bf16 bits (R16)
   std::mutex mu;             // guards dev
   std::unordered_map<int, fc::DeviceTables> dev;
 };

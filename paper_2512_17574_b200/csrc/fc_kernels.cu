@@ -31,6 +31,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <unordered_map>
 #include <vector>
 
@@ -72,15 +73,17 @@ struct Params {
   const int32_t* vcnt;
   const int32_t* vys;   // V MMA groups: 4-aligned window start per (band, group of 8 rows)
   const uint32_t* vfr;  // V MMA groups: B fragments [group][KS][3][32][2]
-  const float* lut;
-  float* tokens;      // first token row of this launch's first pair
+  const uint32_t* lut;  // 3 x 256 token bits (fp32, or bf16 zero-extended)
+  uint32_t ckR, ckG, ckGv, ckB;  // colour matrix (R3/R15): packed s16 (Y, chroma) coefficient pairs for dp2a
+  int cbR, cbG, cbB;             // colour biases: -y0*cY - 128*(chroma coefficients) + 128
+  void* tokens;       // first token row of this launch's first pair
   uint8_t* dbg_src;   // [nframes_total, H, W, 3] or null
   uint8_t* dbg_rs;    // [nframes_total, H2, W2, 3] or null
   int frame_base;     // index of fr[0] within the rank's frame list (debug dumps)
   uint32_t trw_magic;  // ceil(2^32 / TRW): x mod TRW = x - TRW * umulhi(x, magic) for the row words used
   int nframes;
   int ppj;            // pairs per job (batch launches; == npairs for one job)
-  float* const* tokj; // device: per-job token base (batch launches) or null -> tokens
+  void* const* tokj;  // device: per-job token base (batch launches) or null -> tokens
   const CUtensorMap* tmg;  // device copy of the maps (launches past kMaxInlineFrames frames) or null -> tm
   CUtensorMap tm[2 * kMaxInlineFrames];  // per frame: Y plane (box BW x 16), UV plane (box BW x 8)
 };
@@ -133,14 +136,14 @@ __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, 
 // Work items are (pair, strip, band) triples; CTA b takes [b*T/G, (b+1)*T/G).
 // Strips are whole merge blocks, so every token row is written by one CTA in
 // one band (no partial-sector merging across CTAs in L2).
-template <int KSH, int KSV, bool DBG>
+template <int KSH, int KSV, bool DBG, int TOK>
 __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_constant__ Params p) {
   constexpr int SW = kStrip;
   constexpr int CH = kChunkRows;
   constexpr int RS = kRingStride;
 
   extern __shared__ __align__(1024) uint8_t smem[];
-  float* lut = reinterpret_cast<float*>(smem);                    // 3 x 256 f32 at offset 0
+  uint32_t* lut = reinterpret_cast<uint32_t*>(smem);              // 3 x 256 token bits at offset 0
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + 3072);      // kStages full barriers
   const int RAWF = 24 * p.BW * p.NX;                              // raw bytes per frame per stage
   uint8_t* raw = smem + 3072 + 128;                               // [kStages][2 f][Y boxes | UV boxes]
@@ -245,10 +248,10 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
             const uint4 Yv = *reinterpret_cast<const uint4*>(rawb + oy);
             const uint4 UVv = *reinterpret_cast<const uint4*>(rawb + ouv);
             uint4 Rv, Gv, Bv;
-            bt601_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x);
-            bt601_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y);
-            bt601_4(Yv.z, UVv.z, Rv.z, Gv.z, Bv.z);
-            bt601_4(Yv.w, UVv.w, Rv.w, Gv.w, Bv.w);
+            yuv2rgb_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
+            yuv2rgb_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
+            yuv2rgb_4(Yv.z, UVv.z, Rv.z, Gv.z, Bv.z, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
+            yuv2rgb_4(Yv.w, UVv.w, Rv.w, Gv.w, Bv.w, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
             uint8_t* dst = rgb + orgb;
             *reinterpret_cast<uint4*>(dst) = Rv;
             *reinterpret_cast<uint4*>(dst + CH * SWP) = Gv;
@@ -365,20 +368,21 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
         // column offset (X0 + 14 q): merge block wb = (X0/28) + q/2, sub-block wm = q&1
         // first token row of this pair (R6: a job's pairs are consecutive gh*gw-row blocks)
         const size_t pair_rows = static_cast<size_t>(p.gh2) * p.gw2 * 4;
-        float* tpair;
+        using TokT = std::conditional_t<TOK == FC_TOKENS_BF16, uint16_t, float>;
+        TokT* tpair;
         if (p.tokj != nullptr) {
           const int job = r.pair / p.ppj;
-          tpair = p.tokj[job] + static_cast<size_t>(r.pair - job * p.ppj) * pair_rows * kCols;
+          tpair = static_cast<TokT*>(p.tokj[job]) + static_cast<size_t>(r.pair - job * p.ppj) * pair_rows * kCols;
         } else {
-          tpair = p.tokens + static_cast<size_t>(r.pair) * pair_rows * kCols;
+          tpair = static_cast<TokT*>(p.tokens) + static_cast<size_t>(r.pair) * pair_rows * kCols;
         }
-        float* tb = tpair + (static_cast<size_t>(hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + g;
+        TokT* tb = tpair + (static_cast<size_t>(hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + g;
 #pragma unroll
         for (int e = 0; e < kPlanesPerWarp; ++e) {
           // this warp's planes are frame f = vsub, channels c = e (plane index 3f + c)
           const int f = vsub, c = e;
           const uint32_t lutc = lut_s + c * 1024;
-          float* tp = tb + (c * 2 + f) * 196;
+          TokT* tp = tb + (c * 2 + f) * 196;
           constexpr int VG = KSV == 1 ? 2 : 1;  // patches interleaved per group
 #pragma unroll
           for (int q0 = 0; q0 < kStrip / 14; q0 += VG) {
@@ -403,14 +407,14 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
               if (q >= npatch) break;
               // d0,d1: column g, rows j0, j0+1; d2,d3: column g+8
               uint32_t sv[4];
-              float o[4];
+              uint32_t o[4];
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 sv[i] = static_cast<uint32_t>(
                     add_min_relu(combine_planes(d2[e2][i], d1[e2][i], d0[e2][i]), 0, (1 << 30) - 1));
-                o[i] = ldsf(lutc + ((sv[i] >> 20) & 0x3FCu));
+                o[i] = lds32(lutc + ((sv[i] >> 20) & 0x3FCu));
               }
-              float* op = tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
+              TokT* op = tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
               st_cs_pred(op, o[0], jok0);
               st_cs_pred(op + 14, o[1], jok1);
               st_cs_pred(op + 8, o[2], jok0 && xok1);
@@ -442,9 +446,11 @@ using KernelFn = void (*)(Params);
 
 struct Instance {
   int ksh, ksv;
-  KernelFn fn, fn_dbg;  // production / with the parity-test dumps of fc_preprocess_debug
+  KernelFn fn, fn_dbg, fn_bf16;  // fp32 tokens / + the parity-test dumps of fc_preprocess_debug / bf16 tokens
 };
-#define FC_INST(A, B) {A, B, fc_fused_kernel<A, B, false>, fc_fused_kernel<A, B, true>},
+#define FC_INST(A, B)                                                                                           \
+  {A, B, fc_fused_kernel<A, B, false, FC_TOKENS_F32>, fc_fused_kernel<A, B, true, FC_TOKENS_F32>, \
+   fc_fused_kernel<A, B, false, FC_TOKENS_BF16>},
 static const Instance kInstances[] = {FC_INSTANCES(FC_INST)};
 #undef FC_INST
 constexpr int kMaxKS = 4;
@@ -586,7 +592,7 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
   key.w2 = P->th->out;
   key.h = P->tv->in;
   key.h2 = P->tv->out;
-  std::memcpy(key.lut_bits, P->lut.data(), sizeof(key.lut_bits));
+  std::memcpy(key.lut_bits, P->lut_dev.data(), sizeof(key.lut_bits));
   std::lock_guard<std::mutex> gk(g_tables_mu);
   auto git = g_tables->find(key);
   if (git != g_tables->end()) {
@@ -608,7 +614,7 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
   if (e == cudaSuccess) e = upload(&t.vcnt, P->tv->cnt);
   if (e == cudaSuccess) e = upload(&t.vys, m.vys);
   if (e == cudaSuccess) e = upload(&t.vfr, m.vfr);
-  if (e == cudaSuccess) e = upload(&t.lut, P->lut);
+  if (e == cudaSuccess) e = upload(&t.lut, P->lut_dev);
   if (e != cudaSuccess) {
     cudaFree(t.hx); cudaFree(t.hxs); cudaFree(t.hfr); cudaFree(t.vx); cudaFree(t.vcnt); cudaFree(t.vys);
     cudaFree(t.vfr); cudaFree(t.lut);
@@ -622,7 +628,7 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
 
 struct Geometry {
   int sw, htiles, SWPN, SWP, BW, NX, TR, TRW, nstrips, nchunks;
-  KernelFn fn, fn_dbg;
+  KernelFn fn, fn_dbg, fn_bf16;
   size_t smem;
 };
 
@@ -676,6 +682,7 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
     if (in.ksh == dt->ksh && in.ksv == dt->ksv) {
       g->fn = in.fn;
       g->fn_dbg = in.fn_dbg;
+      g->fn_bf16 = in.fn_bf16;
     }
   if (!g->fn) return fail(FC_ERR_UNSUPPORTED, "no kernel instance for this resize window");
   if (dt->ksh <= 2 && 2 * kChunkRows * (g->SWPN / 16) > 2 * kComputeThreads)
@@ -747,6 +754,27 @@ static fc_status tensor_map(const uint8_t* base, int64_t pitch, int64_t rows, in
   return FC_OK;
 }
 
+// Colour matrix constants (R3, R15): rounded 256x coefficients of the
+// standard matrices (include/fc.h), folded into dp2a operand pairs and biases.
+static void color_constants(fc_color m, Params* p) {
+  struct K { int y, y0, rv, gu, gv, bu; };
+  static const K kTab[4] = {
+      {298, 16, 409, -100, -208, 516},  // BT.601 limited (R3)
+      {298, 16, 459, -55, -136, 541},   // BT.709 limited
+      {256, 0, 359, -88, -183, 454},    // BT.601 full
+      {256, 0, 403, -48, -120, 475},    // BT.709 full
+  };
+  const K& k = kTab[static_cast<int>(m)];
+  auto pack = [](int hi, int lo) { return (static_cast<uint32_t>(hi & 0xFFFF) << 16) | static_cast<uint32_t>(lo & 0xFFFF); };
+  p->ckR = pack(k.rv, k.y);
+  p->ckB = pack(k.bu, k.y);
+  p->ckG = pack(k.gu, k.y);
+  p->ckGv = pack(k.gv, 0);
+  p->cbR = -k.y0 * k.y - 128 * k.rv + 128;
+  p->cbG = -k.y0 * k.y - 128 * (k.gu + k.gv) + 128;
+  p->cbB = -k.y0 * k.y - 128 * k.bu + 128;
+}
+
 // The rank's frame list (its sampled frames, then pad copies of the last),
 // after validating every surface it reads.  Empty for a rank with no rows.
 static std::atomic<uint64_t> g_launches{0};
@@ -778,7 +806,7 @@ static fc_status rank_frames(const fc_plan_s* P, int32_t rank, const fc_nv12_sur
 struct Job {
   std::vector<int64_t> frames;
   const fc_nv12_surface* surfaces;
-  float* tokens;
+  void* tokens;
 };
 
 // ONE persistent launch over every pair of `jobs` (all of P's geometry and
@@ -810,7 +838,9 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
     if (st == FC_OK) break;
   }
   if (st != FC_OK) return st;
-  KernelFn fn = (dbg_src || dbg_rs) ? g.fn_dbg : g.fn;
+  const bool bf16 = P->cfg.token_dtype == FC_TOKENS_BF16;
+  if (bf16 && (dbg_src || dbg_rs)) return fail(FC_ERR_UNSUPPORTED, "debug dumps are built for fp32 tokens only");
+  KernelFn fn = (dbg_src || dbg_rs) ? g.fn_dbg : bf16 ? g.fn_bf16 : g.fn;
   e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(g.smem));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
@@ -846,6 +876,7 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   prm.vys = dt->vys;
   prm.vfr = dt->vfr;
   prm.lut = dt->lut;
+  color_constants(P->cfg.color, &prm);
   prm.dbg_src = dbg_src;
   prm.dbg_rs = dbg_rs;
   prm.trw_magic = static_cast<uint32_t>(((1ull << 32) + g.TRW - 1) / g.TRW);
@@ -873,11 +904,12 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   void* desc = nullptr;
   if (!inline_maps) {
     const size_t mbytes = maps.size() * sizeof(CUtensorMap);
-    const size_t bytes = mbytes + (jobs.size() > 1 ? jobs.size() * sizeof(float*) : 0);
+    const size_t bytes = mbytes + (jobs.size() > 1 ? jobs.size() * sizeof(void*) : 0);
     std::vector<uint8_t> host(bytes);
     std::memcpy(host.data(), maps.data(), mbytes);
     if (jobs.size() > 1)
-      for (size_t j = 0; j < jobs.size(); ++j) std::memcpy(host.data() + mbytes + j * sizeof(float*), &jobs[j].tokens, sizeof(float*));
+      for (size_t j = 0; j < jobs.size(); ++j)
+        std::memcpy(host.data() + mbytes + j * sizeof(void*), &jobs[j].tokens, sizeof(void*));
     e = cudaMallocAsync(&desc, bytes, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (launch descriptor)");
     // pageable source: returns once the bytes are staged, so `host` may die
@@ -887,7 +919,7 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
       return cuda_fail(e, "descriptor upload");
     }
     prm.tmg = reinterpret_cast<const CUtensorMap*>(desc);
-    if (jobs.size() > 1) prm.tokj = reinterpret_cast<float* const*>(static_cast<uint8_t*>(desc) + mbytes);
+    if (jobs.size() > 1) prm.tokj = reinterpret_cast<void* const*>(static_cast<uint8_t*>(desc) + mbytes);
   }
   const int grid = static_cast<int>(std::min<long long>(items, static_cast<long long>(occ) * nsm));
   fn<<<grid, kThreads, g.smem, s>>>(prm);
@@ -899,7 +931,7 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
 }
 
 static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv12_surface* surfaces,
-                                 int64_t num_surfaces, float* tokens, int64_t grid_thw[3], void* stream,
+                                 int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream,
                                  uint8_t* dbg_src, uint8_t* dbg_rs) {
   if (!Pc) return fail(FC_ERR_INVALID_ARG, "plan is NULL");
   fc_plan_s* P = const_cast<fc_plan_s*>(Pc);
@@ -925,19 +957,19 @@ using namespace fc;
 extern "C" {
 
 fc_status fc_preprocess(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
-                        int64_t num_surfaces, float* tokens, int64_t grid_thw[3], void* stream) {
+                        int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream) {
   return preprocess_impl(plan, rank, surfaces, num_surfaces, tokens, grid_thw, stream, nullptr, nullptr);
 }
 
 fc_status fc_preprocess_debug(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
-                              int64_t num_surfaces, float* tokens, int64_t grid_thw[3], void* stream,
+                              int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream,
                               uint8_t* rgb_src, uint8_t* rgb_resized) {
   return preprocess_impl(plan, rank, surfaces, num_surfaces, tokens, grid_thw, stream, rgb_src, rgb_resized);
 }
 
 fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* ranks, int32_t count,
                               const fc_nv12_surface* const* surfaces, const int64_t* num_surfaces,
-                              float* const* tokens, void* stream) {
+                              void* const* tokens, void* stream) {
   if (count < 0 || (count > 0 && (!plans || !ranks || !surfaces || !num_surfaces || !tokens)))
     return fail(FC_ERR_INVALID_ARG, "batch arguments");
   // validate every job before any launch; then one launch per maximal run of
@@ -957,6 +989,7 @@ fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* rank
   auto same = [&](int a, int b) {
     const fc_plan_s &A = *jp[a], &B = *jp[b];
     return A.meta.width == B.meta.width && A.meta.height == B.meta.height && A.w2 == B.w2 && A.h2 == B.h2 &&
+           A.cfg.token_dtype == B.cfg.token_dtype && A.cfg.color == B.cfg.color && A.lut_dev == B.lut_dev &&
            jobs[a].frames.size() == jobs[b].frames.size();
   };
   std::vector<Job> group;

@@ -457,6 +457,10 @@ fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t*
   if (!(c.rescale_factor > 0)) return fail(FC_ERR_INVALID_ARG, "rescale_factor must be > 0");
   for (int i = 0; i < 3; ++i)
     if (!(c.image_std[i] != 0.0f)) return fail(FC_ERR_INVALID_ARG, "image_std must be non-zero");
+  if (c.token_dtype != FC_TOKENS_F32 && c.token_dtype != FC_TOKENS_BF16)
+    return fail(FC_ERR_UNSUPPORTED, "unknown token_dtype");
+  if (c.color < FC_COLOR_BT601_LIMITED || c.color > FC_COLOR_BT709_FULL)
+    return fail(FC_ERR_UNSUPPORTED, "unknown color matrix");
 
   fc_plan_s* P = new (std::nothrow) fc_plan_s();
   if (!P) return fail(FC_ERR_OOM, "plan allocation failed");
@@ -490,6 +494,14 @@ fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t*
         const float d = x - c.image_mean[ch];
         P->lut[ch * 256 + v] = d / c.image_std[ch];
       }
+    // the table the kernel stores from: fp32 bits, or (R16) the bf16 bits of
+    // the fp32 value rounded to nearest-even, zero-extended (finite values)
+    P->lut_dev.resize(3 * 256);
+    for (int i = 0; i < 3 * 256; ++i) {
+      uint32_t b;
+      std::memcpy(&b, &P->lut[i], 4);
+      P->lut_dev[i] = c.token_dtype == FC_TOKENS_BF16 ? (b + 0x7FFFu + ((b >> 16) & 1u)) >> 16 : b;
+    }
   }
   if (st != FC_OK) {
     delete P;

@@ -180,6 +180,58 @@ def test_bt601_colour_bars(oracle):
         assert oracle.bt601_pixel(Y, U, V) == (R, G, B), r
 
 
+@pytest.mark.parametrize("matrix", ["bt601", "bt709", "bt601_full", "bt709_full"])
+def test_colour_variants_exhaustive_vs_real_valued(oracle, matrix):
+    """R15: every (Y,U,V) through the integer form of each matrix is within 2
+    LSB of the real-valued ITU-R matrix built from its luma weights and
+    range (BT.601 Kr=0.299 Kb=0.114; BT.709 Kr=0.2126 Kb=0.0722; limited =
+    Y 16..235 / C 16..240, full = 0..255), and black, white and grey land
+    exactly where the standard puts them."""
+    t = oracle.yuv_table(matrix).astype(np.float64)
+    Y, U, V = np.meshgrid(np.arange(256.0), np.arange(256.0), np.arange(256.0), indexing="ij")
+    kr, kb = (0.2126, 0.0722) if "709" in matrix else (0.299, 0.114)
+    kg = 1 - kr - kb
+    full = matrix.endswith("_full")
+    yy = Y if full else (Y - 16) * 255 / 219
+    pb = (U - 128) * (1.0 if full else 255 / 224)
+    pr = (V - 128) * (1.0 if full else 255 / 224)
+    ref = np.stack([yy + 2 * (1 - kr) * pr,
+                    yy - 2 * (1 - kb) * kb / kg * pb - 2 * (1 - kr) * kr / kg * pr,
+                    yy + 2 * (1 - kb) * pb], -1)
+    ref = np.clip(np.rint(ref), 0, 255)
+    assert np.abs(t - ref).max() <= 2.0
+    lo, hi = (0, 255) if full else (16, 235)
+    assert tuple(t[lo, 128, 128]) == (0, 0, 0) and tuple(t[hi, 128, 128]) == (255, 255, 255)
+    if full:  # grey is the identity
+        np.testing.assert_array_equal(t[:, 128, 128, 0], np.arange(256.0))
+    if matrix == "bt601":  # the generic form reproduces the pinned O7 function
+        for (y_, u_, v_) in [(16, 128, 128), (81, 90, 240), (145, 54, 34), (41, 240, 110), (235, 16, 16), (0, 0, 0)]:
+            assert tuple(int(x) for x in t[y_, u_, v_]) == oracle.bt601_pixel(y_, u_, v_)
+
+
+def test_colour_variant_coefficients(oracle):
+    """R15 integer coefficients: round(256 x the standard's matrix entries)."""
+    assert oracle.yuv_coeffs("bt601") == (298, 16, 409, -100, -208, 516)
+    assert oracle.yuv_coeffs("bt709") == (298, 16, 459, -55, -136, 541)
+    assert oracle.yuv_coeffs("bt601_full") == (256, 0, 359, -88, -183, 454)
+    assert oracle.yuv_coeffs("bt709_full") == (256, 0, 403, -48, -120, 475)
+
+
+def test_bf16_rounding_vs_torch(oracle):
+    """R16: the oracle's fp32 -> bf16 equals torch's conversion (RNE) on every
+    normalisation-table value, random floats, exact ties and the boundaries."""
+    import torch
+    lut = np.array([oracle.normalize_value(v, c) for c in range(3) for v in range(256)], np.float32)
+    rng = np.random.default_rng(5)
+    rnd = (rng.standard_normal(100000) * 4).astype(np.float32)
+    ties = (np.array([0x3F808000, 0x3F818000, 0xBF808000, 0x40490000 | 0x8000], np.uint32)).view(np.float32)
+    for x in (lut, rnd, ties, np.array([0.0, -0.0, 1.0, -2.5, 3.4e38], np.float32)):
+        ref = torch.from_numpy(x).to(torch.bfloat16).view(torch.int16).numpy().view(np.uint16)
+        np.testing.assert_array_equal(oracle.to_bf16(x), ref)
+    assert oracle.to_bf16(np.array([1.00390625], np.float32))[0] == 0x3F80  # tie -> even
+    assert oracle.to_bf16(np.array([1.01171875], np.float32))[0] == 0x3F82  # tie -> even (up)
+
+
 def test_nv12_chroma_siting(oracle):
     """A single chroma sample covers exactly its 2x2 luma block."""
     W = H = 8

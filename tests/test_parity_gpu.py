@@ -42,7 +42,8 @@ def run_case(fc, oracle, cuda, W, H, N, gops, kind="natural", seed=7, world=1, c
     dev = synth.to_device(host)
     surf = fc.SurfaceTable.from_tensors(dev, N)
     h2, w2 = plan.resized
-    ref_tok, ref_src, ref_rs = oracle.preprocess([host[i] for i in idx], W, H, w2, h2, want_rgb=True)
+    ref_tok, ref_src, ref_rs = oracle.preprocess([host[i] for i in idx], W, H, w2, h2, want_rgb=True,
+                                                 matrix=cfg.get("color", "bt601"))
     parts = []
     for r in range(world):
         rp = plan.rank(r)
@@ -266,3 +267,70 @@ def test_full_c5_batch_64_clips(fc, oracle, cuda):
             ref = oracle.preprocess([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2)
             got = outs[clip][t * rpp:(t + 1) * rpp].cpu().numpy()
             assert tol_check(got, ref, f"c5 clip {clip} pair {t}") == ref.size
+
+
+# ------------------------------------------------------ NEXT-4 variants
+@pytest.mark.parametrize("color", ["bt709", "bt601_full", "bt709_full"])
+@pytest.mark.parametrize("kind", ["uniform", "edges"])
+def test_colour_variants(fc, oracle, cuda, color, kind):
+    """R15: the colour-matrix variants, RGB intermediates and tokens vs the oracle."""
+    plan, exact, size = run_case(fc, oracle, cuda, 320, 240, 40, [0, 20], kind, seed=13,
+                                 sampling="explicit", explicit_indices=[1, 9, 22, 33], color=color)
+    assert exact == size
+
+
+def _bf16_case(fc, oracle, W, H, N, gops, kind, seed, h2w2=None, **cfg):
+    import torch
+    extra = dict(resized_height=h2w2[0], resized_width=h2w2[1]) if h2w2 else {}
+    plan = fc.Plan(fc.VideoMeta(W, H, N, (30, 1), gops), fc.ModelCfg(token_dtype="bf16", **cfg, **extra))
+    idx = plan.sampled_indices
+    host = {i: synth.frame_nv12(W, H, i, kind, seed) for i in idx}
+    dev = synth.to_device(host)
+    surf = fc.SurfaceTable.from_tensors(dev, N)
+    out = fc.preprocess(plan, 0, surf)
+    torch.cuda.synchronize()
+    assert out.dtype == torch.bfloat16 and out.shape == (plan.token_rows, 1176)
+    h2, w2 = plan.resized
+    ref = oracle.preprocess([host[i] for i in idx], W, H, w2, h2, matrix=cfg.get("color", "bt601"))
+    got = out.view(torch.int16).cpu().numpy().view(np.uint16)
+    np.testing.assert_array_equal(got, oracle.to_bf16(ref))
+
+
+@pytest.mark.parametrize("shape", [(320, 240, None), (200, 120, (56, 84)), (1920, 1080, (224, 224))])
+def test_bf16_tokens(fc, oracle, cuda, shape):
+    """R16: bf16 tokens == RNE(oracle fp32 tokens), bit for bit (ragged strip,
+    the paper's 224x224 eval size, and a colour variant on top)."""
+    W, H, hw = shape
+    _bf16_case(fc, oracle, W, H, 30, [0, 15], "uniform", 17, hw, sampling="explicit",
+               explicit_indices=[0, 4, 15, 29, 7][:4] if W != 200 else [0, 4, 15])
+    _bf16_case(fc, oracle, W, H, 30, [0, 15], "natural", 18, hw, sampling="explicit",
+               explicit_indices=[2, 3], color="bt709")
+
+
+def test_bf16_full_c2_sampled_pairs(fc, oracle, cuda):
+    """bf16 at BASELINE config 2 in the bench's launch configuration; sampled pairs."""
+    import torch
+    wl = synth.CONFIGS["c2"]
+    plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
+                   fc.ModelCfg(sample_fps=wl.sample_fps, token_dtype="bf16"))
+    idx = plan.sampled_indices
+    host = synth.frames_nv12(wl, idx, "natural")
+    surf = fc.SurfaceTable.from_tensors(synth.to_device(host), wl.num_frames)
+    out = fc.preprocess(plan, 0, surf)
+    torch.cuda.synchronize()
+    rpp = plan.grid_thw[1] * plan.grid_thw[2]
+    h2, w2 = plan.resized
+    for t in _sample_pairs(plan.grid_thw[0]):
+        ref = oracle.preprocess([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2)
+        got = out[t * rpp:(t + 1) * rpp].view(torch.int16).cpu().numpy().view(np.uint16)
+        np.testing.assert_array_equal(got, oracle.to_bf16(ref), err_msg=f"pair {t}")
+
+
+def test_bf16_debug_dumps_rejected(fc, cuda):
+    plan = fc.Plan(fc.VideoMeta(64, 48, 8, (30, 1), [0]),
+                   fc.ModelCfg(token_dtype="bf16", sampling="explicit", explicit_indices=[0, 1]))
+    host = {i: synth.frame_nv12(64, 48, i, "uniform", 1) for i in (0, 1)}
+    surf = fc.SurfaceTable.from_tensors(synth.to_device(host), 8)
+    with pytest.raises(fc.FcError) as e:
+        fc.preprocess_debug(plan, 0, surf)
+    assert e.value.name == "FC_ERR_UNSUPPORTED"

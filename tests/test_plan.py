@@ -29,7 +29,7 @@ def test_abi_exports_every_declared_symbol(fc):
     lib = ctypes.CDLL(fc._native.LIB_PATH)
     missing = [n for n in sorted(names) if not hasattr(lib, n)]
     assert not missing, missing
-    assert fc.lib().fc_abi_version() == 1
+    assert fc.lib().fc_abi_version() == 2
 
 
 @pytest.mark.parametrize("name", sorted(synth.CONFIGS))
@@ -197,3 +197,25 @@ def test_missing_surface_reported(fc):
     out = (ctypes.c_float * (p.token_rows * 1176))()
     st = fc.lib().fc_preprocess(p.handle, 0, surf.arr, 100, ctypes.cast(out, ctypes.c_void_p), None, None)
     assert fc._native.STATUS[st] == "FC_ERR_MISSING_SURFACE"
+
+
+@pytest.mark.parametrize("field,value", [("token_dtype", 2), ("color", 4), ("color", -1)])
+def test_unknown_variant_enums_rejected(fc, field, value):
+    """NEXT-4 variant enums are validated by fc_plan (S:34 structured errors)."""
+    meta = fc.VideoMeta(64, 48, 100, (30, 1), [0, 50])
+    m, _k1 = meta.to_c()
+    c, _k2 = fc.ModelCfg().to_c()
+    setattr(c, field, value)
+    h = ctypes.c_void_p()
+    st = fc.lib().fc_plan(ctypes.byref(m), ctypes.byref(c), ctypes.byref(h))
+    assert fc._native.STATUS[st] == "FC_ERR_UNSUPPORTED"
+
+
+def test_model_cfg_struct_matches_abi(fc):
+    """The ctypes mirror of fc_model_cfg has the C layout: fc_model_cfg_default
+    fills the trailing fields with their documented defaults."""
+    c = fc._native.ModelCfgC()
+    c.token_dtype, c.color = 9, 9
+    fc.lib().fc_model_cfg_default(ctypes.byref(c))
+    assert (c.token_dtype, c.color, c.world_size, c.encoder_rank) == (0, 0, 1, 0)
+    assert abs(c.rescale_factor - 1 / 255) < 1e-15 and c.patch_size == 14
