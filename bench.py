@@ -190,7 +190,11 @@ def run_ours(args):
     wl = synth.CONFIGS[args.config]
     clips = wl.clips                              # c5: 64 independent requests per step
     meta = workload_meta(fc, wl)
-    cfg = fc.ModelCfg(world_size=world, sample_fps=wl.sample_fps, token_dtype=args.tokens, color=args.color)
+    # N>1 with the u8 exchange (NEXT-1, default): ranks produce u8 codes, the
+    # gather moves 1176-byte rows, the encoder expands them to tokens
+    u8x = world > 1 and args.exchange == "u8"
+    cfg = fc.ModelCfg(world_size=world, sample_fps=wl.sample_fps, token_dtype="u8" if u8x else args.tokens,
+                      color=args.color)
     tok_bytes = 2 if args.tokens == "bf16" else 4
     plan0 = fc.Plan(meta, cfg)
     rp = plan0.rank(rank)
@@ -202,12 +206,22 @@ def run_ours(args):
     surfs = [fc.SurfaceTable.from_tensors(d, wl.num_frames) for d in devs]
     rows = rp["row_end"] - rp["row_begin"]
     tdt = torch.bfloat16 if args.tokens == "bf16" else torch.float32
-    outs = [torch.empty((max(rows, 1), 1176), dtype=tdt, device="cuda") for _ in range(clips)]
+    xdt = torch.uint8 if u8x else tdt  # what the kernel writes and the gather moves
+    outs = [torch.empty((max(rows, 1), 1176), dtype=xdt, device="cuda") for _ in range(clips)]
     comm = fc.NcclComm(rank, world) if world > 1 else None
     enc = cfg.encoder_rank
-    fulls = [torch.empty((plan0.token_rows, 1176), dtype=tdt, device="cuda")
+    fulls = [torch.empty((plan0.token_rows, 1176), dtype=xdt, device="cuda")
              if (world > 1 and rank == enc) else None for _ in range(clips)]
+    toks = [torch.empty((plan0.token_rows, 1176), dtype=tdt, device="cuda")
+            if (u8x and rank == enc) else None for _ in range(clips)]
     stream = torch.cuda.current_stream()
+
+    def exchange(plans):
+        """a10 (+ the encoder-side expand of the u8 exchange)."""
+        for pl, o, fl, tk in zip(plans, outs, fulls, toks):
+            fc.gather(pl, rank, comm, o if rows else None, fl)
+            if tk is not None:
+                fc.expand_tokens(pl, fl, tk, args.tokens)
 
     def step(plans_keep, ev_a=None, ev_b=None):
         plans = [fc.Plan(meta, cfg) for _ in range(clips)]   # a1-a4 (host), one plan per request
@@ -222,8 +236,7 @@ def run_ours(args):
         if ev_b is not None:
             ev_b.record(stream)
         if world > 1:
-            for pl, o, fl in zip(plans, outs, fulls):
-                fc.gather(pl, rank, comm, o if rows else None, fl)  # a10
+            exchange(plans)                        # a10
         if len(plans_keep) > 64:
             del plans_keep[:32]                   # older plans' work has long completed
 
@@ -264,15 +277,15 @@ def run_ours(args):
         torch.cuda.synchronize()
         g0.record(stream)
         for _ in range(max(3, args.steps // 4)):
-            for o, fl in zip(outs, fulls):
-                fc.gather(plan0, rank, comm, o if rows else None, fl)
+            exchange([plan0] * clips)
         g1.record(stream)
         torch.cuda.synchronize()
         gms = torch.tensor([g0.elapsed_time(g1) / max(3, args.steps // 4)], dtype=torch.float64, device="cuda")
         dist.all_reduce(gms, op=dist.ReduceOp.MAX)
-        gbytes = clips * sum((r["row_end"] - r["row_begin"]) * 1176 * tok_bytes for i, r in enumerate(plan0.ranks())
-                             if i != enc)
-        gather = {"ms": round(gms.item(), 4), "bytes_into_encoder": gbytes,
+        gbytes = clips * sum((r["row_end"] - r["row_begin"]) * 1176 * (1 if u8x else tok_bytes)
+                             for i, r in enumerate(plan0.ranks()) if i != enc)
+        gather = {"exchange": "u8 codes + encoder expand" if u8x else args.tokens,
+                  "ms": round(gms.item(), 4), "bytes_into_encoder": gbytes,
                   "GB/s": round(gbytes / (gms.item() * 1e-3) / 1e9, 1), "nvlink_nominal_GB/s": 900,
                   "nvlink_measured_peer_GB/s": 770}
 
@@ -296,11 +309,11 @@ def run_ours(args):
             else:
                 fc.preprocess_batch([(pl, rank, sf) for pl, sf in zip(plans, surfs)], outs)
         if world > 1:
-            for pl, o, fl in zip(plans, outs, fulls):
-                fc.gather(pl, rank, comm, o if rows else None, fl)
-        for c in range(clips):  # one token row of every request's result back to the host
-            src = fulls[c] if (world > 1 and rank == enc) else outs[c]
-            res_host[c].copy_(src[0], non_blocking=True)
+            exchange(plans)
+        if world == 1 or rank == enc:  # one token row of every request's result back to the host
+            for c in range(clips):
+                src = (toks[c] if u8x else fulls[c]) if world > 1 else outs[c]
+                res_host[c].copy_(src[0], non_blocking=True)
 
     e2e_step(keep)
     torch.cuda.synchronize()
@@ -323,7 +336,7 @@ def run_ours(args):
             abytes = clips * algorithmic_bytes(plan0, wl, tok_bytes=tok_bytes)
             kern_for_roof = kern_avg
         else:  # dominant kernel = this rank's launch; bytes of the largest shard
-            abytes = clips * max(algorithmic_bytes(plan0, wl, r, tok_bytes) for r in plan0.ranks())
+            abytes = clips * max(algorithmic_bytes(plan0, wl, r, 1 if u8x else tok_bytes) for r in plan0.ranks())
             kern_for_roof = kern_max
         achieved = abytes / (kern_for_roof * 1e-3) / 1e9
         traffic = load_traffic(args.config) if (world == 1 and args.tokens == "f32" and args.color == "bt601") else None
@@ -374,6 +387,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tokens", default="f32", choices=["f32", "bf16"],
                     help="token dtype (NEXT-4 variant; the BASELINE metric is f32)")
+    ap.add_argument("--exchange", default="u8", choices=["u8", "f32"],
+                    help="N>1 exchange format: u8 codes + encoder-side expand (default), or the tokens themselves")
     ap.add_argument("--color", default="bt601", choices=["bt601", "bt709", "bt601_full", "bt709_full"],
                     help="YUV->RGB matrix (NEXT-4 variant; the BASELINE metric is bt601)")
     args = ap.parse_args()

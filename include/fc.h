@@ -81,7 +81,15 @@ typedef enum { FC_SAMPLE_FPS_STRIDE = 0, FC_SAMPLE_LINSPACE = 1, FC_SAMPLE_EXPLI
  * token rounded to nearest-even bfloat16 -- exactly torch's
  * `.to(torch.bfloat16)` of the F32 result -- for encoders that consume bf16;
  * it halves the token bytes written (reading R16). */
-typedef enum { FC_TOKENS_F32 = 0, FC_TOKENS_BF16 = 1 } fc_token_dtype;
+typedef enum {
+  FC_TOKENS_F32 = 0,
+  FC_TOKENS_BF16 = 1,
+  /* u8 "codes" (NEXT-1 exchange format): the resized RGB value (R4's clip8
+   * result) of every token element, same [rows][1176] layout, 1 byte each.
+   * fc_expand_tokens turns codes into F32/BF16 tokens (R5's table), so a
+   * multi-GPU request can gather 1176-byte rows instead of 4704-byte ones. */
+  FC_TOKENS_U8 = 2
+} fc_token_dtype;
 
 /* YUV -> RGB matrix (reading R3 for the default; R15 for the variants):
  * 8-bit fixed point, out = clamp((cY*(Y - y0) + cU*(U-128) + cV*(V-128) + 128) >> 8)
@@ -218,6 +226,17 @@ fc_status fc_preprocess_debug(const fc_plan_t* plan, int32_t rank, const fc_nv12
 fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* ranks, int32_t count,
                               const fc_nv12_surface* const* surfaces, const int64_t* num_surfaces,
                               void* const* tokens, void* stream);
+
+/* fc_expand_tokens -- R5 on u8 codes (FC_TOKENS_U8 output of fc_preprocess,
+ * usually gathered from all ranks): tokens[r][i] = table[channel(i)][codes[r][i]]
+ * with channel(i) = i / 392 (columns are (c, tp, ph, pw)).  The table is the
+ * plan's normalisation (mean/std/rescale), in fp32 or rounded to bf16 (R16).
+ *   codes:     device pointer, rows x 1176 u8, contiguous.
+ *   tokens:    device pointer, rows x 1176 elements of out_dtype (F32 | BF16).
+ * One HBM-bound kernel launch on `stream`; results equal fc_preprocess with
+ * token_dtype = out_dtype bit for bit. */
+fc_status fc_expand_tokens(const fc_plan_t* plan, int64_t rows, const uint8_t* codes, void* tokens,
+                           fc_token_dtype out_dtype, void* stream);
 
 /* ---- exchange: gather row shards to the encoder rank ---- */
 

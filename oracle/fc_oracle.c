@@ -288,6 +288,35 @@ void oracle_tokens(const uint8_t* rs, int64_t n, int w2, int h2, const float* me
           }
 }
 
+/* NEXT-1 exchange format: the same R6 walk, storing the resized u8 value
+ * itself (the "code") instead of its normalised token.  Pinned: normalising
+ * the codes reproduces oracle_tokens exactly. */
+void oracle_codes(const uint8_t* rs, int64_t n, int w2, int h2, uint8_t* codes) {
+  const int P = 14, M = 2, TP = 2;
+  int64_t gt = (n + TP - 1) / TP;
+  int gh = h2 / P, gw = w2 / P;
+  int64_t row = 0;
+  for (int64_t t = 0; t < gt; ++t)
+    for (int hb = 0; hb < gh / M; ++hb)
+      for (int wb = 0; wb < gw / M; ++wb)
+        for (int hm = 0; hm < M; ++hm)
+          for (int wm = 0; wm < M; ++wm) {
+            int64_t col = 0;
+            for (int c = 0; c < 3; ++c)
+              for (int tp = 0; tp < TP; ++tp)
+                for (int ph = 0; ph < P; ++ph)
+                  for (int pw = 0; pw < P; ++pw) {
+                    int64_t f = TP * t + tp;
+                    if (f > n - 1) f = n - 1;
+                    int y = (hb * M + hm) * P + ph;
+                    int x = (wb * M + wm) * P + pw;
+                    codes[row * 1176 + col] = rs[(((size_t)f * h2 + y) * w2 + x) * 3 + c];
+                    ++col;
+                  }
+            ++row;
+          }
+}
+
 /* ------------------------------------------------------- end to end -- */
 typedef struct {
   const uint8_t* const* y;

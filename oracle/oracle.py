@@ -78,6 +78,7 @@ def lib():
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p,
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
         L.oracle_yuv_coeffs.argtypes = [ctypes.c_int, ctypes.c_void_p]
+        L.oracle_codes.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         L.oracle_yuv_pixel.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p]
         L.oracle_yuv_table.argtypes = [ctypes.c_int, ctypes.c_void_p]
         L.oracle_preprocess.restype = ctypes.c_int
@@ -330,6 +331,16 @@ def tokens_from_resized(rs: np.ndarray, mean=CLIP_MEAN, std=CLIP_STD, rescale: f
     m = np.array(mean, np.float32)
     s = np.array(std, np.float32)
     lib().oracle_tokens(_ptr(rs), n, w2, h2, _ptr(m), _ptr(s), rescale, _ptr(out))
+    return out
+
+
+def codes_from_resized(rs: np.ndarray) -> np.ndarray:
+    """NEXT-1 exchange format: the R6 layout of the resized u8 values."""
+    rs = np.ascontiguousarray(rs, dtype=np.uint8)
+    n, h2, w2 = rs.shape[:3]
+    gt, gh, gw = grid_thw(n, h2, w2)
+    out = np.empty((gt * gh * gw, COLS), np.uint8)
+    lib().oracle_codes(_ptr(rs), n, w2, h2, _ptr(out))
     return out
 
 

@@ -21,6 +21,7 @@ from . import _native
 from ._native import FcError, FC_TOKEN_COLS, check, lib
 
 __all__ = ["VideoMeta", "ModelCfg", "Plan", "SurfaceTable", "preprocess", "preprocess_debug", "preprocess_batch",
+           "expand_tokens",
            "NcclComm", "gather", "FcError", "FC_TOKEN_COLS", "lib"]
 
 
@@ -62,7 +63,7 @@ class ModelCfg:
     image_mean: tuple[float, float, float] | None = None
     image_std: tuple[float, float, float] | None = None
     rescale_factor: float | None = None
-    token_dtype: str = "f32"        # "f32" (HF output) | "bf16" (R16: RNE of the f32 token)
+    token_dtype: str = "f32"        # "f32" (HF output) | "bf16" (R16) | "u8" (codes; NEXT-1 exchange format)
     color: str = "bt601"            # "bt601" (R3) | "bt709" | "bt601_full" | "bt709_full" (R15)
 
     def to_c(self):
@@ -138,7 +139,10 @@ class Plan:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib().fc_plan_destroy(h)
+            try:
+                lib().fc_plan_destroy(h)
+            except TypeError:  # interpreter teardown: module globals already cleared
+                pass
             self._h = None
 
 
@@ -177,7 +181,7 @@ def _stream_ptr(stream) -> ctypes.c_void_p:
 
 def _tok_dtype(plan: Plan):
     import torch
-    return torch.bfloat16 if plan.cfg.token_dtype == "bf16" else torch.float32
+    return {"f32": torch.float32, "bf16": torch.bfloat16, "u8": torch.uint8}[plan.cfg.token_dtype]
 
 
 def _rank_rows(plan: Plan, rank: int) -> int:
@@ -234,6 +238,20 @@ def preprocess_batch(jobs: Sequence[tuple[Plan, int, SurfaceTable]], outs=None, 
     toks = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs])
     check(lib().fc_preprocess_batch(plans, ranks, n, surfs, nsurf, toks, _stream_ptr(stream)), "fc_preprocess_batch")
     return outs
+
+
+def expand_tokens(plan: Plan, codes, out=None, out_dtype: str = "f32", stream=None):
+    """fc_expand_tokens: u8 codes [rows, 1176] -> f32/bf16 tokens with the
+    plan's normalisation (one HBM-bound launch)."""
+    import torch
+    rows = codes.shape[0]
+    if out is None:
+        out = torch.empty((rows, FC_TOKEN_COLS), dtype=torch.bfloat16 if out_dtype == "bf16" else torch.float32,
+                          device="cuda")
+    check(lib().fc_expand_tokens(plan.handle, rows, ctypes.c_void_p(codes.data_ptr()),
+                                 ctypes.c_void_p(out.data_ptr()), _native.TOKEN_DTYPES[out_dtype],
+                                 _stream_ptr(stream)), "fc_expand_tokens")
+    return out
 
 
 class NcclComm:

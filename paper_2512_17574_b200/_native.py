@@ -19,7 +19,7 @@ STATUS = {0: "FC_OK", 1: "FC_ERR_INVALID_ARG", 2: "FC_ERR_EMPTY_SELECTION", 3: "
           4: "FC_ERR_UNSUPPORTED", 5: "FC_ERR_MISSING_SURFACE", 6: "FC_ERR_RANK", 7: "FC_ERR_OOM",
           8: "FC_ERR_CUDA", 9: "FC_ERR_NCCL"}
 SAMPLING = {"fps_stride": 0, "linspace": 1, "explicit": 2}
-TOKEN_DTYPES = {"f32": 0, "bf16": 1}
+TOKEN_DTYPES = {"f32": 0, "bf16": 1, "u8": 2}
 COLORS = {"bt601": 0, "bt709": 1, "bt601_full": 2, "bt709_full": 3}
 
 
@@ -73,7 +73,7 @@ class Nv12SurfaceC(ctypes.Structure):
 EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_get", "fc_plan_sampled_indices",
            "fc_plan_rank", "fc_preprocess", "fc_preprocess_debug", "fc_preprocess_batch", "fc_nccl_unique_id",
            "fc_nccl_comm_init", "fc_nccl_comm_destroy", "fc_gather", "fc_status_string", "fc_last_error",
-           "fc_abi_version", "fc_kernel_launches"]
+           "fc_abi_version", "fc_kernel_launches", "fc_expand_tokens"]
 
 _lib = None
 
@@ -111,6 +111,7 @@ def lib() -> ctypes.CDLL:
     L.fc_last_error.restype = ctypes.c_char_p
     L.fc_abi_version.argtypes = []
     L.fc_abi_version.restype = ctypes.c_int32
+    L.fc_expand_tokens.argtypes = [vp, i64, vp, vp, ctypes.c_int, vp]
     L.fc_kernel_launches.argtypes = []
     L.fc_kernel_launches.restype = ctypes.c_uint64
     for name in EXPORTS:

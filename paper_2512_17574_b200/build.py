@@ -17,7 +17,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libfc.so")
-SOURCES = ["fc_plan.cpp", "fc_kernels.cu", "fc_gather.cpp"]
+SOURCES = ["fc_plan.cpp", "fc_kernels.cu", "fc_expand.cu", "fc_gather.cpp"]
 HEADERS = ["fc_internal.h", "fc_device.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -43,9 +43,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc, libdir = nccl_dirs()
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
               "-I", INCLUDE, "-I", CSRC, "-I", inc]
+    cmds, objs = [], []
     for src in SOURCES:
         obj = os.path.join(objdir, src + ".o")
         cmd = [NVCC, *ARCH, *common, "-lineinfo", "-c", os.path.join(CSRC, src), "-o", obj]
@@ -53,8 +53,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd += ["-Xptxas", "-v", "--fmad=false"] if verbose else ["--fmad=false"]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
+        cmds.append(cmd)
         objs.append(obj)
+    # the translation units are independent: compile them concurrently
+    procs = [subprocess.Popen(c) for c in cmds]
+    bad = [c for c, p in zip(cmds, procs) if p.wait() != 0]
+    if bad:
+        raise subprocess.CalledProcessError(1, bad[0])
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", libdir, "-l:libnccl.so.2",
            "-Xlinker", "-rpath," + libdir, "-cudart", "static"]

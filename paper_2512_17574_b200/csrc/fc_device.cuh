@@ -243,6 +243,12 @@ __device__ __forceinline__ void st_cs_pred(uint16_t* p, uint32_t v, bool pred) {
                : "memory");
 }
 
+__device__ __forceinline__ void st_cs_pred(uint8_t* p, uint32_t v, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\t.reg .b16 h;\n\tsetp.ne.b32 q, %2, 0;\n\tcvt.u16.u32 h, %1;\n\t@q st.global.cs.u8 [%0], h;\n}" ::"l"(p),
+               "r"(v), "r"(static_cast<int>(pred))
+               : "memory");
+}
+
 __device__ __forceinline__ void st_cs_f2(float* p, float a, float b) {
   asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }

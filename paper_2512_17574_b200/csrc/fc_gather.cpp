@@ -55,8 +55,9 @@ fc_status fc_gather(const fc_plan_t* P, int32_t rank, void* comm, const void* sh
   if (rank < 0 || rank >= P->world) return fail(FC_ERR_RANK, "rank outside [0, world_size)");
   const int e = P->cfg.encoder_rank;
   const fc_rank_plan& me = P->ranks[rank].p;
-  // rows are exchanged as bytes: 1176 tokens x (4 B fp32 | 2 B bf16)
-  const size_t row_bytes = static_cast<size_t>(kCols) * (P->cfg.token_dtype == FC_TOKENS_BF16 ? 2 : 4);
+  // rows are exchanged as bytes: 1176 tokens x (4 B fp32 | 2 B bf16 | 1 B u8 code)
+  const int elem = P->cfg.token_dtype == FC_TOKENS_U8 ? 1 : P->cfg.token_dtype == FC_TOKENS_BF16 ? 2 : 4;
+  const size_t row_bytes = static_cast<size_t>(kCols) * elem;
   const size_t my_bytes = static_cast<size_t>(me.row_end - me.row_begin) * row_bytes;
   uint8_t* fullb = static_cast<uint8_t*>(full);
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -368,7 +368,8 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
         // column offset (X0 + 14 q): merge block wb = (X0/28) + q/2, sub-block wm = q&1
         // first token row of this pair (R6: a job's pairs are consecutive gh*gw-row blocks)
         const size_t pair_rows = static_cast<size_t>(p.gh2) * p.gw2 * 4;
-        using TokT = std::conditional_t<TOK == FC_TOKENS_BF16, uint16_t, float>;
+        using TokT = std::conditional_t<TOK == FC_TOKENS_BF16, uint16_t,
+                                        std::conditional_t<TOK == FC_TOKENS_U8, uint8_t, float>>;
         TokT* tpair;
         if (p.tokj != nullptr) {
           const int job = r.pair / p.ppj;
@@ -412,7 +413,10 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
               for (int i = 0; i < 4; ++i) {
                 sv[i] = static_cast<uint32_t>(
                     add_min_relu(combine_planes(d2[e2][i], d1[e2][i], d0[e2][i]), 0, (1 << 30) - 1));
-                o[i] = lds32(lutc + ((sv[i] >> 20) & 0x3FCu));
+                if constexpr (TOK == FC_TOKENS_U8)
+                  o[i] = sv[i] >> 22;  // the u8 code (NEXT-1 exchange format)
+                else
+                  o[i] = lds32(lutc + ((sv[i] >> 20) & 0x3FCu));
               }
               TokT* op = tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
               st_cs_pred(op, o[0], jok0);
@@ -446,11 +450,11 @@ using KernelFn = void (*)(Params);
 
 struct Instance {
   int ksh, ksv;
-  KernelFn fn, fn_dbg, fn_bf16;  // fp32 tokens / + the parity-test dumps of fc_preprocess_debug / bf16 tokens
+  KernelFn fn, fn_dbg, fn_bf16, fn_u8;  // fp32 tokens / + parity-test dumps / bf16 tokens / u8 codes
 };
 #define FC_INST(A, B)                                                                                           \
   {A, B, fc_fused_kernel<A, B, false, FC_TOKENS_F32>, fc_fused_kernel<A, B, true, FC_TOKENS_F32>, \
-   fc_fused_kernel<A, B, false, FC_TOKENS_BF16>},
+   fc_fused_kernel<A, B, false, FC_TOKENS_BF16>, fc_fused_kernel<A, B, false, FC_TOKENS_U8>},
 static const Instance kInstances[] = {FC_INSTANCES(FC_INST)};
 #undef FC_INST
 constexpr int kMaxKS = 4;
@@ -628,7 +632,7 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
 
 struct Geometry {
   int sw, htiles, SWPN, SWP, BW, NX, TR, TRW, nstrips, nchunks;
-  KernelFn fn, fn_dbg, fn_bf16;
+  KernelFn fn, fn_dbg, fn_bf16, fn_u8;
   size_t smem;
 };
 
@@ -683,6 +687,7 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
       g->fn = in.fn;
       g->fn_dbg = in.fn_dbg;
       g->fn_bf16 = in.fn_bf16;
+      g->fn_u8 = in.fn_u8;
     }
   if (!g->fn) return fail(FC_ERR_UNSUPPORTED, "no kernel instance for this resize window");
   if (dt->ksh <= 2 && 2 * kChunkRows * (g->SWPN / 16) > 2 * kComputeThreads)
@@ -777,7 +782,10 @@ static void color_constants(fc_color m, Params* p) {
 
 // The rank's frame list (its sampled frames, then pad copies of the last),
 // after validating every surface it reads.  Empty for a rank with no rows.
-static std::atomic<uint64_t> g_launches{0};
+std::atomic<uint64_t>& launch_counter() {  // fc_kernel_launches(); shared with fc_expand.cu
+  static std::atomic<uint64_t> c{0};
+  return c;
+}
 
 static fc_status rank_frames(const fc_plan_s* P, int32_t rank, const fc_nv12_surface* surfaces, int64_t num_surfaces,
                              std::vector<int64_t>* frames) {
@@ -838,9 +846,13 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
     if (st == FC_OK) break;
   }
   if (st != FC_OK) return st;
-  const bool bf16 = P->cfg.token_dtype == FC_TOKENS_BF16;
-  if (bf16 && (dbg_src || dbg_rs)) return fail(FC_ERR_UNSUPPORTED, "debug dumps are built for fp32 tokens only");
-  KernelFn fn = (dbg_src || dbg_rs) ? g.fn_dbg : bf16 ? g.fn_bf16 : g.fn;
+  const fc_token_dtype td = P->cfg.token_dtype;
+  if (td != FC_TOKENS_F32 && (dbg_src || dbg_rs))
+    return fail(FC_ERR_UNSUPPORTED, "debug dumps are built for fp32 tokens only");
+  KernelFn fn = (dbg_src || dbg_rs)      ? g.fn_dbg
+                : td == FC_TOKENS_BF16 ? g.fn_bf16
+                : td == FC_TOKENS_U8   ? g.fn_u8
+                                       : g.fn;
   e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(g.smem));
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
@@ -926,7 +938,7 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   e = cudaGetLastError();
   if (desc) cudaFreeAsync(desc, s);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
-  g_launches.fetch_add(1, std::memory_order_relaxed);
+  launch_counter().fetch_add(1, std::memory_order_relaxed);
   return FC_OK;
 }
 
@@ -1011,7 +1023,7 @@ fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* rank
   return FC_OK;
 }
 
-uint64_t fc_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+uint64_t fc_kernel_launches(void) { return launch_counter().load(std::memory_order_relaxed); }
 
 void fc_plan_destroy(fc_plan_t* P) {
   // device tables belong to the process-wide cache (shared by equal shapes)

@@ -457,7 +457,7 @@ fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t*
   if (!(c.rescale_factor > 0)) return fail(FC_ERR_INVALID_ARG, "rescale_factor must be > 0");
   for (int i = 0; i < 3; ++i)
     if (!(c.image_std[i] != 0.0f)) return fail(FC_ERR_INVALID_ARG, "image_std must be non-zero");
-  if (c.token_dtype != FC_TOKENS_F32 && c.token_dtype != FC_TOKENS_BF16)
+  if (c.token_dtype != FC_TOKENS_F32 && c.token_dtype != FC_TOKENS_BF16 && c.token_dtype != FC_TOKENS_U8)
     return fail(FC_ERR_UNSUPPORTED, "unknown token_dtype");
   if (c.color < FC_COLOR_BT601_LIMITED || c.color > FC_COLOR_BT709_FULL)
     return fail(FC_ERR_UNSUPPORTED, "unknown color matrix");

@@ -27,7 +27,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, q):
+def _worker(rank, world, port, case, q, exchange="f32"):
     import sys
     sys.path.insert(0, ROOT)
     import hashlib
@@ -59,21 +59,29 @@ def _worker(rank, world, port, case, q):
         h2, w2 = plan.resized
         host = {i: synth.frame_nv12(W, H, i, "natural", 21) for i in set(frames)}
         rows = rp["row_end"] - rp["row_begin"]
-        shard = (oracle.preprocess([host[f] for f in frames], W, H, w2, h2) if frames
-                 else np.zeros((0, 1176), np.float32))
+        if exchange == "u8":  # NEXT-1: ship the u8 codes, expand on the encoder
+            shard = (oracle.codes_from_resized(oracle.preprocess([host[f] for f in frames], W, H, w2, h2,
+                                                                 want_rgb=True)[2]) if frames
+                     else np.zeros((0, 1176), np.uint8))
+        else:
+            shard = (oracle.preprocess([host[f] for f in frames], W, H, w2, h2) if frames
+                     else np.zeros((0, 1176), np.float32))
         assert shard.shape[0] == rows
         # 3) gather to the encoder rank at the planned row offsets
         maxrows = max(r["row_end"] - r["row_begin"] for r in plan.ranks())
-        buf = torch.zeros((maxrows, 1176), dtype=torch.float32)
+        buf = torch.zeros((maxrows, 1176), dtype=torch.uint8 if exchange == "u8" else torch.float32)
         buf[:rows] = torch.from_numpy(shard)
         enc = plan.cfg.encoder_rank
         gathered = [torch.empty_like(buf) for _ in range(world)] if rank == enc else None
         dist.gather(buf, gathered, dst=enc)
         if rank == enc:
-            full = np.zeros((plan.token_rows, 1176), np.float32)
+            full = np.zeros((plan.token_rows, 1176), shard.dtype)
             for r, rp_r in enumerate(plan.ranks()):
                 n = rp_r["row_end"] - rp_r["row_begin"]
                 full[rp_r["row_begin"]:rp_r["row_end"]] = gathered[r][:n].numpy()
+            if exchange == "u8":  # expand: R5 table per channel of each column
+                lut = np.array([[oracle.normalize_value(v, c) for v in range(256)] for c in range(3)], np.float32)
+                full = lut[(np.arange(1176) // 392)[None, :], full]
             host_all = {i: synth.frame_nv12(W, H, i, "natural", 21) for i in idx}
             ref = oracle.preprocess([host_all[i] for i in idx], W, H, w2, h2)
             assert full.view(np.uint32).tobytes() == ref.view(np.uint32).tobytes(), "gathered != single-GPU result"
@@ -92,16 +100,27 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("case", range(len(CASES)))
-def test_gloo_gather_equals_single_gpu(world, case):
+def _run(world, case, exchange):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES[case], q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASES[case], q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=240) for _ in procs)
     for p in procs:
         p.join(timeout=60)
     assert res == {r: "ok" for r in range(world)}, res
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", range(len(CASES)))
+def test_gloo_gather_equals_single_gpu(world, case):
+    _run(world, case, "f32")
+
+
+@pytest.mark.parametrize("case", [0, 1])
+def test_gloo_u8_exchange_equals_single_gpu(case):
+    """NEXT-1 exchange: u8 codes gathered (4x fewer bytes) and expanded on the
+    encoder give the single-GPU fp32 tokens bit for bit."""
+    _run(3, case, "u8")

@@ -14,6 +14,10 @@ define the reading fix:
                          resize/rescale/normalise off; brute-force index encoding
   end to end            vs transformers Qwen2VLImageProcessorPil._preprocess
   O6     plan checks    brute-force optimum + invariant checker self-test
+  R15    colour variants exhaustive 2^24 vs the real-valued ITU-R matrices
+                         (<= 2 LSB), black/white/grey points, coefficients
+  R16    bf16 tokens    vs torch's float32 -> bfloat16 conversion (RNE)
+  codes  NEXT-1 format  normalised codes == oracle tokens
 A plausible mistake in any of them (dropped term, wrong sign/index,
 transposed operand) fails at least one of these.
 """
@@ -381,3 +385,15 @@ def test_plan_checker_rejects_bad_plans(oracle):
     bad[0]["gop_end"] = 1  # frame 10 outside owned GOPs
     with pytest.raises(AssertionError):
         oracle.check_rank_plans(gs, 30, sampled, 2, bad, 1, 1)
+
+
+def test_codes_normalise_to_tokens(oracle):
+    """NEXT-1 exchange format: normalising the oracle's u8 codes with the R5
+    table reproduces the (pinned) oracle tokens exactly, odd frame count incl."""
+    rng = np.random.default_rng(3)
+    rs = rng.integers(0, 256, size=(3, 56, 84, 3), dtype=np.uint8)
+    codes = oracle.codes_from_resized(rs)
+    tok = oracle.tokens_from_resized(rs)
+    lut = np.array([[oracle.normalize_value(v, c) for v in range(256)] for c in range(3)], np.float32)
+    ch = np.arange(1176) // 392
+    np.testing.assert_array_equal(lut[ch[None, :], codes].view(np.uint32), tok.view(np.uint32))

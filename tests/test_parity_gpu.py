@@ -334,3 +334,52 @@ def test_bf16_debug_dumps_rejected(fc, cuda):
     with pytest.raises(fc.FcError) as e:
         fc.preprocess_debug(plan, 0, surf)
     assert e.value.name == "FC_ERR_UNSUPPORTED"
+
+
+# ------------------------------------------------------ NEXT-1 u8 exchange
+def _codes_case(fc, oracle, W, H, N, gops, world, kind, seed, **cfg):
+    import torch
+    plan = fc.Plan(fc.VideoMeta(W, H, N, (30, 1), gops), fc.ModelCfg(world_size=world, token_dtype="u8", **cfg))
+    idx = plan.sampled_indices
+    host = {i: synth.frame_nv12(W, H, i, kind, seed) for i in idx}
+    surf = fc.SurfaceTable.from_tensors(synth.to_device(host), N)
+    parts = [fc.preprocess(plan, r, surf) for r in range(world) if plan.rank(r)["row_end"] > plan.rank(r)["row_begin"]]
+    codes = torch.cat(parts, 0)  # what the u8 gather assembles on the encoder
+    torch.cuda.synchronize()
+    assert codes.dtype == torch.uint8 and codes.shape == (plan.token_rows, 1176)
+    h2, w2 = plan.resized
+    ref_tok, _, ref_rs = oracle.preprocess([host[i] for i in idx], W, H, w2, h2, want_rgb=True)
+    np.testing.assert_array_equal(codes.cpu().numpy(), oracle.codes_from_resized(ref_rs))
+    tok = fc.expand_tokens(plan, codes)
+    tok16 = fc.expand_tokens(plan, codes, out_dtype="bf16")
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(tok.cpu().numpy().view(np.uint32), ref_tok.view(np.uint32))
+    np.testing.assert_array_equal(tok16.view(torch.int16).cpu().numpy().view(np.uint16), oracle.to_bf16(ref_tok))
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_u8_codes_exchange_and_expand(fc, oracle, cuda, world):
+    """NEXT-1: u8 codes per rank (concatenated as the gather would) == the
+    oracle's resized values in token layout; fc_expand_tokens of them == the
+    oracle's fp32 tokens (and their bf16 rounding) bit for bit."""
+    _codes_case(fc, oracle, 320, 240, 300, list(range(0, 300, 30)), world, "natural", 31, sample_fps=2.0)
+    _codes_case(fc, oracle, 200, 120, 100, list(range(0, 100, 10)), world, "uniform", 32, sampling="explicit",
+                explicit_indices=[0, 3, 12, 13, 14, 25, 41, 42, 57, 70, 81])
+
+
+def test_u8_codes_full_c2(fc, oracle, cuda):
+    """Config 2 through the u8 path (one launch) + expand, sampled pairs vs the oracle."""
+    import torch
+    wl = synth.CONFIGS["c2"]
+    plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
+                   fc.ModelCfg(sample_fps=wl.sample_fps, token_dtype="u8"))
+    idx = plan.sampled_indices
+    host = synth.frames_nv12(wl, idx, "natural")
+    surf = fc.SurfaceTable.from_tensors(synth.to_device(host), wl.num_frames)
+    tok = fc.expand_tokens(plan, fc.preprocess(plan, 0, surf))
+    torch.cuda.synchronize()
+    rpp = plan.grid_thw[1] * plan.grid_thw[2]
+    h2, w2 = plan.resized
+    for t in _sample_pairs(plan.grid_thw[0]):
+        ref = oracle.preprocess([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2)
+        np.testing.assert_array_equal(tok[t * rpp:(t + 1) * rpp].cpu().numpy().view(np.uint32), ref.view(np.uint32))

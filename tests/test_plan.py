@@ -199,7 +199,7 @@ def test_missing_surface_reported(fc):
     assert fc._native.STATUS[st] == "FC_ERR_MISSING_SURFACE"
 
 
-@pytest.mark.parametrize("field,value", [("token_dtype", 2), ("color", 4), ("color", -1)])
+@pytest.mark.parametrize("field,value", [("token_dtype", 3), ("color", 4), ("color", -1)])
 def test_unknown_variant_enums_rejected(fc, field, value):
     """NEXT-4 variant enums are validated by fc_plan (S:34 structured errors)."""
     meta = fc.VideoMeta(64, 48, 100, (30, 1), [0, 50])
