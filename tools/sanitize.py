@@ -1,0 +1,39 @@
+"""Small runs of every kernel path for compute-sanitizer (memcheck / racecheck /
+synccheck / initcheck): fused kernel fp32 + debug + bf16 + u8 codes, a batch,
+a >120-frame launch (device descriptor), and fc_expand_tokens."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2512_17574_b200 as fc  # noqa: E402
+import synth  # noqa: E402
+
+
+def run(W, H, N, gops, **cfg):
+    plan = fc.Plan(fc.VideoMeta(W, H, N, (30, 1), gops), fc.ModelCfg(**cfg))
+    host = {i: synth.frame_nv12(W, H, i, "natural", 3) for i in plan.sampled_indices}
+    dev = synth.to_device(host)
+    surf = fc.SurfaceTable.from_tensors(dev, N)
+    return plan, surf, dev
+
+
+plan, surf, _ = run(320, 240, 120, [0], sample_fps=2.0)
+fc.preprocess(plan, 0, surf)
+fc.preprocess_debug(plan, 0, surf)
+plan16, surf16, _ = run(200, 120, 40, [0, 20], sampling="explicit", explicit_indices=[1, 5, 9], token_dtype="bf16")
+fc.preprocess(plan16, 0, surf16)
+plan8, surf8, _ = run(320, 240, 120, [0], sample_fps=2.0, token_dtype="u8")
+codes = fc.preprocess(plan8, 0, surf8)
+fc.expand_tokens(plan8, codes)
+fc.expand_tokens(plan8, codes, out_dtype="bf16")
+jobs = [run(256, 144, 60, [0, 30], sample_fps=2.0) for _ in range(3)]
+fc.preprocess_batch([(p, 0, s) for p, s, _ in jobs])
+planL, surfL, _ = run(64, 48, 300, list(range(0, 300, 30)), sampling="explicit", explicit_indices=list(range(0, 260, 2)))
+fc.preprocess(planL, 0, surfL)  # 130 frames: tensor maps in the device descriptor
+plan224, surf224, _ = run(1920, 1080, 8, [0], sampling="explicit", explicit_indices=[0, 3],
+                          resized_height=224, resized_width=224)
+fc.preprocess(plan224, 0, surf224)  # KSH=KSV=3, 28-column strips
+torch.cuda.synchronize()
+print("sanitize workload done")
