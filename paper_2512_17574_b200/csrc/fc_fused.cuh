@@ -1,0 +1,451 @@
+// fc_fused.cuh -- the fused sm_100a kernel of the preprocessing hot path
+// (template; instantiated in fc_inst_ks*.cu, launched by fc_kernels.cu).
+//
+// One launch per rank (or per batch of requests) computes, for each temporal
+// pair of the sampled frames (Alg. 1 l.21-22, P:386-389,
+// "convert_AVframes_to_tensor_and_resize"):
+//   a5  NV12 -> RGB, integer YUV matrix (BT.601 limited by default)  (R3, R15)
+//   a6  horizontal Pillow-bicubic pass, u8 intermediate             (R4)
+//   a7  vertical Pillow-bicubic pass                                 (R4)
+//   a8  rescale + normalise through a 3x256 table                    (R5, R16)
+//   a9  temporal pad + 14x14x2 patchify in 2x2 merge order           (R6)
+// in ONE pass over HBM: NV12 bytes are read once (plus strip halos), tokens
+// are written once.  Work unit: one temporal pair x one strip of 2 merge
+// blocks (56 output columns), walking down the frame one merge-block row (28
+// output rows, a "band") at a time.  Source rows are converted and
+// horizontally filtered once each into a ring of u8 rows (column-major, so
+// that 4 vertically adjacent taps are one 32-bit word); the vertical pass
+// reads the ring.  Both resize passes are exact int8 tensor-core MMAs
+// (mma.sync m16n8k32, u8 x s8/u8 -> s32) on byte planes of Pillow's 22-bit
+// weights: sum px*iw = ((D2 << 8) + D1) << 8 + D0.  DESIGN.md section 6.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "fc_device.cuh"
+#include "fc_internal.h"
+
+namespace fc {
+
+constexpr int kChunkRows = 16;             // source rows per chunk
+constexpr int kTileN = 8;                  // outputs per H-pass MMA tile (N of m16n8k32)
+constexpr int kStrip = 56;                 // output columns per strip: 2 merge blocks = 4 patches
+constexpr int kComputeWarps = 8;
+constexpr int kPlanesPerWarp = 24 / kComputeWarps;  // V pass: (4 row groups x 6 planes) / warps
+static_assert(kPlanesPerWarp == 3, "V pass: each warp owns the 3 channels of one frame");
+constexpr int kComputeThreads = 32 * kComputeWarps;
+constexpr int kThreads = kComputeThreads;  // thread 0 also issues the TMA copies
+constexpr int kMaxInlineFrames = 120;      // tensor maps (2 per frame) passed by value up to this many frames
+constexpr int kRingStride = 6 * kStrip + 24;  // ring row stride (words): == 8 mod 32, conflict-free A loads
+static_assert(kRingStride % 32 == 8, "ring stride must be 8 mod 32");
+constexpr int kStages = 4;                 // raw NV12 chunk buffers (TMA runs kStages-1 chunks ahead)
+constexpr int kIssueWarp = kComputeWarps - 1;  // owns no H-pass tile (7 tiles of 8 cover a 56-column strip)
+static_assert((kStrip + kTileN - 1) / kTileN < kComputeWarps, "the TMA issuing warp must own no H tile");
+
+struct Params {
+  int W, H, W2, H2;
+  int gh2, gw2;       // merge blocks per column / row
+  int nstrips, npairs;
+  int sw, htiles;      // strip width (84 or 28 output columns), H tiles per strip
+  int SWP;            // RGB-plane row stride (odd multiple of 16)
+  int SWPN;           // converted (and TMA-loaded) bytes per row: taps of the strip's outputs
+  int BW, NX;         // TMA box width (<= 256) and boxes per row: NX*BW >= SWPN
+  int bwshift, bwmask;  // box index / offset of a byte column (NX == 1: 31 / ~0; else BW = 256: 8 / 255)
+  int TR, TRW;        // ring rows / words
+  int nchunks;        // chunks any band needs
+  const int32_t* hx;    // H table: xmin per output column
+  const int32_t* hxs;   // H MMA tiles: 4-aligned window start per tile of 8 outputs
+  const uint32_t* hfr;  // H MMA tiles: B fragments [tile][KS][3][32][2]
+  const int32_t* vx;    // V table: ymin / count per output row
+  const int32_t* vcnt;
+  const int32_t* vys;   // V MMA groups: 4-aligned window start per (band, group of 8 rows)
+  const uint32_t* vfr;  // V MMA groups: B fragments [group][KS][3][32][2]
+  const uint32_t* lut;  // 3 x 256 token bits (fp32, or bf16 zero-extended)
+  uint32_t ckR, ckG, ckGv, ckB;  // colour matrix (R3/R15): packed s16 (Y, chroma) coefficient pairs for dp2a
+  int cbR, cbG, cbB;             // colour biases: -y0*cY - 128*(chroma coefficients) + 128
+  void* tokens;       // first token row of this launch's first pair
+  uint8_t* dbg_src;   // [nframes_total, H, W, 3] or null
+  uint8_t* dbg_rs;    // [nframes_total, H2, W2, 3] or null
+  int frame_base;     // index of fr[0] within the rank's frame list (debug dumps)
+  uint32_t trw_magic;  // ceil(2^32 / TRW): x mod TRW = x - TRW * umulhi(x, magic) for the row words used
+  int nframes;
+  int ppj;            // pairs per job (batch launches; == npairs for one job)
+  void* const* tokj;  // device: per-job token base (batch launches) or null -> tokens
+  const CUtensorMap* tmg;  // device copy of the maps (launches past kMaxInlineFrames frames) or null -> tm
+  CUtensorMap tm[2 * kMaxInlineFrames];  // per frame: Y plane (box BW x 16), UV plane (box BW x 8)
+};
+
+// Walk of one CTA's work: contiguous (pair, strip, band) items, split into
+// runs that stay inside one (pair, strip).
+struct Run {
+  int pair, strip, hb0, hb1, kfirst, klast;
+};
+
+__device__ __forceinline__ bool next_run(const Params& p, int& cur, int i1, Run& r) {
+  if (cur >= i1) return false;
+  const int ps = cur / p.gh2;
+  r.hb0 = cur - ps * p.gh2;
+  r.pair = ps / p.nstrips;
+  r.strip = ps - r.pair * p.nstrips;
+  r.hb1 = min(p.gh2, r.hb0 + (i1 - cur));
+  cur += r.hb1 - r.hb0;
+  r.kfirst = (__ldg(p.vx + 28 * r.hb0) & ~3) / kChunkRows;
+  r.klast = min(p.nchunks, (__ldg(p.vx + 28 * r.hb1 - 1) + __ldg(p.vcnt + 28 * r.hb1 - 1) + kChunkRows - 1) / kChunkRows);
+  return true;
+}
+
+// Issue the TMA tensor copies of one 16-row chunk into a raw stage (one
+// thread): per frame of the pair, NX boxes of Y (BW x 16 rows) then NX boxes
+// of UV (BW x 8 rows), after arming the stage's full barrier with their bytes.
+__device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, int k, uint8_t* raw, uint64_t* bar) {
+  const CUtensorMap* tm = p.tmg != nullptr ? p.tmg : p.tm;
+  fence_proxy_async();
+  mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * 24 * p.BW * p.NX));
+  for (int f = 0; f < 2; ++f)
+    for (int pl = 0; pl < 2; ++pl)
+      for (int sub = 0; sub < p.NX; ++sub) {
+        uint8_t* dst = raw + f * 24 * p.BW * p.NX + (pl ? 16 * p.BW * p.NX + sub * 8 * p.BW : sub * 16 * p.BW);
+        tma_load_2d(dst, &tm[2 * (2 * pair + f) + pl], SX0 + sub * p.BW,
+                    pl ? k * (kChunkRows / 2) : k * kChunkRows, bar);
+      }
+}
+
+// Persistent fused kernel, 8 warps, 3 CTAs/SM.  Per 16-row chunk:
+//   lane 0 of warp 7 refills the raw stage just converted with the chunk 4
+//       ahead (2-D TMA, mbarrier expect_tx) beside the H pass;
+//   all warps: a5 colour (dp2a) -> RGB planes; barrier;
+//   warps 0..6: a6 horizontal pass, warp w owns output tile w (8 columns) of
+//       the strip; three byte-plane MMAs per 16 rows x 8 outputs -> u8 ring
+//       (4 source rows per 32-bit word); barrier.
+// Per band: a7 vertical pass, warp w owns 8-row group (w&3) and the three
+// channels of frame w>>2; one MMA tile per 14-column patch, then a8 table +
+// a9 patch-order stores; barrier.
+// Work items are (pair, strip, band) triples; CTA b takes [b*T/G, (b+1)*T/G).
+// Strips are whole merge blocks, so every token row is written by one CTA in
+// one band (no partial-sector merging across CTAs in L2).
+template <int KSH, int KSV, bool DBG, int TOK>
+__global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_constant__ Params p) {
+  constexpr int SW = kStrip;
+  constexpr int CH = kChunkRows;
+  constexpr int RS = kRingStride;
+
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint32_t* lut = reinterpret_cast<uint32_t*>(smem);              // 3 x 256 token bits at offset 0
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 3072);      // kStages full barriers
+  const int RAWF = 24 * p.BW * p.NX;                              // raw bytes per frame per stage
+  uint8_t* raw = smem + 3072 + 128;                               // [kStages][2 f][Y boxes | UV boxes]
+  const int SWP = p.SWP;
+  uint8_t* rgb = raw + kStages * 2 * RAWF;                        // [2 f][3 c][16 rows][SWP]
+  uint32_t* ring = reinterpret_cast<uint32_t*>(rgb + 6 * CH * SWP);  // [TRW][RS] words: [w][f][c][x]
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, tq = lane & 3;
+  const bool issuer = tid == kIssueWarp * 32;  // lane 0 of the warp without an H tile issues the TMA copies
+
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < 768; i += kThreads) lut[i] = __ldg(p.lut + i);
+  // bytes of the RGB planes past the converted width are only ever multiplied
+  // by zero weights (MMA read-ahead); keep them zero, never garbage
+  for (int i = tid; i < 6 * CH * SWP / 16; i += kThreads)
+    reinterpret_cast<uint4*>(rgb)[i] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+
+  const int total = p.npairs * p.nstrips * p.gh2;
+  const int i0 = static_cast<int>((static_cast<long long>(blockIdx.x) * total) / gridDim.x);
+  const int i1 = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * total) / gridDim.x);
+
+  // ------------------------------------------------------------ compute warps
+  // colour items (frame, row, 16-pixel group): at most 2 per thread; their
+  // offsets are launch constants (raw stage: Y / UV byte, RGB plane byte)
+  const int NQ16 = p.SWPN >> 4;
+  const int citems = 2 * CH * NQ16;
+  int cy[2], cuv[2], crgb[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int it = tid + e * kComputeThreads;
+    const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
+    const int xb = 16 * q, sub = xb >> p.bwshift, xo = xb & p.bwmask;
+    cy[e] = f * RAWF + (sub * 16 + rr) * p.BW + xo;
+    cuv[e] = f * RAWF + 16 * p.BW * p.NX + (sub * 8 + (rr >> 1)) * p.BW + xo;
+    crgb[e] = ((f * 3) * CH + rr) * SWP + xb;
+  }
+  const uint32_t rgb_s = smem_u32(rgb);
+  const uint32_t ring_s = smem_u32(ring);
+  const uint32_t lut_s = smem_u32(lut);
+  // V-pass role: row group vjg, planes [kPlanesPerWarp*vsub, +kPlanesPerWarp)
+  const int vjg = warp & 3, vsub = warp >> 2;
+  const int j0 = 8 * vjg + 2 * tq;                 // output rows j0, j0+1 of the band
+  const bool jok0 = j0 < 28, jok1 = j0 + 1 < 28;   // group 3 covers rows 24..31
+  const bool xok1 = g < 6;                         // second column g+8 inside the 14-wide patch
+  // token offset of (row j, patch column 0) within a band's token block (R6):
+  // row part hm*2*1176 + ph*14
+  const int jo0 = (j0 / 14) * 2 * kCols + (j0 % 14) * 14;
+
+  uint32_t seq = 0;
+  int cur = i0;
+  Run r;
+  while (next_run(p, cur, i1, r)) {
+    const int X0 = r.strip * p.sw;
+    const int SX0 = __ldg(p.hx + X0) & ~15;
+    const int npatch = min(p.sw / 14, (p.W2 - X0) / 14);  // valid patches in this strip
+    const bool hact = warp < p.htiles;
+    // H-pass B fragments of this warp's output tile (constant over the strip)
+    const int htile = r.strip * p.htiles + min(warp, p.htiles - 1);
+    uint32_t hb[KSH][3][2];
+    {
+      const uint32_t* f = p.hfr + static_cast<size_t>(htile) * KSH * 3 * 64 + lane * 2;
+#pragma unroll
+      for (int k = 0; k < KSH; ++k)
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl) {
+          hb[k][pl][0] = __ldg(f + (k * 3 + pl) * 64);
+          hb[k][pl][1] = __ldg(f + (k * 3 + pl) * 64 + 1);
+        }
+    }
+    // A-fragment byte addresses in an RGB plane: rows g, g+8; columns xs + 4t (+16)
+    const uint32_t hA0 = rgb_s + g * SWP + (hact ? __ldg(p.hxs + htile) - SX0 : 0) + 4 * tq;
+    const uint32_t hA1 = hA0 + 8 * SWP;
+    // ring columns of this thread's outputs (2t, 2t+1 of the tile); masked past the strip / frame
+    const int ho = warp * kTileN + 2 * tq;
+    const bool hst0 = hact && ho < p.sw && X0 + ho < p.W2;
+    const bool hst1 = hact && ho + 1 < p.sw && X0 + ho + 1 < p.W2;
+    int next_k = r.kfirst;
+    // ring words of source rows kfirst*16 + g and + g + 8 (advanced per chunk)
+    int hwA = ((r.kfirst * CH) / 4 + (g >> 2)) % p.TRW;
+    int hwB = ((r.kfirst * CH) / 4 + 2 + (g >> 2)) % p.TRW;
+    // prefill: the run's first kStages chunks (every stage is free: the previous
+    // run consumed all it issued, before the barrier that ended its last band)
+    if (issuer)
+      for (int j = 0; j < kStages && r.kfirst + j < r.klast; ++j)
+        issue_chunk(p, r.pair, SX0, r.kfirst + j, raw + ((seq + j) % kStages) * 2 * RAWF, &full[(seq + j) % kStages]);
+    for (int hb_ = r.hb0; hb_ < r.hb1; ++hb_) {
+      const int yo0 = hb_ * 28;
+      const int kneed = min(p.nchunks, (__ldg(p.vx + yo0 + 27) + __ldg(p.vcnt + yo0 + 27) + CH - 1) / CH);
+      for (; next_k < kneed; ++next_k, ++seq) {
+        const int k = next_k;
+        const int buf = seq % kStages;
+        const uint8_t* rawb = raw + buf * 2 * RAWF;
+        mbar_wait(&full[buf], (seq / kStages) & 1);
+        // ---- a5: NV12 -> RGB planes, 16 pixels per item
+        auto convert = [&](int oy, int ouv, int orgb, int e) {
+            const uint4 Yv = *reinterpret_cast<const uint4*>(rawb + oy);
+            const uint4 UVv = *reinterpret_cast<const uint4*>(rawb + ouv);
+            uint4 Rv, Gv, Bv;
+            yuv2rgb_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
+            yuv2rgb_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
+            yuv2rgb_4(Yv.z, UVv.z, Rv.z, Gv.z, Bv.z, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
+            yuv2rgb_4(Yv.w, UVv.w, Rv.w, Gv.w, Bv.w, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
+            uint8_t* dst = rgb + orgb;
+            *reinterpret_cast<uint4*>(dst) = Rv;
+            *reinterpret_cast<uint4*>(dst + CH * SWP) = Gv;
+            *reinterpret_cast<uint4*>(dst + 2 * CH * SWP) = Bv;
+            if (DBG && p.dbg_src != nullptr) {
+              const int it = tid + e * kComputeThreads;
+              const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
+              const int y = k * CH + rr, x = SX0 + 16 * q;
+              if (y < p.H) {
+                const uint32_t cw[3][4] = {{Rv.x, Rv.y, Rv.z, Rv.w}, {Gv.x, Gv.y, Gv.z, Gv.w}, {Bv.x, Bv.y, Bv.z, Bv.w}};
+                const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
+                for (int i = 0; i < 16 && x + i < p.W; ++i)
+                  for (int c = 0; c < 3; ++c)
+                    p.dbg_src[((fi * p.H + y) * p.W + x + i) * 3 + c] = (cw[c][i >> 2] >> (8 * (i & 3))) & 0xFF;
+              }
+            }
+        };
+        {
+          if constexpr (KSH <= 2) {  // <= 2 items per thread (host-checked), offsets precomputed
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              if (tid + e * kComputeThreads >= citems) break;
+              convert(cy[e], cuv[e], crgb[e], e);
+            }
+          } else {  // very wide resize windows: any number of items
+            for (int it = tid; it < citems; it += kComputeThreads) {
+              const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
+              const int xb = 16 * q, sub = xb >> p.bwshift, xo = xb & p.bwmask;
+              convert(f * RAWF + (sub * 16 + rr) * p.BW + xo, f * RAWF + 16 * p.BW * p.NX + (sub * 8 + (rr >> 1)) * p.BW + xo,
+                      ((f * 3) * CH + rr) * SWP + xb, (it - tid) / kComputeThreads);
+            }
+          }
+        }
+        bar_sync(1, kComputeThreads);              // RGB planes complete; raw stage free
+        // refill the stage just converted with chunk k + kStages; the issuing
+        // warp owns no H tile, so this runs beside the H pass, off the critical path
+        if (issuer && k + kStages < r.klast) issue_chunk(p, r.pair, SX0, k + kStages, raw + buf * 2 * RAWF, &full[buf]);
+        // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of 3 for ILP
+        if (hact) {
+          const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + (g & 3);
+          const uint32_t dB = ring_s + (hwB * RS + ho) * 4 + (g & 3);
+          constexpr int HG = KSH == 1 ? 3 : 2;  // planes interleaved per group (ILP vs registers)
+#pragma unroll
+          for (int fg = 0; fg < 6; fg += HG) {
+            uint32_t a[HG][KSH][4];
+#pragma unroll
+            for (int e = 0; e < HG; ++e)
+#pragma unroll
+              for (int kk = 0; kk < KSH; ++kk) {
+                const uint32_t po = (fg + e) * CH * SWP + 32 * kk;
+                a[e][kk][0] = lds32(hA0 + po);
+                a[e][kk][1] = lds32(hA1 + po);
+                a[e][kk][2] = lds32(hA0 + po + 16);
+                a[e][kk][3] = lds32(hA1 + po + 16);
+              }
+            int d2[HG][4], d1[HG][4], d0[HG][4];
+#pragma unroll
+            for (int e = 0; e < HG; ++e) fir_mma_planes<KSH>(d2[e], d1[e], d0[e], a[e], hb);
+#pragma unroll
+            for (int e = 0; e < HG; ++e) {
+              // clip8 (R4): d0,d1 = row g, columns ho, ho+1; d2,d3 = row g+8
+              const uint32_t off = (fg + e) * SW * 4;
+              uint32_t q[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                q[i] = static_cast<uint32_t>(add_min_relu(combine_planes(d2[e][i], d1[e][i], d0[e][i]), 0,
+                                                          (1 << 30) - 1)) >> 22;
+              if (hst0) {
+                sts8(dA + off, q[0]);
+                sts8(dB + off, q[2]);
+              }
+              if (hst1) {
+                sts8(dA + off + 4, q[1]);
+                sts8(dB + off + 4, q[3]);
+              }
+            }
+          }
+        }
+        // advance this thread's two ring rows by one chunk (4 words), wrapping
+        hwA += 4;
+        hwA -= hwA >= p.TRW ? p.TRW : 0;
+        hwB += 4;
+        hwB -= hwB >= p.TRW ? p.TRW : 0;
+        bar_sync(1, kComputeThreads);  // ring rows complete, RGB planes free
+      }
+      // ---- a7 + a8 + a9: vertical pass (MMA), normalise, patchify
+      {
+        const int grp = hb_ * 4 + vjg;
+        uint32_t vb[KSV][3][2];
+        const uint32_t* f = p.vfr + static_cast<size_t>(grp) * KSV * 3 * 64 + lane * 2;
+#pragma unroll
+        for (int kk = 0; kk < KSV; ++kk)
+#pragma unroll
+          for (int pl = 0; pl < 3; ++pl) {
+            vb[kk][pl][0] = __ldg(f + (kk * 3 + pl) * 64);
+            vb[kk][pl][1] = __ldg(f + (kk * 3 + pl) * 64 + 1);
+          }
+        const int ys = __ldg(p.vys + grp);
+        // A rows: columns (g, g+8) of a patch; k = source rows ys + 32kk + 4t (+16)
+        uint32_t rb[KSV][2];
+        {
+          const uint32_t yw = static_cast<uint32_t>(ys) >> 2;
+          int w = static_cast<int>(yw - p.TRW * __umulhi(yw, p.trw_magic)) + tq;  // (ys/4) mod TRW
+#pragma unroll
+          for (int kk = 0; kk < KSV; ++kk) {
+            const int wa = w >= p.TRW ? w - p.TRW : w;
+            const int wb4 = wa + 4 >= p.TRW ? wa + 4 - p.TRW : wa + 4;
+            rb[kk][0] = ring_s + (wa * RS + kPlanesPerWarp * vsub * SW + g) * 4;
+            rb[kk][1] = ring_s + (wb4 * RS + kPlanesPerWarp * vsub * SW + g) * 4;
+            w = wa + 8;
+          }
+        }
+        // token block of this (pair, band, strip); patch q of the strip starts at
+        // column offset (X0 + 14 q): merge block wb = (X0/28) + q/2, sub-block wm = q&1
+        // first token row of this pair (R6: a job's pairs are consecutive gh*gw-row blocks)
+        const size_t pair_rows = static_cast<size_t>(p.gh2) * p.gw2 * 4;
+        using TokT = std::conditional_t<TOK == FC_TOKENS_BF16, uint16_t,
+                                        std::conditional_t<TOK == FC_TOKENS_U8, uint8_t, float>>;
+        TokT* tpair;
+        if (p.tokj != nullptr) {
+          const int job = r.pair / p.ppj;
+          tpair = static_cast<TokT*>(p.tokj[job]) + static_cast<size_t>(r.pair - job * p.ppj) * pair_rows * kCols;
+        } else {
+          tpair = static_cast<TokT*>(p.tokens) + static_cast<size_t>(r.pair) * pair_rows * kCols;
+        }
+        TokT* tb = tpair + (static_cast<size_t>(hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + g;
+#pragma unroll
+        for (int e = 0; e < kPlanesPerWarp; ++e) {
+          // this warp's planes are frame f = vsub, channels c = e (plane index 3f + c)
+          const int f = vsub, c = e;
+          const uint32_t lutc = lut_s + c * 1024;
+          TokT* tp = tb + (c * 2 + f) * 196;
+          constexpr int VG = KSV == 1 ? 2 : 1;  // patches interleaved per group
+#pragma unroll
+          for (int q0 = 0; q0 < kStrip / 14; q0 += VG) {
+            if (q0 >= npatch) break;
+            uint32_t a[VG][KSV][4];
+#pragma unroll
+            for (int e2 = 0; e2 < VG; ++e2)
+#pragma unroll
+              for (int kk = 0; kk < KSV; ++kk) {
+                const uint32_t co = (e * SW + 14 * (q0 + e2)) * 4;
+                a[e2][kk][0] = lds32(rb[kk][0] + co);
+                a[e2][kk][1] = lds32(rb[kk][0] + co + 32);
+                a[e2][kk][2] = lds32(rb[kk][1] + co);
+                a[e2][kk][3] = lds32(rb[kk][1] + co + 32);
+              }
+            int d2[VG][4], d1[VG][4], d0[VG][4];
+#pragma unroll
+            for (int e2 = 0; e2 < VG; ++e2) fir_mma_planes<KSV>(d2[e2], d1[e2], d0[e2], a[e2], vb);
+#pragma unroll
+            for (int e2 = 0; e2 < VG; ++e2) {
+              const int q = q0 + e2;
+              if (q >= npatch) break;
+              // d0,d1: column g, rows j0, j0+1; d2,d3: column g+8
+              uint32_t sv[4];
+              uint32_t o[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                sv[i] = static_cast<uint32_t>(
+                    add_min_relu(combine_planes(d2[e2][i], d1[e2][i], d0[e2][i]), 0, (1 << 30) - 1));
+                if constexpr (TOK == FC_TOKENS_U8)
+                  o[i] = sv[i] >> 22;  // the u8 code (NEXT-1 exchange format)
+                else
+                  o[i] = lds32(lutc + ((sv[i] >> 20) & 0x3FCu));
+              }
+              TokT* op = tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
+              st_cs_pred(op, o[0], jok0);
+              st_cs_pred(op + 14, o[1], jok1);
+              st_cs_pred(op + 8, o[2], jok0 && xok1);
+              st_cs_pred(op + 22, o[3], jok1 && xok1);
+              if (DBG && p.dbg_rs != nullptr) {
+                const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
+                for (int ee = 0; ee < 4; ++ee) {
+                  const int x = X0 + 14 * q + g + ((ee >= 2) ? 8 : 0), j = j0 + (ee & 1);
+                  if ((ee < 2 || xok1) && x < p.W2 && j < 28)
+                    p.dbg_rs[((fi * p.H2 + yo0 + j) * p.W2 + x) * 3 + c] = sv[ee] >> 22;
+                }
+              }
+            }
+          }
+        }
+      }
+      bar_sync(1, kComputeThreads);  // ring may be overwritten by the next chunks
+    }
+  }
+}
+
+
+// ------------------------------------------------------------ instances
+using KernelFn = void (*)(Params);
+
+struct Instance {
+  int ksh, ksv;
+  KernelFn fn, fn_dbg, fn_bf16, fn_u8;  // fp32 tokens / + parity-test dumps / bf16 tokens / u8 codes
+};
+
+// One translation unit per KSH instantiates its instances (parallel build).
+#define FC_INST(A, B)                                                                                  \
+  Instance{A, B, fc_fused_kernel<A, B, false, FC_TOKENS_F32>, fc_fused_kernel<A, B, true, FC_TOKENS_F32>, \
+           fc_fused_kernel<A, B, false, FC_TOKENS_BF16>, fc_fused_kernel<A, B, false, FC_TOKENS_U8>}
+void instances_ksh1(Instance* out);  // out[0..3] = KSV 1..4
+void instances_ksh2(Instance* out);
+void instances_ksh3(Instance* out);
+void instances_ksh4(Instance* out);
+
+}  // namespace fc
