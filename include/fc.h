@@ -227,6 +227,34 @@ fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* rank
                               const fc_nv12_surface* const* surfaces, const int64_t* num_surfaces,
                               void* const* tokens, void* stream);
 
+/* NEXT-2 -- paged token output (Fig. 10; SPEC embed_buffer
+ * write_chunk).  The rank's token rows are written, in order, as ONE write
+ * chunk of a paged embedding buffer, straight from the kernel's epilogue (no
+ * linear staging buffer): row i of the rank goes to pool row
+ *     page_ids[s / page_rows] * page_rows + s % page_rows,   s = first_offset + i.
+ *   pool:          device pointer, pool_pages pages of page_rows x 1176 tokens
+ *                  (element type cfg.token_dtype: F32 or BF16).
+ *   page_rows:     tokens per page; a power of two.
+ *   page_ids:      HOST array of num_pages page ids -- the request's
+ *                  pv_page_indices segment for this write -- each in
+ *                  [0, pool_pages); copied (uploaded with the launch).
+ *   first_offset:  pv_cu_page_len mod page_rows (tokens already in the first
+ *                  page), in [0, page_rows).
+ * num_pages must cover ceil((first_offset + rows) / page_rows).  Rows of other
+ * requests in the same pages are untouched.  Errors as fc_preprocess, plus
+ * FC_ERR_INVALID_ARG for an inconsistent page table (nothing is launched). */
+typedef struct {
+  void* pool;
+  int64_t pool_pages;
+  int32_t page_rows;
+  int32_t num_pages;
+  const int32_t* page_ids;
+  int64_t first_offset;
+} fc_paged_tokens;
+
+fc_status fc_preprocess_paged(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
+                              int64_t num_surfaces, const fc_paged_tokens* out, int64_t grid_thw[3], void* stream);
+
 /* fc_expand_tokens -- R5 on u8 codes (FC_TOKENS_U8 output of fc_preprocess,
  * usually gathered from all ranks): tokens[r][i] = table[channel(i)][codes[r][i]]
  * with channel(i) = i / 392 (columns are (c, tp, ph, pw)).  The table is the

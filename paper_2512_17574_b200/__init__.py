@@ -21,7 +21,7 @@ from . import _native
 from ._native import FcError, FC_TOKEN_COLS, check, lib
 
 __all__ = ["VideoMeta", "ModelCfg", "Plan", "SurfaceTable", "preprocess", "preprocess_debug", "preprocess_batch",
-           "expand_tokens",
+           "expand_tokens", "preprocess_paged",
            "NcclComm", "gather", "FcError", "FC_TOKEN_COLS", "lib"]
 
 
@@ -238,6 +238,20 @@ def preprocess_batch(jobs: Sequence[tuple[Plan, int, SurfaceTable]], outs=None, 
     toks = (ctypes.c_void_p * n)(*[o.data_ptr() for o in outs])
     check(lib().fc_preprocess_batch(plans, ranks, n, surfs, nsurf, toks, _stream_ptr(stream)), "fc_preprocess_batch")
     return outs
+
+
+def preprocess_paged(plan: Plan, rank: int, surfaces: SurfaceTable, pool, page_ids: Sequence[int],
+                     first_offset: int = 0, stream=None) -> None:
+    """fc_preprocess_paged (NEXT-2): write the rank's token rows, in order, as
+    one write chunk of a paged buffer.  pool: device tensor [pool_pages,
+    page_rows, 1176] of the plan's token dtype; page_ids: this write's pages
+    (pv_page_indices segment); first_offset: pv_cu_page_len mod page_rows."""
+    ids = (ctypes.c_int32 * max(len(page_ids), 1))(*page_ids)
+    d = _native.PagedTokensC(ctypes.c_void_p(pool.data_ptr()), pool.shape[0], pool.shape[1], len(page_ids),
+                             ctypes.cast(ids, ctypes.POINTER(ctypes.c_int32)), first_offset)
+    grid = (ctypes.c_int64 * 3)()
+    check(lib().fc_preprocess_paged(plan.handle, rank, surfaces.arr, surfaces.n, ctypes.byref(d), grid,
+                                    _stream_ptr(stream)), "fc_preprocess_paged")
 
 
 def expand_tokens(plan: Plan, codes, out=None, out_dtype: str = "f32", stream=None):

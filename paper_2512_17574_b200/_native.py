@@ -51,6 +51,12 @@ class ModelCfgC(ctypes.Structure):
                 ("encoder_rank", ctypes.c_int32), ("token_dtype", ctypes.c_int), ("color", ctypes.c_int)]
 
 
+class PagedTokensC(ctypes.Structure):
+    _fields_ = [("pool", ctypes.c_void_p), ("pool_pages", ctypes.c_int64), ("page_rows", ctypes.c_int32),
+                ("num_pages", ctypes.c_int32), ("page_ids", ctypes.POINTER(ctypes.c_int32)),
+                ("first_offset", ctypes.c_int64)]
+
+
 class PlanInfoC(ctypes.Structure):
     _fields_ = [("grid_thw", ctypes.c_int64 * 3), ("resized_h", ctypes.c_int32), ("resized_w", ctypes.c_int32),
                 ("num_sampled", ctypes.c_int64), ("pad_frames", ctypes.c_int64), ("token_rows", ctypes.c_int64),
@@ -73,7 +79,7 @@ class Nv12SurfaceC(ctypes.Structure):
 EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_get", "fc_plan_sampled_indices",
            "fc_plan_rank", "fc_preprocess", "fc_preprocess_debug", "fc_preprocess_batch", "fc_nccl_unique_id",
            "fc_nccl_comm_init", "fc_nccl_comm_destroy", "fc_gather", "fc_status_string", "fc_last_error",
-           "fc_abi_version", "fc_kernel_launches", "fc_expand_tokens"]
+           "fc_abi_version", "fc_kernel_launches", "fc_expand_tokens", "fc_preprocess_paged"]
 
 _lib = None
 
@@ -112,6 +118,8 @@ def lib() -> ctypes.CDLL:
     L.fc_abi_version.argtypes = []
     L.fc_abi_version.restype = ctypes.c_int32
     L.fc_expand_tokens.argtypes = [vp, i64, vp, vp, ctypes.c_int, vp]
+    L.fc_preprocess_paged.argtypes = [vp, i32, ctypes.POINTER(Nv12SurfaceC), i64, ctypes.POINTER(PagedTokensC),
+                                      ctypes.POINTER(ctypes.c_int64), vp]
     L.fc_kernel_launches.argtypes = []
     L.fc_kernel_launches.restype = ctypes.c_uint64
     for name in EXPORTS:

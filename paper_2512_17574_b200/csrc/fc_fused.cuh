@@ -73,6 +73,11 @@ struct Params {
   uint32_t trw_magic;  // ceil(2^32 / TRW): x mod TRW = x - TRW * umulhi(x, magic) for the row words used
   int nframes;
   int ppj;            // pairs per job (batch launches; == npairs for one job)
+  // NEXT-2 paged output (PAGED instances): token row i of this launch goes to
+  // pool row page_ids[(page_first + i) >> page_shift] * page_rows + ((page_first + i) & page_mask)
+  const int32_t* page_ids;  // device (launch descriptor)
+  long long page_first;     // pv_cu_page_len mod page_rows (slot of the launch's first row)
+  uint32_t page_shift, page_mask, page_rows;
   void* const* tokj;  // device: per-job token base (batch launches) or null -> tokens
   const CUtensorMap* tmg;  // device copy of the maps (launches past kMaxInlineFrames frames) or null -> tm
   CUtensorMap tm[2 * kMaxInlineFrames];  // per frame: Y plane (box BW x 16), UV plane (box BW x 8)
@@ -126,7 +131,7 @@ __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, 
 // Work items are (pair, strip, band) triples; CTA b takes [b*T/G, (b+1)*T/G).
 // Strips are whole merge blocks, so every token row is written by one CTA in
 // one band (no partial-sector merging across CTAs in L2).
-template <int KSH, int KSV, bool DBG, int TOK>
+template <int KSH, int KSV, bool DBG, int TOK, bool PAGED = false>
 __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_constant__ Params p) {
   constexpr int SW = kStrip;
   constexpr int CH = kChunkRows;
@@ -368,6 +373,20 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
           tpair = static_cast<TokT*>(p.tokens) + static_cast<size_t>(r.pair) * pair_rows * kCols;
         }
         TokT* tb = tpair + (static_cast<size_t>(hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + g;
+        // paged output: the pool row of each patch's token row (merge block q/2,
+        // sub-block q&1, this thread's half hm = j0/14) -- SPEC write_chunk mapping
+        uint32_t prow[4];
+        if constexpr (PAGED) {
+          const long long row0 = static_cast<long long>(r.pair) * static_cast<long long>(pair_rows) +
+                                 (static_cast<long long>(hb_) * p.gw2 + X0 / 28) * 4 + (j0 / 14) * 2;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const long long sl = p.page_first + row0 + (q >> 1) * 4 + (q & 1);
+            prow[q] = q < npatch ? static_cast<uint32_t>(__ldg(p.page_ids + (sl >> p.page_shift))) * p.page_rows +
+                                       static_cast<uint32_t>(sl & p.page_mask)
+                                 : 0u;
+          }
+        }
 #pragma unroll
         for (int e = 0; e < kPlanesPerWarp; ++e) {
           // this warp's planes are frame f = vsub, channels c = e (plane index 3f + c)
@@ -408,7 +427,9 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
                 else
                   o[i] = lds32(lutc + ((sv[i] >> 20) & 0x3FCu));
               }
-              TokT* op = tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
+              TokT* op = PAGED ? static_cast<TokT*>(p.tokens) + static_cast<size_t>(prow[q]) * kCols + (c * 2 + f) * 196 +
+                                     (j0 % 14) * 14 + g
+                               : tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
               st_cs_pred(op, o[0], jok0);
               st_cs_pred(op + 14, o[1], jok1);
               st_cs_pred(op + 8, o[2], jok0 && xok1);
@@ -437,12 +458,14 @@ using KernelFn = void (*)(Params);
 struct Instance {
   int ksh, ksv;
   KernelFn fn, fn_dbg, fn_bf16, fn_u8;  // fp32 tokens / + parity-test dumps / bf16 tokens / u8 codes
+  KernelFn fn_paged, fn_paged_bf16;     // NEXT-2: fp32 / bf16 tokens into a paged pool
 };
 
 // One translation unit per KSH instantiates its instances (parallel build).
 #define FC_INST(A, B)                                                                                  \
   Instance{A, B, fc_fused_kernel<A, B, false, FC_TOKENS_F32>, fc_fused_kernel<A, B, true, FC_TOKENS_F32>, \
-           fc_fused_kernel<A, B, false, FC_TOKENS_BF16>, fc_fused_kernel<A, B, false, FC_TOKENS_U8>}
+           fc_fused_kernel<A, B, false, FC_TOKENS_BF16>, fc_fused_kernel<A, B, false, FC_TOKENS_U8>,   \
+           fc_fused_kernel<A, B, false, FC_TOKENS_F32, true>, fc_fused_kernel<A, B, false, FC_TOKENS_BF16, true>}
 void instances_ksh1(Instance* out);  // out[0..3] = KSV 1..4
 void instances_ksh2(Instance* out);
 void instances_ksh3(Instance* out);

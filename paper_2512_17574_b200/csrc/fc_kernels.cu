@@ -213,7 +213,7 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
 
 struct Geometry {
   int sw, htiles, SWPN, SWP, BW, NX, TR, TRW, nstrips, nchunks;
-  KernelFn fn, fn_dbg, fn_bf16, fn_u8;
+  KernelFn fn, fn_dbg, fn_bf16, fn_u8, fn_paged, fn_paged_bf16;
   size_t smem;
 };
 
@@ -270,6 +270,8 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
       g->fn_dbg = in.fn_dbg;
       g->fn_bf16 = in.fn_bf16;
       g->fn_u8 = in.fn_u8;
+      g->fn_paged = in.fn_paged;
+      g->fn_paged_bf16 = in.fn_paged_bf16;
     }
   }
   if (!g->fn) return fail(FC_ERR_UNSUPPORTED, "no kernel instance for this resize window");
@@ -407,7 +409,7 @@ struct Job {
 // is copied to a stream-ordered device allocation (cudaMallocAsync, freed
 // after the launch in stream order).
 static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, uint8_t* dbg_src,
-                             uint8_t* dbg_rs) {
+                             uint8_t* dbg_rs, const fc_paged_tokens* paged = nullptr) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -432,7 +434,10 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   const fc_token_dtype td = P->cfg.token_dtype;
   if (td != FC_TOKENS_F32 && (dbg_src || dbg_rs))
     return fail(FC_ERR_UNSUPPORTED, "debug dumps are built for fp32 tokens only");
+  if (paged && (td == FC_TOKENS_U8 || jobs.size() != 1))
+    return fail(FC_ERR_UNSUPPORTED, "paged output: one job, F32 or BF16 tokens");
   KernelFn fn = (dbg_src || dbg_rs)      ? g.fn_dbg
+                : paged                ? (td == FC_TOKENS_BF16 ? g.fn_paged_bf16 : g.fn_paged)
                 : td == FC_TOKENS_BF16 ? g.fn_bf16
                 : td == FC_TOKENS_U8   ? g.fn_u8
                                        : g.fn;
@@ -483,7 +488,15 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   prm.nframes = static_cast<int>(nf);
   prm.npairs = static_cast<int>(nf / 2);
   prm.ppj = static_cast<int>(nfj / 2);
-  prm.tokens = jobs[0].tokens;
+  prm.tokens = paged ? paged->pool : jobs[0].tokens;
+  if (paged) {
+    int sh = 0;
+    while ((1 << sh) < paged->page_rows) ++sh;
+    prm.page_shift = static_cast<uint32_t>(sh);
+    prm.page_mask = static_cast<uint32_t>(paged->page_rows - 1);
+    prm.page_rows = static_cast<uint32_t>(paged->page_rows);
+    prm.page_first = paged->first_offset;
+  }
   const bool inline_maps = jobs.size() == 1 && nf <= kMaxInlineFrames;
   std::vector<CUtensorMap> maps(inline_maps ? 0 : 2 * nf);
   CUtensorMap* mp = inline_maps ? prm.tm : maps.data();
@@ -497,14 +510,18 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
     }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   void* desc = nullptr;
-  if (!inline_maps) {
+  if (!inline_maps || paged) {
+    // descriptor sections: [tensor maps | per-job token bases | page ids]
     const size_t mbytes = maps.size() * sizeof(CUtensorMap);
-    const size_t bytes = mbytes + (jobs.size() > 1 ? jobs.size() * sizeof(void*) : 0);
+    const size_t tbytes = jobs.size() > 1 ? jobs.size() * sizeof(void*) : 0;
+    const size_t pbytes = paged ? static_cast<size_t>(paged->num_pages) * sizeof(int32_t) : 0;
+    const size_t bytes = mbytes + tbytes + pbytes;
     std::vector<uint8_t> host(bytes);
     std::memcpy(host.data(), maps.data(), mbytes);
     if (jobs.size() > 1)
       for (size_t j = 0; j < jobs.size(); ++j)
         std::memcpy(host.data() + mbytes + j * sizeof(void*), &jobs[j].tokens, sizeof(void*));
+    if (paged) std::memcpy(host.data() + mbytes + tbytes, paged->page_ids, pbytes);
     e = cudaMallocAsync(&desc, bytes, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (launch descriptor)");
     // pageable source: returns once the bytes are staged, so `host` may die
@@ -513,8 +530,9 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
       cudaFreeAsync(desc, s);
       return cuda_fail(e, "descriptor upload");
     }
-    prm.tmg = reinterpret_cast<const CUtensorMap*>(desc);
+    if (!inline_maps) prm.tmg = reinterpret_cast<const CUtensorMap*>(desc);
     if (jobs.size() > 1) prm.tokj = reinterpret_cast<void* const*>(static_cast<uint8_t*>(desc) + mbytes);
+    if (paged) prm.page_ids = reinterpret_cast<const int32_t*>(static_cast<uint8_t*>(desc) + mbytes + tbytes);
   }
   const int grid = static_cast<int>(std::min<long long>(items, static_cast<long long>(occ) * nsm));
   fn<<<grid, kThreads, g.smem, s>>>(prm);
@@ -527,7 +545,7 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
 
 static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv12_surface* surfaces,
                                  int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream,
-                                 uint8_t* dbg_src, uint8_t* dbg_rs) {
+                                 uint8_t* dbg_src, uint8_t* dbg_rs, const fc_paged_tokens* paged = nullptr) {
   if (!Pc) return fail(FC_ERR_INVALID_ARG, "plan is NULL");
   fc_plan_s* P = const_cast<fc_plan_s*>(Pc);
   if (rank < 0 || rank >= P->world) return fail(FC_ERR_RANK, "rank outside [0, world_size)");
@@ -539,10 +557,24 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
   std::vector<Job> jobs(1);
   fc_status st = rank_frames(P, rank, surfaces, num_surfaces, &jobs[0].frames);
   if (st != FC_OK || jobs[0].frames.empty()) return st;
-  if (!tokens) return fail(FC_ERR_INVALID_ARG, "tokens is NULL");
+  if (!tokens && !paged) return fail(FC_ERR_INVALID_ARG, "tokens is NULL");
+  if (paged) {  // the page table must hold the write (SPEC write_chunk: CapacityError)
+    const fc_rank_plan& rp = P->ranks[rank].p;
+    const int64_t rows = rp.row_end - rp.row_begin;
+    if (!paged->pool || !paged->page_ids || paged->page_rows <= 0 || (paged->page_rows & (paged->page_rows - 1)))
+      return fail(FC_ERR_INVALID_ARG, "paged output: pool/page_ids NULL or page_rows not a power of two");
+    if (paged->first_offset < 0 || paged->first_offset >= paged->page_rows)
+      return fail(FC_ERR_INVALID_ARG, "paged output: first_offset outside [0, page_rows)");
+    if (paged->num_pages < (paged->first_offset + rows + paged->page_rows - 1) / paged->page_rows)
+      return fail(FC_ERR_INVALID_ARG, "paged output: not enough pages for the rank's rows");
+    for (int32_t i = 0; i < paged->num_pages; ++i)
+      if (paged->page_ids[i] < 0 || paged->page_ids[i] >= paged->pool_pages ||
+          static_cast<int64_t>(paged->page_ids[i] + 1) * paged->page_rows > UINT32_MAX)
+        return fail(FC_ERR_INVALID_ARG, "paged output: page id outside the pool");
+  }
   jobs[0].surfaces = surfaces;
   jobs[0].tokens = tokens;
-  return launch_jobs(P, jobs, stream, dbg_src, dbg_rs);
+  return launch_jobs(P, jobs, stream, dbg_src, dbg_rs, paged);
 }
 
 }  // namespace fc
@@ -554,6 +586,12 @@ extern "C" {
 fc_status fc_preprocess(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
                         int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream) {
   return preprocess_impl(plan, rank, surfaces, num_surfaces, tokens, grid_thw, stream, nullptr, nullptr);
+}
+
+fc_status fc_preprocess_paged(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
+                              int64_t num_surfaces, const fc_paged_tokens* out, int64_t grid_thw[3], void* stream) {
+  if (!out) return fail(FC_ERR_INVALID_ARG, "paged descriptor is NULL");
+  return preprocess_impl(plan, rank, surfaces, num_surfaces, nullptr, grid_thw, stream, nullptr, nullptr, out);
 }
 
 fc_status fc_preprocess_debug(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,

@@ -383,3 +383,82 @@ def test_u8_codes_full_c2(fc, oracle, cuda):
     for t in _sample_pairs(plan.grid_thw[0]):
         ref = oracle.preprocess([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2)
         np.testing.assert_array_equal(tok[t * rpp:(t + 1) * rpp].cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+# ------------------------------------------------------ NEXT-2 paged output
+def _paged_request(fc, W, H, N, gops, seed, token_dtype, **cfg):
+    plan = fc.Plan(fc.VideoMeta(W, H, N, (30, 1), gops), fc.ModelCfg(token_dtype=token_dtype, **cfg))
+    host = {i: synth.frame_nv12(W, H, i, "natural", seed) for i in plan.sampled_indices}
+    dev = synth.to_device(host)
+    return plan, fc.SurfaceTable.from_tensors(dev, N), host, dev
+
+
+def _pool_rows(pool, page_ids, first, n, page_rows):
+    """Linear-buffer view of a write chunk: row i -> page_ids[s // R], row s % R."""
+    import torch
+    idx = [page_ids[(first + i) // page_rows] * page_rows + (first + i) % page_rows for i in range(n)]
+    return pool.view(-1, 1176)[torch.tensor(idx, device=pool.device)]
+
+
+@pytest.mark.parametrize("token_dtype", ["f32", "bf16"])
+def test_paged_two_requests_interleaved_pages(fc, oracle, cuda, token_dtype):
+    """NEXT-2 (Fig. 10): two requests write into one pool through
+    interleaved, non-contiguous page lists, starting mid-page
+    (pv_cu_page_len mod page_rows != 0).  Each request reads back exactly its
+    single-GPU tokens (differential test vs a linear buffer, SPEC embed_buffer);
+    every other pool row keeps its sentinel."""
+    import torch
+    import random
+    R = 64
+    tdt = torch.float32 if token_dtype == "f32" else torch.bfloat16
+    a = _paged_request(fc, 320, 240, 60, [0, 30], 41, token_dtype, sampling="explicit", explicit_indices=[0, 7, 31, 44])
+    b = _paged_request(fc, 200, 120, 40, [0], 42, token_dtype, sampling="explicit", explicit_indices=[1, 2, 3])
+    first_a, first_b = 5, 60
+    need_a = -(-(first_a + a[0].token_rows) // R)
+    need_b = -(-(first_b + b[0].token_rows) // R)
+    P = need_a + need_b + 4
+    perm = list(range(P))
+    random.Random(10).shuffle(perm)  # interleaved, non-contiguous page lists
+    ids_a, ids_b = perm[0::2][:need_a], perm[1::2][:need_b]
+    assert len(ids_a) == need_a and len(ids_b) == need_b and not set(ids_a) & set(ids_b)
+    pool = torch.full((P, R, 1176), -7.0, dtype=tdt, device="cuda")
+    fc.preprocess_paged(a[0], 0, a[1], pool, ids_a, first_a)
+    fc.preprocess_paged(b[0], 0, b[1], pool, ids_b, first_b)
+    torch.cuda.synchronize()
+    written = torch.zeros(P * R, dtype=torch.bool)
+    for (plan, _, host, _), ids, first in ((a, ids_a, first_a), (b, ids_b, first_b)):
+        W, H = plan.meta.width, plan.meta.height
+        h2, w2 = plan.resized
+        ref = oracle.preprocess([host[i] for i in plan.sampled_indices], W, H, w2, h2)
+        got = _pool_rows(pool, ids, first, plan.token_rows, R)
+        if token_dtype == "f32":
+            np.testing.assert_array_equal(got.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+        else:
+            np.testing.assert_array_equal(got.view(torch.int16).cpu().numpy().view(np.uint16), oracle.to_bf16(ref))
+        for i in range(plan.token_rows):
+            written[ids[(first + i) // R] * R + (first + i) % R] = True
+    rest = pool.view(-1, 1176)[~written.to(pool.device)]
+    assert bool((rest == -7.0).all())
+
+
+def test_paged_full_c2_matches_linear(fc, cuda):
+    """Config 2 through the paged epilogue (page_rows 128, shuffled pages) ==
+    the linear fc_preprocess output, bit for bit."""
+    import random
+    import torch
+    wl = synth.CONFIGS["c2"]
+    plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
+                   fc.ModelCfg(sample_fps=wl.sample_fps))
+    surf = fc.SurfaceTable.from_tensors(synth.to_device(synth.frames_nv12(wl, plan.sampled_indices, "natural")),
+                                        wl.num_frames)
+    lin = fc.preprocess(plan, 0, surf)
+    R = 128
+    npages = -(-(plan.token_rows + 37) // R)
+    ids = list(range(npages + 5))
+    random.Random(7).shuffle(ids)
+    ids = ids[:npages]
+    pool = torch.zeros((npages + 5, R, 1176), dtype=torch.float32, device="cuda")
+    fc.preprocess_paged(plan, 0, surf, pool, ids, 37)
+    torch.cuda.synchronize()
+    got = _pool_rows(pool, ids, 37, plan.token_rows, R)
+    assert torch.equal(got.view(torch.int32), lin.view(torch.int32))

@@ -219,3 +219,29 @@ def test_model_cfg_struct_matches_abi(fc):
     fc.lib().fc_model_cfg_default(ctypes.byref(c))
     assert (c.token_dtype, c.color, c.world_size, c.encoder_rank) == (0, 0, 1, 0)
     assert abs(c.rescale_factor - 1 / 255) < 1e-15 and c.patch_size == 14
+
+
+@pytest.mark.parametrize("kw,ok", [
+    (dict(page_rows=48), False),                      # not a power of two
+    (dict(first_offset=64), False),                   # outside [0, page_rows)
+    (dict(page_ids=[0]), False),                      # one page cannot hold first_offset + rows
+    (dict(page_ids=[0, 9]), False),                   # page id outside the 8-page pool
+    (dict(page_ids=[], first_offset=0), False),
+])
+def test_paged_output_validation(fc, kw, ok):
+    """NEXT-2 write_chunk preconditions (SPEC CapacityError / bad page ids) are
+    rejected before any device work: FC_ERR_INVALID_ARG, nothing launched."""
+    p = plan_of(fc, 64, 48, 100, [0, 50], sampling="explicit", explicit_indices=[0, 10, 20, 30])
+    rows = p.token_rows
+    buf = (ctypes.c_uint8 * (48 * 64 * 2 + 64))()
+    base = (ctypes.addressof(buf) + 15) & ~15
+    surf = fc.SurfaceTable(100)
+    for i in (0, 10, 20, 30):
+        surf.arr[i] = fc._native.Nv12SurfaceC(base, base + 48 * 64, 64, 64)
+    args = dict(page_rows=64, page_ids=[3], first_offset=60)
+    args.update(kw)
+    ids = (ctypes.c_int32 * max(1, len(args["page_ids"])))(*args["page_ids"])
+    d = fc._native.PagedTokensC(ctypes.c_void_p(base), 8, args["page_rows"], len(args["page_ids"]),
+                                ctypes.cast(ids, ctypes.POINTER(ctypes.c_int32)), args["first_offset"])
+    st = fc.lib().fc_preprocess_paged(p.handle, 0, surf.arr, 100, ctypes.byref(d), None, None)
+    assert rows > 4 and fc._native.STATUS[st] == "FC_ERR_INVALID_ARG"
