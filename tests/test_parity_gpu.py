@@ -462,3 +462,45 @@ def test_paged_full_c2_matches_linear(fc, cuda):
     torch.cuda.synchronize()
     got = _pool_rows(pool, ids, 37, plan.token_rows, R)
     assert torch.equal(got.view(torch.int32), lin.view(torch.int32))
+
+
+# ------------------------------------------------------ more edge cases
+def test_8k_input_wide_windows(fc, oracle, cuda):
+    """7680x4320 -> smart_resize: ~5.9x downscale, 24+-tap windows, strips whose
+    source span needs two TMA boxes per row (NX = 2); one pair vs the oracle."""
+    plan, exact, size = run_case(fc, oracle, cuda, 7680, 4320, 8, [0], "natural", seed=77, check_rgb=False,
+                                 sampling="explicit", explicit_indices=[2, 5])
+    assert plan.max_taps[0] >= 20 and exact == size
+
+
+def test_cuda_graph_capture_replay(fc, oracle, cuda):
+    """fc_preprocess (tensor maps in the kernel parameters, <= 120 frames) is
+    stream-capturable: a captured graph replays to the same tokens, and
+    replays after the NV12 surfaces change pick up the new content."""
+    import torch
+    W, H, N = 320, 240, 120
+    plan = make_plan(fc, W, H, N, [0], sample_fps=2.0)
+    idx = plan.sampled_indices
+    dev = synth.to_device({i: synth.frame_nv12(W, H, i, "natural", 3) for i in idx})
+    surf = fc.SurfaceTable.from_tensors(dev, N)
+    out = torch.empty((plan.token_rows, 1176), dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    fc.preprocess(plan, 0, surf, out, stream=s)  # warm-up outside capture (tables, maps)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        fc.preprocess(plan, 0, surf, out, stream=s)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    h2, w2 = plan.resized
+    host2 = {i: synth.frame_nv12(W, H, i, "uniform", 4) for i in idx}
+    ref1 = oracle.preprocess([synth.frame_nv12(W, H, i, "natural", 3) for i in idx], W, H, w2, h2)
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), ref1.view(np.uint32))
+    for i in idx:  # new content in the same surfaces
+        dev[i][0].copy_(torch.from_numpy(host2[i][0]))
+        dev[i][1].copy_(torch.from_numpy(host2[i][1]))
+    g.replay()
+    torch.cuda.synchronize()
+    ref2 = oracle.preprocess([host2[i] for i in idx], W, H, w2, h2)
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), ref2.view(np.uint32))
