@@ -41,7 +41,7 @@ constexpr int kThreads = kComputeThreads;  // thread 0 also issues the TMA copie
 constexpr int kMaxInlineFrames = 120;      // tensor maps (2 per frame) passed by value up to this many frames
 constexpr int kRingStride = 6 * kStrip + 24;  // ring row stride (words): == 8 mod 32, conflict-free A loads
 static_assert(kRingStride % 32 == 8, "ring stride must be 8 mod 32");
-constexpr int kStages = 4;                 // raw NV12 chunk buffers (TMA runs kStages-1 chunks ahead)
+constexpr int kMaxStages = 4;              // raw NV12 chunk buffers: p.nstages in {2, 4} (host-chosen)
 constexpr int kIssueWarp = kComputeWarps - 1;  // owns no H-pass tile (7 tiles of 8 cover a 56-column strip)
 static_assert((kStrip + kTileN - 1) / kTileN < kComputeWarps, "the TMA issuing warp must own no H tile");
 
@@ -73,6 +73,7 @@ struct Params {
   uint32_t trw_magic;  // ceil(2^32 / TRW): x mod TRW = x - TRW * umulhi(x, magic) for the row words used
   int nframes;
   int ppj;            // pairs per job (batch launches; == npairs for one job)
+  int nstages, stage_shift;  // raw TMA stages (2 or 4; the host trades pipeline depth for CTAs/SM) and log2
   // NEXT-2 paged output (PAGED instances): token row i of this launch goes to
   // pool row page_ids[(page_first + i) >> page_shift] * page_rows + ((page_first + i) & page_mask)
   const int32_t* page_ids;  // device (launch descriptor)
@@ -139,11 +140,13 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
 
   extern __shared__ __align__(1024) uint8_t smem[];
   uint32_t* lut = reinterpret_cast<uint32_t*>(smem);              // 3 x 256 token bits at offset 0
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 3072);      // kStages full barriers
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 3072);      // nstages full barriers
   const int RAWF = 24 * p.BW * p.NX;                              // raw bytes per frame per stage
-  uint8_t* raw = smem + 3072 + 128;                               // [kStages][2 f][Y boxes | UV boxes]
+  uint8_t* raw = smem + 3072 + 128;                               // [nstages][2 f][Y boxes | UV boxes]
+  const int NS = p.nstages;
+  const uint32_t smask = static_cast<uint32_t>(NS - 1);
   const int SWP = p.SWP;
-  uint8_t* rgb = raw + kStages * 2 * RAWF;                        // [2 f][3 c][16 rows][SWP]
+  uint8_t* rgb = raw + NS * 2 * RAWF;                             // [2 f][3 c][16 rows][SWP]
   uint32_t* ring = reinterpret_cast<uint32_t*>(rgb + 6 * CH * SWP);  // [TRW][RS] words: [w][f][c][x]
 
   const int tid = threadIdx.x;
@@ -152,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
   const bool issuer = tid == kIssueWarp * 32;  // lane 0 of the warp without an H tile issues the TMA copies
 
   if (tid == 0) {
-    for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+    for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
   for (int i = tid; i < 768; i += kThreads) lut[i] = __ldg(p.lut + i);
@@ -225,19 +228,19 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
     // ring words of source rows kfirst*16 + g and + g + 8 (advanced per chunk)
     int hwA = ((r.kfirst * CH) / 4 + (g >> 2)) % p.TRW;
     int hwB = ((r.kfirst * CH) / 4 + 2 + (g >> 2)) % p.TRW;
-    // prefill: the run's first kStages chunks (every stage is free: the previous
+    // prefill: the run's first nstages chunks (every stage is free: the previous
     // run consumed all it issued, before the barrier that ended its last band)
     if (issuer)
-      for (int j = 0; j < kStages && r.kfirst + j < r.klast; ++j)
-        issue_chunk(p, r.pair, SX0, r.kfirst + j, raw + ((seq + j) % kStages) * 2 * RAWF, &full[(seq + j) % kStages]);
+      for (int j = 0; j < NS && r.kfirst + j < r.klast; ++j)
+        issue_chunk(p, r.pair, SX0, r.kfirst + j, raw + ((seq + j) & smask) * 2 * RAWF, &full[(seq + j) & smask]);
     for (int hb_ = r.hb0; hb_ < r.hb1; ++hb_) {
       const int yo0 = hb_ * 28;
       const int kneed = min(p.nchunks, (__ldg(p.vx + yo0 + 27) + __ldg(p.vcnt + yo0 + 27) + CH - 1) / CH);
       for (; next_k < kneed; ++next_k, ++seq) {
         const int k = next_k;
-        const int buf = seq % kStages;
+        const int buf = seq & smask;
         const uint8_t* rawb = raw + buf * 2 * RAWF;
-        mbar_wait(&full[buf], (seq / kStages) & 1);
+        mbar_wait(&full[buf], (seq >> p.stage_shift) & 1);
         // ---- a5: NV12 -> RGB planes, 16 pixels per item
         auto convert = [&](int oy, int ouv, int orgb, int e) {
             const uint4 Yv = *reinterpret_cast<const uint4*>(rawb + oy);
@@ -281,9 +284,9 @@ __global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_cons
           }
         }
         bar_sync(1, kComputeThreads);              // RGB planes complete; raw stage free
-        // refill the stage just converted with chunk k + kStages; the issuing
+        // refill the stage just converted with chunk k + nstages; the issuing
         // warp owns no H tile, so this runs beside the H pass, off the critical path
-        if (issuer && k + kStages < r.klast) issue_chunk(p, r.pair, SX0, k + kStages, raw + buf * 2 * RAWF, &full[buf]);
+        if (issuer && k + NS < r.klast) issue_chunk(p, r.pair, SX0, k + NS, raw + buf * 2 * RAWF, &full[buf]);
         // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of 3 for ILP
         if (hact) {
           const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + (g & 3);

@@ -214,11 +214,12 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
 struct Geometry {
   int sw, htiles, SWPN, SWP, BW, NX, TR, TRW, nstrips, nchunks;
   KernelFn fn, fn_dbg, fn_bf16, fn_u8, fn_paged, fn_paged_bf16;
-  size_t smem;
+  size_t smem;   // at nstages
+  int nstages;   // raw TMA stages: 4, or 2 when that buys another CTA per SM (wide-window configs)
 };
 
-static size_t smem_bytes(int SWP, int RAWW, int TRW) {
-  return 3072 + 128 + static_cast<size_t>(kStages) * 48 * RAWW + static_cast<size_t>(6) * kChunkRows * SWP +
+static size_t smem_bytes(int stages, int SWP, int RAWW, int TRW) {
+  return 3072 + 128 + static_cast<size_t>(stages) * 48 * RAWW + static_cast<size_t>(6) * kChunkRows * SWP +
          static_cast<size_t>(TRW) * kRingStride * 4;
 }
 
@@ -277,7 +278,12 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
   if (!g->fn) return fail(FC_ERR_UNSUPPORTED, "no kernel instance for this resize window");
   if (dt->ksh <= 2 && 2 * kChunkRows * (g->SWPN / 16) > 2 * kComputeThreads)
     return fail(FC_ERR_UNSUPPORTED, "colour stage: more than 2 items per thread");
-  g->smem = smem_bytes(g->SWP, g->BW * g->NX, g->TRW);
+  g->nstages = kMaxStages;
+  g->smem = smem_bytes(kMaxStages, g->SWP, g->BW * g->NX, g->TRW);
+  if (g->smem > static_cast<size_t>(max_smem)) {
+    g->nstages = 2;
+    g->smem = smem_bytes(2, g->SWP, g->BW * g->NX, g->TRW);
+  }
   if (g->smem > static_cast<size_t>(max_smem))
     return fail(FC_ERR_UNSUPPORTED, "working set exceeds shared memory (resize window too wide)");
   return FC_OK;
@@ -447,6 +453,17 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, g.smem);
   if (e != cudaSuccess || occ < 1) return cuda_fail(e, "occupancy query");
+  if (g.nstages == kMaxStages && occ < 3) {
+    // a shallower TMA pipeline (2 stages) when it buys another CTA per SM:
+    // latency hiding across CTAs is worth more than 2 extra chunks in flight
+    const size_t smem2 = smem_bytes(2, g.SWP, g.BW * g.NX, g.TRW);
+    int occ2 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, fn, kThreads, smem2) == cudaSuccess && occ2 > occ) {
+      g.nstages = 2;
+      g.smem = smem2;
+      occ = occ2;
+    }
+  }
 
   static thread_local Params prm;  // ~31 KB: keep it off the stack
   std::memset(&prm, 0, offsetof(Params, tm));
@@ -480,6 +497,8 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   prm.dbg_src = dbg_src;
   prm.dbg_rs = dbg_rs;
   prm.trw_magic = static_cast<uint32_t>(((1ull << 32) + g.TRW - 1) / g.TRW);
+  prm.nstages = g.nstages;
+  prm.stage_shift = g.nstages == 4 ? 2 : 1;
   const int64_t nfj = static_cast<int64_t>(jobs[0].frames.size());
   const int64_t nf = nfj * static_cast<int64_t>(jobs.size());
   const long long items = (nf / 2) * static_cast<long long>(g.nstrips) * prm.gh2;
