@@ -453,7 +453,7 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   int occ = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, g.smem);
   if (e != cudaSuccess || occ < 1) return cuda_fail(e, "occupancy query");
-  if (g.nstages == kMaxStages && occ < 3) {
+  if (g.nstages == kMaxStages) {
     // a shallower TMA pipeline (2 stages) when it buys another CTA per SM:
     // latency hiding across CTAs is worth more than 2 extra chunks in flight
     const size_t smem2 = smem_bytes(2, g.SWP, g.BW * g.NX, g.TRW);
