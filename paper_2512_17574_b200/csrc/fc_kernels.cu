@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -554,6 +555,13 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
     if (paged) prm.page_ids = reinterpret_cast<const int32_t*>(static_cast<uint8_t*>(desc) + mbytes + tbytes);
   }
   const int grid = static_cast<int>(std::min<long long>(items, static_cast<long long>(occ) * nsm));
+  if (std::getenv("FC_VERBOSE")) {  // launch geometry, for experiments and profiles
+    std::fprintf(stderr,
+                 "fc launch: %dx%d->%dx%d KSH=%d KSV=%d sw=%d SWPN=%d SWP=%d BW=%d NX=%d TR=%d stages=%d smem=%zu "
+                 "CTAs/SM=%d grid=%d items=%lld\n",
+                 W, H, P->w2, P->h2, dt->ksh, dt->ksv, g.sw, g.SWPN, g.SWP, g.BW, g.NX, g.TR, g.nstages, g.smem, occ,
+                 grid, items);
+  }
   fn<<<grid, kThreads, g.smem, s>>>(prm);
   e = cudaGetLastError();
   if (desc) cudaFreeAsync(desc, s);
