@@ -133,7 +133,10 @@ __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, 
 // Strips are whole merge blocks, so every token row is written by one CTA in
 // one band (no partial-sector merging across CTAs in L2).
 template <int KSH, int KSV, bool DBG, int TOK, bool PAGED = false>
-__global__ void __launch_bounds__(kThreads, 3) fc_fused_kernel(const __grid_constant__ Params p) {
+// Narrow-window instances (KSH = KSV = 1: c2, c3, c5) fit 64 registers without
+// spills and run 4 CTAs/SM (with 2 TMA stages); wider windows keep 80 / 3.
+__global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
+    fc_fused_kernel(const __grid_constant__ Params p) {
   constexpr int SW = kStrip;
   constexpr int CH = kChunkRows;
   constexpr int RS = kRingStride;

@@ -13,3 +13,4 @@ for round in 1 2 3; do
     done
   done
 done
+true
