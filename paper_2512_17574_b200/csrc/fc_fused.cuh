@@ -399,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
           const int f = vsub, c = e;
           const uint32_t lutc = lut_s + c * 1024;
           TokT* tp = tb + (c * 2 + f) * 196;
-          constexpr int VG = KSV == 1 ? 2 : 1;  // patches interleaved per group
+          constexpr int VG = 1;  // patches per MMA group (interleaving 2 or 4 measured slower at 64 regs)
 #pragma unroll
           for (int q0 = 0; q0 < kStrip / 14; q0 += VG) {
             if (q0 >= npatch) break;
