@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(HERE, f"libfc_{os.environ['FC_LIB_VARIANT']}.so" if os.e
                         else "libfc.so")
 
 FC_TOKEN_COLS = 1176
+ABI_VERSION = 2  # include/fc.h FC_ABI_VERSION this binding marshals for
 STATUS = {0: "FC_OK", 1: "FC_ERR_INVALID_ARG", 2: "FC_ERR_EMPTY_SELECTION", 3: "FC_ERR_ASPECT_RATIO",
           4: "FC_ERR_UNSUPPORTED", 5: "FC_ERR_MISSING_SURFACE", 6: "FC_ERR_RANK", 7: "FC_ERR_OOM",
           8: "FC_ERR_CUDA", 9: "FC_ERR_NCCL"}

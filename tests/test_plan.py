@@ -29,7 +29,9 @@ def test_abi_exports_every_declared_symbol(fc):
     lib = ctypes.CDLL(fc._native.LIB_PATH)
     missing = [n for n in sorted(names) if not hasattr(lib, n)]
     assert not missing, missing
-    assert fc.lib().fc_abi_version() == 2
+    assert fc.lib().fc_abi_version() == fc._native.ABI_VERSION
+    m = re.search(r"#define FC_ABI_VERSION (\d+)", hdr)
+    assert m and int(m.group(1)) == fc._native.ABI_VERSION
 
 
 @pytest.mark.parametrize("name", sorted(synth.CONFIGS))
@@ -245,3 +247,13 @@ def test_paged_output_validation(fc, kw, ok):
                                 ctypes.cast(ids, ctypes.POINTER(ctypes.c_int32)), args["first_offset"])
     st = fc.lib().fc_preprocess_paged(p.handle, 0, surf.arr, 100, ctypes.byref(d), None, None)
     assert rows > 4 and fc._native.STATUS[st] == "FC_ERR_INVALID_ARG"
+
+
+def test_graft_entry_build_runs():
+    """The driver's build check: __graft_entry__.build() compiles (or finds
+    current) libfc.so + the oracle and checks the ABI version."""
+    import importlib
+    import sys
+    sys.path.insert(0, ROOT)
+    ge = importlib.import_module("__graft_entry__")
+    ge.build()
