@@ -45,11 +45,11 @@ def load_peaks():
         return 6650.0, "fallback"  # B200_PROFILING.md fallback
 
 
-def load_traffic(workload: str):
+def load_traffic(workload: str, key: str = "dram_bytes_per_launch"):
     try:
         with open(TRAFFIC_PATH) as f:
             d = json.load(f)
-        return d.get(workload, {}).get("dram_bytes_per_launch")
+        return d.get(workload, {}).get(key)
     except Exception:
         return None
 
@@ -240,6 +240,13 @@ def run_ours(args):
         if len(plans_keep) > 64:
             del plans_keep[:32]                   # older plans' work has long completed
 
+    # host planning cost (a1-a4), timed separately; inside the
+    # timed steps it overlaps the previous request's kernel
+    tp0 = time.perf_counter()
+    for _ in range(20):
+        fc.Plan(meta, cfg)
+    plan_us = (time.perf_counter() - tp0) / 20 * 1e6
+
     keep = []
     for _ in range(args.warmup):
         step(keep)
@@ -339,7 +346,19 @@ def run_ours(args):
             abytes = clips * max(algorithmic_bytes(plan0, wl, r, 1 if u8x else tok_bytes) for r in plan0.ranks())
             kern_for_roof = kern_max
         achieved = abytes / (kern_for_roof * 1e-3) / 1e9
-        traffic = load_traffic(args.config) if (world == 1 and args.tokens == "f32" and args.color == "bt601") else None
+        same_kernel = world == 1 and args.tokens == "f32" and args.color == "bt601"
+        traffic = load_traffic(args.config) if same_kernel else None
+        # second roofline: the kernel is bound by instruction issue;
+        # warp instructions per launch from the committed ncu capture of this config
+        winstr = load_traffic(args.config, "warp_instructions_per_launch") if same_kernel else None
+        issue = None
+        if winstr:
+            clk_mhz = clk.summary().get("sm_mhz") or 1965
+            peak_g = 148 * 4 * clk_mhz * 1e6 / 1e9  # warp instructions per second (G), 4 schedulers/SM
+            ach_g = winstr / (kern_for_roof * 1e-3) / 1e9
+            issue = {"bound": "issue", "achieved": round(ach_g, 1), "peak": round(peak_g, 1),
+                     "unit": "G warp-instr/s", "frac": round(ach_g / peak_g, 4),
+                     "warp_instructions_per_launch": int(winstr)}
         line = {
             "metric": METRIC, "value": round(n_all / (ms_per_step * 1e-3), 2), "unit": "frames/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
@@ -353,7 +372,8 @@ def run_ours(args):
                        "kernel_ms_avg": round(kern_max if world > 1 else kern_avg, 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_launch": abytes},
+                         "algorithmic_bytes_per_launch": abytes, **({"issue": issue} if issue else {})},
+            "plan_host_us": round(plan_us, 1),
             "gpu_launches": int(launches),  # fc_kernel_launches() delta over the timed region (this rank)
             "e2e": {"value": round(n_all / (e2e_ms * 1e-3), 2), "unit": "frames/s", "ms_per_step": round(e2e_ms, 3),
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 1176 * tok_bytes * clips},

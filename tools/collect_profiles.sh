@@ -29,6 +29,8 @@ for c in ("c2", "c4"):
     b = json.load(open(f"gpurun_out/{tag}/bench_{c}.json"))
     rd, wr = get("dram__bytes_read.sum"), get("dram__bytes_write.sum")
     out[c] = {"dram_bytes_read": rd, "dram_bytes_write": wr, "dram_bytes_per_launch": rd + wr,
+              "warp_instructions_per_launch": get("smsp__inst_executed.sum"),
+              "issue_active_pct": get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
               "algorithmic_bytes_per_launch": b["roofline"]["algorithmic_bytes_per_launch"],
               "kernel_us_under_ncu": get("gpu__time_duration.sum") / (1e3 if u[h.index("gpu__time_duration.sum")] == "nsecond" else 1),
               "source": f"profiles/{tag}_ncu_full_{c}_summary.txt (ncu --set full --clock-control none, 1 launch)"}
