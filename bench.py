@@ -29,6 +29,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
+
 import synth  # noqa: E402
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -202,7 +204,19 @@ def run_ours(args):
     # this rank's frames (global indices) -- only those are materialised
     my_frames = plan0.sampled_indices[rp["sampled_begin"]:rp["sampled_begin"] + rp["sampled_count"]]
     hosts = [synth.frames_nv12(wl, my_frames, "natural", clip=c) for c in range(clips)]
-    devs = [synth.to_device(h) for h in hosts]
+
+    def stack_device(h):
+        """One contiguous device Y stack and UV stack per request (frames in
+        index order); surfaces point into them."""
+        fr = sorted(h)
+        if not fr:
+            return {}, None
+        Y = torch.from_numpy(np.stack([h[f][0] for f in fr])).cuda()
+        UV = torch.from_numpy(np.stack([h[f][1] for f in fr])).cuda()
+        return {f: (Y[i], UV[i]) for i, f in enumerate(fr)}, (Y, UV)
+
+    stacks = [stack_device(h) for h in hosts]
+    devs = [d for d, _ in stacks]
     surfs = [fc.SurfaceTable.from_tensors(d, wl.num_frames) for d in devs]
     rows = rp["row_end"] - rp["row_begin"]
     tdt = torch.bfloat16 if args.tokens == "bf16" else torch.float32
@@ -296,25 +310,51 @@ def run_ours(args):
                   "GB/s": round(gbytes / (gms.item() * 1e-3) / 1e9, 1), "nvlink_nominal_GB/s": 900,
                   "nvlink_measured_peer_GB/s": 770}
 
-    # e2e: same step from pinned host buffers through the public API
-    pinned = [{k: (torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()) for k, (a, b) in h.items()}
-              for h in hosts]
-    res_host = torch.empty((clips, 1176), dtype=tdt).pin_memory()
-    h2d = sum(a.numel() + b.numel() for pc in pinned for a, b in pc.values())
-    e2e_steps = max(3, min(args.steps, 10))
+    # e2e: the same step from pinned host NV12 through the public API.  Each
+    # step uploads its request's frames (visible bytes only: 2-D copies of W
+    # bytes per row) on a copy stream into one of two device surface sets, so
+    # request k+1 uploads while request k computes; the result's first token
+    # row per request comes back to the host.  Timed from the first upload to
+    # the last read-back.
+    from cuda.bindings import runtime as cudart
 
-    def e2e_step(keep):
-        for pc, dv in zip(pinned, devs):
-            for k, (y, uv) in pc.items():
-                dv[k][0].copy_(y, non_blocking=True)
-                dv[k][1].copy_(uv, non_blocking=True)
+    pinned = [(torch.from_numpy(np.stack([h[f][0] for f in sorted(h)])).pin_memory(),
+               torch.from_numpy(np.stack([h[f][1] for f in sorted(h)])).pin_memory()) if h else None for h in hosts]
+    stacks2 = [stack_device(h) for h in hosts]
+    surfs2 = [fc.SurfaceTable.from_tensors(d, wl.num_frames) for d, _ in stacks2]
+    sets = [([st for _, st in stacks], surfs), ([st for _, st in stacks2], surfs2)]
+    res_host = torch.empty((clips, 1176), dtype=tdt).pin_memory()
+    W, H = wl.width, wl.height
+    h2d = sum(len(h) * (W * H + W * (H // 2)) for h in hosts)
+    e2e_steps = max(3, min(args.steps, 10))
+    cstream = torch.cuda.Stream()
+    up_done = [torch.cuda.Event(), torch.cuda.Event()]
+    used = [torch.cuda.Event(), torch.cuda.Event()]
+    H2D = cudart.cudaMemcpyKind.cudaMemcpyHostToDevice
+
+    def upload(k):
+        dv_set = sets[k & 1][0]
+        cstream.wait_event(used[k & 1])  # the compute of request k-2 released this set
+        for pc, st in zip(pinned, dv_set):
+            if pc is None:
+                continue
+            for src, dst in zip(pc, st):  # Y stack, UV stack: one 2-D copy each (W bytes per row)
+                err, = cudart.cudaMemcpy2DAsync(dst.data_ptr(), dst.stride(1), src.data_ptr(), src.stride(1), W,
+                                                src.shape[0] * src.shape[1], H2D, cstream.cuda_stream)
+                assert err == cudart.cudaError_t.cudaSuccess, err
+        up_done[k & 1].record(cstream)
+
+    def e2e_step(k, keep):
+        sf_set = sets[k & 1][1]
         plans = [fc.Plan(meta, cfg) for _ in range(clips)]
         keep.append(plans)
+        stream.wait_event(up_done[k & 1])
         if rows:
             if clips == 1:
-                fc.preprocess(plans[0], rank, surfs[0], outs[0])
+                fc.preprocess(plans[0], rank, sf_set[0], outs[0])
             else:
-                fc.preprocess_batch([(pl, rank, sf) for pl, sf in zip(plans, surfs)], outs)
+                fc.preprocess_batch([(pl, rank, sf) for pl, sf in zip(plans, sf_set)], outs)
+        used[k & 1].record(stream)
         if world > 1:
             exchange(plans)
         if world == 1 or rank == enc:  # one token row of every request's result back to the host
@@ -322,14 +362,20 @@ def run_ours(args):
                 src = (toks[c] if u8x else fulls[c]) if world > 1 else outs[c]
                 res_host[c].copy_(src[0], non_blocking=True)
 
-    e2e_step(keep)
+    for k in range(2):  # warm-up of both surface sets
+        upload(k)
+        e2e_step(k, keep)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(e2e_steps):
-        e2e_step(keep)
+    cstream.wait_event(e0)
+    upload(0)
+    for k in range(e2e_steps):
+        if k + 1 < e2e_steps:
+            upload(k + 1)  # overlaps request k's compute
+        e2e_step(k, keep)
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = torch.tensor([e0.elapsed_time(e1) / e2e_steps], dtype=torch.float64, device="cuda")
