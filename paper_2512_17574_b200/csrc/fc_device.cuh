@@ -207,12 +207,26 @@ __device__ __forceinline__ int combine_planes(int d2, int d1, int d0) {
   return static_cast<int>((t << 8) + static_cast<uint32_t>(d0));
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned s;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(s));
+  return s;
+}
 __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void sts8(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(static_cast<unsigned short>(v)) : "memory");
 }
 
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
@@ -249,6 +263,18 @@ __device__ __forceinline__ void st_cs_pred(uint8_t* p, uint32_t v, bool pred) {
                : "memory");
 }
 
+// predicated streaming store of two adjacent tokens (a at p, b at p + 1)
+__device__ __forceinline__ void st_cs_pred2(float* p, uint32_t a, uint32_t b, bool pred) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t@q st.global.cs.v2.b32 [%0], {%1, %2};\n}" ::"l"(p),
+               "r"(a), "r"(b), "r"(static_cast<int>(pred))
+               : "memory");
+}
+__device__ __forceinline__ void st_cs_pred2(uint16_t* p, uint32_t a, uint32_t b, bool pred) {
+  st_cs_pred(reinterpret_cast<float*>(p), __byte_perm(a, b, 0x5410), pred);  // bf16 bits in the low halves
+}
+__device__ __forceinline__ void st_cs_pred2(uint8_t* p, uint32_t a, uint32_t b, bool pred) {
+  st_cs_pred(reinterpret_cast<uint16_t*>(p), __byte_perm(a, b, 0x0040), pred);  // u8 codes in the low bytes
+}
 __device__ __forceinline__ void st_cs_f2(float* p, float a, float b) {
   asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }

@@ -50,7 +50,7 @@ struct Params {
   int gh2, gw2;       // merge blocks per column / row
   int nstrips, npairs;
   int sw, htiles;      // strip width (84 or 28 output columns), H tiles per strip
-  int SWP;            // RGB-plane row stride (odd multiple of 16)
+  int SWP;            // RGB-plane row stride (8 mod 16)
   int SWPN;           // converted (and TMA-loaded) bytes per row: taps of the strip's outputs
   int BW, NX;         // TMA box width (<= 256) and boxes per row: NX*BW >= SWPN
   int bwshift, bwmask;  // box index / offset of a byte column (NX == 1: 31 / ~0; else BW = 256: 8 / 255)
@@ -81,6 +81,8 @@ struct Params {
   uint32_t page_shift, page_mask, page_rows;
   void* const* tokj;  // device: per-job token base (batch launches) or null -> tokens
   const CUtensorMap* tmg;  // device copy of the maps (launches past kMaxInlineFrames frames) or null -> tm
+  unsigned long long* cta_t;
+  int smap;           // 1: strip-synchronous work mapping (grid = a multiple of nstrips)  // FC_CTA_TIMES experiments: per CTA {start, end, smid} (ns) or null
   CUtensorMap tm[2 * kMaxInlineFrames];  // per frame: Y plane (box BW x 16), UV plane (box BW x 8)
 };
 
@@ -90,12 +92,17 @@ struct Run {
   int pair, strip, hb0, hb1, kfirst, klast;
 };
 
-__device__ __forceinline__ bool next_run(const Params& p, int& cur, int i1, Run& r) {
+__device__ __forceinline__ bool next_run(const Params& p, int& cur, int i1, int sfix, Run& r) {
   if (cur >= i1) return false;
   const int ps = cur / p.gh2;
   r.hb0 = cur - ps * p.gh2;
-  r.pair = ps / p.nstrips;
-  r.strip = ps - r.pair * p.nstrips;
+  if (sfix >= 0) {  // strip-synchronous mapping: cur walks (pair, band) of strip sfix
+    r.pair = ps;
+    r.strip = sfix;
+  } else {
+    r.pair = ps / p.nstrips;
+    r.strip = ps - r.pair * p.nstrips;
+  }
   r.hb1 = min(p.gh2, r.hb0 + (i1 - cur));
   cur += r.hb1 - r.hb0;
   r.kfirst = (__ldg(p.vx + 28 * r.hb0) & ~3) / kChunkRows;
@@ -158,6 +165,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
   const bool issuer = tid == kIssueWarp * 32;  // lane 0 of the warp without an H tile issues the TMA copies
 
   if (tid == 0) {
+    if (p.cta_t != nullptr) p.cta_t[3 * blockIdx.x] = globaltimer();
     for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
@@ -169,8 +177,23 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
   __syncthreads();
 
   const int total = p.npairs * p.nstrips * p.gh2;
-  const int i0 = static_cast<int>((static_cast<long long>(blockIdx.x) * total) / gridDim.x);
-  const int i1 = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * total) / gridDim.x);
+  int i0 = static_cast<int>((static_cast<long long>(blockIdx.x) * total) / gridDim.x);
+  int i1 = static_cast<int>((static_cast<long long>(blockIdx.x + 1) * total) / gridDim.x);
+  // strip-synchronous mapping: CTA b owns strip b % nstrips over the (pair,
+  // band) range of group b / nstrips, so the nstrips CTAs of a group walk
+  // side by side down the same frames and share their strip halos in L2
+  int sfix = -1;
+  // (grid = G: the first r strips get Qhi = ceil(G / nstrips) groups, the
+  // others Qhi - 1, so only the r / nstrips boundary drifts)
+  if (KSH == 1 && KSV == 1 && p.smap) {  // narrow windows only (the host rule), keeps wide instances lean
+    const int ns = p.nstrips, q = blockIdx.x / ns;
+    sfix = blockIdx.x - q * ns;
+    const int qhi = (gridDim.x + ns - 1) / ns, rr = gridDim.x - (qhi - 1) * ns;
+    const int Q = sfix < rr ? qhi : qhi - 1;
+    const long long PB = static_cast<long long>(p.npairs) * p.gh2;
+    i0 = static_cast<int>(q * PB / Q);
+    i1 = static_cast<int>((q + 1) * PB / Q);
+  }
 
   // ------------------------------------------------------------ compute warps
   // colour items (frame, row, 16-pixel group): at most 2 per thread; their
@@ -194,15 +217,17 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
   const int vjg = warp & 3, vsub = warp >> 2;
   const int j0 = 8 * vjg + 2 * tq;                 // output rows j0, j0+1 of the band
   const bool jok0 = j0 < 28, jok1 = j0 + 1 < 28;   // group 3 covers rows 24..31
-  const bool xok1 = g < 6;                         // second column g+8 inside the 14-wide patch
+  // V-pass MMA rows g / g+8 are patch columns 2g / 2g+1: one LDS.64 loads both
+  // A words (adjacent ring columns) and one 8-byte store writes both outputs
+  const bool xok = g < 7;                          // columns 2g, 2g+1 inside the 14-wide patch
   // token offset of (row j, patch column 0) within a band's token block (R6):
   // row part hm*2*1176 + ph*14
   const int jo0 = (j0 / 14) * 2 * kCols + (j0 % 14) * 14;
 
   uint32_t seq = 0;
-  int cur = i0;
   Run r;
-  while (next_run(p, cur, i1, r)) {
+  int cur = i0;
+  while (next_run(p, cur, i1, sfix, r)) {
     const int X0 = r.strip * p.sw;
     const int SX0 = __ldg(p.hx + X0) & ~15;
     const int npatch = min(p.sw / 14, (p.W2 - X0) / 14);  // valid patches in this strip
@@ -221,16 +246,18 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
         }
     }
     // A-fragment byte addresses in an RGB plane: rows g, g+8; columns xs + 4t (+16)
-    const uint32_t hA0 = rgb_s + g * SWP + (hact ? __ldg(p.hxs + htile) - SX0 : 0) + 4 * tq;
-    const uint32_t hA1 = hA0 + 8 * SWP;
+    // H-pass MMA rows g / g+8 are source rows 2g / 2g+1 of the chunk, so each
+    // thread's two rows of one output column are adjacent bytes of one ring word
+    // (SWP = 8 mod 16: rows 2g of the 8 lane groups fall in distinct bank quads)
+    const uint32_t hA0 = rgb_s + 2 * g * SWP + (hact ? __ldg(p.hxs + htile) - SX0 : 0) + 4 * tq;
+    const uint32_t hA1 = hA0 + SWP;
     // ring columns of this thread's outputs (2t, 2t+1 of the tile); masked past the strip / frame
     const int ho = warp * kTileN + 2 * tq;
     const bool hst0 = hact && ho < p.sw && X0 + ho < p.W2;
     const bool hst1 = hact && ho + 1 < p.sw && X0 + ho + 1 < p.W2;
     int next_k = r.kfirst;
     // ring words of source rows kfirst*16 + g and + g + 8 (advanced per chunk)
-    int hwA = ((r.kfirst * CH) / 4 + (g >> 2)) % p.TRW;
-    int hwB = ((r.kfirst * CH) / 4 + 2 + (g >> 2)) % p.TRW;
+    int hwA = ((r.kfirst * CH) / 4 + (g >> 1)) % p.TRW;
     // prefill: the run's first nstages chunks (every stage is free: the previous
     // run consumed all it issued, before the barrier that ended its last band)
     if (issuer)
@@ -253,10 +280,13 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
             yuv2rgb_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
             yuv2rgb_4(Yv.z, UVv.z, Rv.z, Gv.z, Bv.z, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
             yuv2rgb_4(Yv.w, UVv.w, Rv.w, Gv.w, Bv.w, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
-            uint8_t* dst = rgb + orgb;
-            *reinterpret_cast<uint4*>(dst) = Rv;
-            *reinterpret_cast<uint4*>(dst + CH * SWP) = Gv;
-            *reinterpret_cast<uint4*>(dst + 2 * CH * SWP) = Bv;
+            uint8_t* dst = rgb + orgb;  // 8-byte aligned rows (SWP = 8 mod 16)
+            reinterpret_cast<uint2*>(dst)[0] = make_uint2(Rv.x, Rv.y);
+            reinterpret_cast<uint2*>(dst)[1] = make_uint2(Rv.z, Rv.w);
+            reinterpret_cast<uint2*>(dst + CH * SWP)[0] = make_uint2(Gv.x, Gv.y);
+            reinterpret_cast<uint2*>(dst + CH * SWP)[1] = make_uint2(Gv.z, Gv.w);
+            reinterpret_cast<uint2*>(dst + 2 * CH * SWP)[0] = make_uint2(Bv.x, Bv.y);
+            reinterpret_cast<uint2*>(dst + 2 * CH * SWP)[1] = make_uint2(Bv.z, Bv.w);
             if (DBG && p.dbg_src != nullptr) {
               const int it = tid + e * kComputeThreads;
               const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
@@ -292,8 +322,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
         if (issuer && k + NS < r.klast) issue_chunk(p, r.pair, SX0, k + NS, raw + buf * 2 * RAWF, &full[buf]);
         // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of 3 for ILP
         if (hact) {
-          const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + (g & 3);
-          const uint32_t dB = ring_s + (hwB * RS + ho) * 4 + (g & 3);
+          const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + 2 * (g & 1);  // bytes of rows 2g, 2g+1
           constexpr int HG = KSH == 1 ? 3 : 2;  // planes interleaved per group (ILP vs registers)
 #pragma unroll
           for (int fg = 0; fg < 6; fg += HG) {
@@ -313,29 +342,20 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
             for (int e = 0; e < HG; ++e) fir_mma_planes<KSH>(d2[e], d1[e], d0[e], a[e], hb);
 #pragma unroll
             for (int e = 0; e < HG; ++e) {
-              // clip8 (R4): d0,d1 = row g, columns ho, ho+1; d2,d3 = row g+8
+              // clip8 (R4) = sat_u8(S >> 22) (arithmetic shift; S < 2^31 by Pillow's
+              // headroom): d0,d1 = row 2g, columns ho, ho+1; d2,d3 = row 2g+1
               const uint32_t off = (fg + e) * SW * 4;
-              uint32_t q[4];
+              int v[4];
 #pragma unroll
-              for (int i = 0; i < 4; ++i)
-                q[i] = static_cast<uint32_t>(add_min_relu(combine_planes(d2[e][i], d1[e][i], d0[e][i]), 0,
-                                                          (1 << 30) - 1)) >> 22;
-              if (hst0) {
-                sts8(dA + off, q[0]);
-                sts8(dB + off, q[2]);
-              }
-              if (hst1) {
-                sts8(dA + off + 4, q[1]);
-                sts8(dB + off + 4, q[3]);
-              }
+              for (int i = 0; i < 4; ++i) v[i] = combine_planes(d2[e][i], d1[e][i], d0[e][i]) >> 22;
+              if (hst0) sts16(dA + off, pack_sat_u8(v[2], v[0], 0u));      // column ho: rows 2g, 2g+1
+              if (hst1) sts16(dA + off + 4, pack_sat_u8(v[3], v[1], 0u));  // column ho + 1
             }
           }
         }
-        // advance this thread's two ring rows by one chunk (4 words), wrapping
+        // advance this thread's ring row word by one chunk (4 words), wrapping
         hwA += 4;
         hwA -= hwA >= p.TRW ? p.TRW : 0;
-        hwB += 4;
-        hwB -= hwB >= p.TRW ? p.TRW : 0;
         bar_sync(1, kComputeThreads);  // ring rows complete, RGB planes free
       }
       // ---- a7 + a8 + a9: vertical pass (MMA), normalise, patchify
@@ -360,8 +380,8 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
           for (int kk = 0; kk < KSV; ++kk) {
             const int wa = w >= p.TRW ? w - p.TRW : w;
             const int wb4 = wa + 4 >= p.TRW ? wa + 4 - p.TRW : wa + 4;
-            rb[kk][0] = ring_s + (wa * RS + kPlanesPerWarp * vsub * SW + g) * 4;
-            rb[kk][1] = ring_s + (wb4 * RS + kPlanesPerWarp * vsub * SW + g) * 4;
+            rb[kk][0] = ring_s + (wa * RS + kPlanesPerWarp * vsub * SW + 2 * g) * 4;
+            rb[kk][1] = ring_s + (wb4 * RS + kPlanesPerWarp * vsub * SW + 2 * g) * 4;
             w = wa + 8;
           }
         }
@@ -378,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
         } else {
           tpair = static_cast<TokT*>(p.tokens) + static_cast<size_t>(r.pair) * pair_rows * kCols;
         }
-        TokT* tb = tpair + (static_cast<size_t>(hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + g;
+        TokT* tb = tpair + (static_cast<size_t>(hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + 2 * g;
         // paged output: the pool row of each patch's token row (merge block q/2,
         // sub-block q&1, this thread's half hm = j0/14) -- SPEC write_chunk mapping
         uint32_t prow[4];
@@ -409,10 +429,12 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
 #pragma unroll
               for (int kk = 0; kk < KSV; ++kk) {
                 const uint32_t co = (e * SW + 14 * (q0 + e2)) * 4;
-                a[e2][kk][0] = lds32(rb[kk][0] + co);
-                a[e2][kk][1] = lds32(rb[kk][0] + co + 32);
-                a[e2][kk][2] = lds32(rb[kk][1] + co);
-                a[e2][kk][3] = lds32(rb[kk][1] + co + 32);
+                const uint2 lo = lds64(rb[kk][0] + co);  // columns 2g, 2g+1; rows k 4t..4t+3
+                const uint2 hi = lds64(rb[kk][1] + co);  // k + 16
+                a[e2][kk][0] = lo.x;
+                a[e2][kk][1] = lo.y;
+                a[e2][kk][2] = hi.x;
+                a[e2][kk][3] = hi.y;
               }
             int d2[VG][4], d1[VG][4], d0[VG][4];
 #pragma unroll
@@ -421,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
             for (int e2 = 0; e2 < VG; ++e2) {
               const int q = q0 + e2;
               if (q >= npatch) break;
-              // d0,d1: column g, rows j0, j0+1; d2,d3: column g+8
+              // d0,d1: column 2g, rows j0, j0+1; d2,d3: column 2g+1
               uint32_t sv[4];
               uint32_t o[4];
 #pragma unroll
@@ -434,17 +456,15 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
                   o[i] = lds32(lutc + ((sv[i] >> 20) & 0x3FCu));
               }
               TokT* op = PAGED ? static_cast<TokT*>(p.tokens) + static_cast<size_t>(prow[q]) * kCols + (c * 2 + f) * 196 +
-                                     (j0 % 14) * 14 + g
+                                     (j0 % 14) * 14 + 2 * g
                                : tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
-              st_cs_pred(op, o[0], jok0);
-              st_cs_pred(op + 14, o[1], jok1);
-              st_cs_pred(op + 8, o[2], jok0 && xok1);
-              st_cs_pred(op + 22, o[3], jok1 && xok1);
+              st_cs_pred2(op, o[0], o[2], jok0 && xok);       // row j0: columns 2g, 2g+1
+              st_cs_pred2(op + 14, o[1], o[3], jok1 && xok);  // row j0 + 1
               if (DBG && p.dbg_rs != nullptr) {
                 const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
                 for (int ee = 0; ee < 4; ++ee) {
-                  const int x = X0 + 14 * q + g + ((ee >= 2) ? 8 : 0), j = j0 + (ee & 1);
-                  if ((ee < 2 || xok1) && x < p.W2 && j < 28)
+                  const int x = X0 + 14 * q + 2 * g + ((ee >= 2) ? 1 : 0), j = j0 + (ee & 1);
+                  if (xok && x < p.W2 && j < 28)
                     p.dbg_rs[((fi * p.H2 + yo0 + j) * p.W2 + x) * 3 + c] = sv[ee] >> 22;
                 }
               }
@@ -454,6 +474,10 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
       }
       bar_sync(1, kComputeThreads);  // ring may be overwritten by the next chunks
     }
+  }
+  if (p.cta_t != nullptr && tid == 0) {
+    p.cta_t[3 * blockIdx.x + 1] = globaltimer();
+    p.cta_t[3 * blockIdx.x + 2] = smid();
   }
 }
 

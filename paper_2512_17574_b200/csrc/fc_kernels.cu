@@ -241,12 +241,13 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
       need = std::max(need, (th.xmin[X0 + 8 * i] & ~3) - SX0 + 32 * dt->ksh);
     for (int o = X0; o < X1; ++o) taps = std::max(taps, th.xmin[o] + th.cnt[o] - SX0);
   }
-  need = std::max(need, taps);
-  // round to an odd multiple of 16 (bank-conflict-free MMA A-fragment loads)
-  int swp = (need + 15) / 16;
-  if (!(swp & 1)) ++swp;
+  need = std::max(need, (taps + 15) / 16 * 16);  // the converted width (SWPN) fits every row
+  // round up to 8 mod 16: H-pass lanes g read rows 2g, 2g+1, and with a row
+  // stride of 4m+2 words the rows 2g of the 8 lane groups hit distinct bank quads
+  const int swp8 = (need + 7) / 8 * 8;
+  const int swpb = swp8 % 16 == 8 ? swp8 : swp8 + 8;
   g->SWPN = ((taps + 15) / 16) * 16;
-  g->SWP = swp * 16;
+  g->SWP = swpb;
   g->NX = (g->SWPN + 255) / 256;                       // TMA boxes are at most 256 wide
   g->BW = g->NX == 1 ? g->SWPN : 256;
   // ring depth: after the chunks a band needs (16-row granularity) the ring
@@ -554,16 +555,51 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
     if (jobs.size() > 1) prm.tokj = reinterpret_cast<void* const*>(static_cast<uint8_t*>(desc) + mbytes);
     if (paged) prm.page_ids = reinterpret_cast<const int32_t*>(static_cast<uint8_t*>(desc) + mbytes + tbytes);
   }
-  const int grid = static_cast<int>(std::min<long long>(items, static_cast<long long>(occ) * nsm));
-  if (std::getenv("FC_VERBOSE")) {  // launch geometry, for experiments and profiles
-    std::fprintf(stderr,
-                 "fc launch: %dx%d->%dx%d KSH=%d KSV=%d sw=%d SWPN=%d SWP=%d BW=%d NX=%d TR=%d stages=%d smem=%zu "
-                 "CTAs/SM=%d grid=%d items=%lld\n",
-                 W, H, P->w2, P->h2, dt->ksh, dt->ksv, g.sw, g.SWPN, g.SWP, g.BW, g.NX, g.TR, g.nstages, g.smem, occ,
-                 grid, items);
+  int grid = static_cast<int>(std::min<long long>(items, static_cast<long long>(occ) * nsm));
+  // strip-synchronous work mapping (see the kernel): DRAM reads of c2 drop from
+  // 669 MB to 404 MB (strip halos become L2 hits) and the kernel gets 0.5%
+  // faster; measured slower for wide windows (c4 +3%) and long single jobs (c3
+  // +2.5%), so only narrow-window requests of <= 128 pairs take it.
+  // FC_SMAP=0/1 forces it off/on (A/B runs).
+  const char* smenv = std::getenv("FC_SMAP");
+  const bool smap_default = dt->ksh == 1 && dt->ksv == 1 && jobs.size() == 1 && prm.npairs <= 128;
+  if ((smenv ? std::atoi(smenv) != 0 : smap_default) && grid >= g.nstrips) prm.smap = 1;
+  unsigned long long* cta_t = nullptr;
+  if (std::getenv("FC_CTA_TIMES") && cudaMalloc(&cta_t, 3 * sizeof(unsigned long long) * grid) == cudaSuccess) {
+    cudaMemsetAsync(cta_t, 0, 3 * sizeof(unsigned long long) * grid, s);
+    prm.cta_t = cta_t;
   }
   fn<<<grid, kThreads, g.smem, s>>>(prm);
   e = cudaGetLastError();
+  if (cta_t) {  // experiment: CTA lifetime distribution (start/end, ns from the first start)
+    prm.cta_t = nullptr;
+    std::vector<unsigned long long> t(3 * grid);
+    cudaMemcpyAsync(t.data(), cta_t, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    cudaFree(cta_t);
+    unsigned long long t0 = ~0ull, t1 = 0;
+    for (int b = 0; b < grid; ++b) t0 = std::min(t0, t[3 * b]), t1 = std::max(t1, t[3 * b + 1]);
+    std::vector<double> st(grid), en(grid);
+    double busy = 0;
+    for (int b = 0; b < grid; ++b) {
+      st[b] = (t[3 * b] - t0) * 1e-3, en[b] = (t[3 * b + 1] - t0) * 1e-3;
+      busy += en[b] - st[b];
+    }
+    std::vector<double> es = en, ss = st;
+    std::sort(es.begin(), es.end());
+    std::sort(ss.begin(), ss.end());
+    std::fprintf(stderr,
+                 "fc cta times (us): span %.1f | start max %.1f | end min %.1f p10 %.1f p50 %.1f p90 %.1f max %.1f | "
+                 "mean lifetime / span %.3f\n",
+                 (t1 - t0) * 1e-3, ss.back(), es.front(), es[grid / 10], es[grid / 2], es[grid * 9 / 10], es.back(),
+                 busy / grid / ((t1 - t0) * 1e-3));
+    if (const char* f = std::getenv("FC_CTA_TIMES_FILE")) {
+      if (FILE* fp = std::fopen(f, "a")) {
+        for (int b = 0; b < grid; ++b) std::fprintf(fp, "%d %llu %.2f %.2f\n", b, t[3 * b + 2], st[b], en[b]);
+        std::fclose(fp);
+      }
+    }
+  }
   if (desc) cudaFreeAsync(desc, s);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   launch_counter().fetch_add(1, std::memory_order_relaxed);
