@@ -283,6 +283,8 @@ def run_ours(args):
     total_ms = t0.elapsed_time(t1)
     kern_ms = [a.elapsed_time(b) for a, b in evs] if rows else [0.0]
     kern_avg = sum(kern_ms) / len(kern_ms)
+    if os.environ.get("FC_BENCH_STEPS"):  # diagnostics: per-step kernel times
+        print("kernel ms per step:", " ".join(f"{x:.3f}" for x in kern_ms), file=sys.stderr)
     # max over ranks
     stats = torch.tensor([total_ms, kern_avg], dtype=torch.float64, device="cuda")
     if world > 1:

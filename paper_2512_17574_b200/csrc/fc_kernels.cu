@@ -416,6 +416,29 @@ struct Job {
 // beyond that, or for several jobs, a descriptor [maps | per-job token bases]
 // is copied to a stream-ordered device allocation (cudaMallocAsync, freed
 // after the launch in stream order).
+// Library-owned stream-ordered pool for launch descriptors: the release
+// threshold keeps freed blocks in the pool across synchronisations, so a
+// steady stream of requests never goes back to the driver for memory (the
+// default pool returns memory at every sync).
+static cudaMemPool_t descriptor_pool(int dev) {
+  static std::mutex mu;
+  static std::map<int, cudaMemPool_t>* pools = new std::map<int, cudaMemPool_t>();
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = pools->find(dev);
+  if (it != pools->end()) return it->second;
+  cudaMemPoolProps props{};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.handleTypes = cudaMemHandleTypeNone;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool = nullptr;
+  if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+  uint64_t keep = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  (*pools)[dev] = pool;
+  return pool;
+}
+
 static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, uint8_t* dbg_src,
                              uint8_t* dbg_rs, const fc_paged_tokens* paged = nullptr) {
   int dev = 0;
@@ -543,7 +566,8 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
       for (size_t j = 0; j < jobs.size(); ++j)
         std::memcpy(host.data() + mbytes + j * sizeof(void*), &jobs[j].tokens, sizeof(void*));
     if (paged) std::memcpy(host.data() + mbytes + tbytes, paged->page_ids, pbytes);
-    e = cudaMallocAsync(&desc, bytes, s);
+    cudaMemPool_t pool = descriptor_pool(dev);
+    e = pool ? cudaMallocFromPoolAsync(&desc, bytes, pool, s) : cudaMallocAsync(&desc, bytes, s);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (launch descriptor)");
     // pageable source: returns once the bytes are staged, so `host` may die
     e = cudaMemcpyAsync(desc, host.data(), bytes, cudaMemcpyHostToDevice, s);
