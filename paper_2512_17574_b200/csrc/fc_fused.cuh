@@ -41,6 +41,13 @@ constexpr int kThreads = kComputeThreads;  // thread 0 also issues the TMA copie
 constexpr int kMaxInlineFrames = 120;      // tensor maps (2 per frame) passed by value up to this many frames
 constexpr int kRingStride = 6 * kStrip + 24;  // ring row stride (words): == 8 mod 32, conflict-free A loads
 static_assert(kRingStride % 32 == 8, "ring stride must be 8 mod 32");
+// normalisation table in shared memory: per channel, entries for v in
+// [-kLutLo, 256 + kLutLo), the entries outside [0, 255] repeating LUT[0] /
+// LUT[255] -- so the V pass indexes it with floor(S / 2^22) and clip8's clamp
+// disappears (the host checks every V output row's reachable range fits)
+constexpr int kLutLo = 48;
+constexpr int kLutN = 256 + 2 * kLutLo;                      // 352 entries per channel
+constexpr int kLutBytes = (3 * kLutN * 4 + 127) / 128 * 128;  // 4224: keeps the TMA stages 128-B aligned
 constexpr int kMaxStages = 4;              // raw NV12 chunk buffers: p.nstages in {2, 4} (host-chosen)
 constexpr int kIssueWarp = kComputeWarps - 1;  // owns no H-pass tile (7 tiles of 8 cover a 56-column strip)
 static_assert((kStrip + kTileN - 1) / kTileN < kComputeWarps, "the TMA issuing warp must own no H tile");
@@ -150,9 +157,9 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
 
   extern __shared__ __align__(1024) uint8_t smem[];
   uint32_t* lut = reinterpret_cast<uint32_t*>(smem);              // 3 x 256 token bits at offset 0
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 3072);      // nstages full barriers
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kLutBytes);  // nstages full barriers
   const int RAWF = 24 * p.BW * p.NX;                              // raw bytes per frame per stage
-  uint8_t* raw = smem + 3072 + 128;                               // [nstages][2 f][Y boxes | UV boxes]
+  uint8_t* raw = smem + kLutBytes + 128;                          // [nstages][2 f][Y boxes | UV boxes]
   const int NS = p.nstages;
   const uint32_t smask = static_cast<uint32_t>(NS - 1);
   const int SWP = p.SWP;
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
     for (int i = 0; i < NS; ++i) mbar_init(&full[i], 1);
     fence_mbar_init();
   }
-  for (int i = tid; i < 768; i += kThreads) lut[i] = __ldg(p.lut + i);
+  for (int i = tid; i < 3 * kLutN; i += kThreads) lut[i] = __ldg(p.lut + i);
   // bytes of the RGB planes past the converted width are only ever multiplied
   // by zero weights (MMA read-ahead); keep them zero, never garbage
   for (int i = tid; i < 6 * CH * SWP / 16; i += kThreads)
@@ -417,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
         for (int e = 0; e < kPlanesPerWarp; ++e) {
           // this warp's planes are frame f = vsub, channels c = e (plane index 3f + c)
           const int f = vsub, c = e;
-          const uint32_t lutc = lut_s + c * 1024;
+          const uint32_t lutc = lut_s + (c * kLutN + kLutLo) * 4;  // entry of v = 0
           TokT* tp = tb + (c * 2 + f) * 196;
           constexpr int VG = 1;  // patches per MMA group (interleaving 2 or 4 measured slower at 64 regs)
 #pragma unroll
@@ -444,16 +451,15 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
               const int q = q0 + e2;
               if (q >= npatch) break;
               // d0,d1: column 2g, rows j0, j0+1; d2,d3: column 2g+1
-              uint32_t sv[4];
+              int sv[4];
               uint32_t o[4];
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
-                sv[i] = static_cast<uint32_t>(
-                    add_min_relu(combine_planes(d2[e2][i], d1[e2][i], d0[e2][i]), 0, (1 << 30) - 1));
+                sv[i] = combine_planes(d2[e2][i], d1[e2][i], d0[e2][i]);  // S = 2^21 + sum T*iv (exact)
                 if constexpr (TOK == FC_TOKENS_U8)
-                  o[i] = sv[i] >> 22;  // the u8 code (NEXT-1 exchange format)
-                else
-                  o[i] = lds32(lutc + ((sv[i] >> 20) & 0x3FCu));
+                  o[i] = static_cast<uint32_t>(add_min_relu(sv[i], 0, (1 << 30) - 1)) >> 22;  // the u8 code (NEXT-1)
+                else  // LUT[clip8(S)] = extended table at floor(S / 2^22) (arithmetic shift)
+                  o[i] = lds32(lutc + (static_cast<uint32_t>(sv[i] >> 20) & ~3u));
               }
               TokT* op = PAGED ? static_cast<TokT*>(p.tokens) + static_cast<size_t>(prow[q]) * kCols + (c * 2 + f) * 196 +
                                      (j0 % 14) * 14 + 2 * g
@@ -465,7 +471,8 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
                 for (int ee = 0; ee < 4; ++ee) {
                   const int x = X0 + 14 * q + 2 * g + ((ee >= 2) ? 1 : 0), j = j0 + (ee & 1);
                   if (xok && x < p.W2 && j < 28)
-                    p.dbg_rs[((fi * p.H2 + yo0 + j) * p.W2 + x) * 3 + c] = sv[ee] >> 22;
+                    p.dbg_rs[((fi * p.H2 + yo0 + j) * p.W2 + x) * 3 + c] =
+                        static_cast<uint32_t>(add_min_relu(sv[ee], 0, (1 << 30) - 1)) >> 22;
                 }
               }
             }

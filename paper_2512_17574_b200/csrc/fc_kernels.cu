@@ -185,6 +185,23 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
     *out = &(P->dev[pkey] = git->second);
     return FC_OK;
   }
+  // every V output must land inside the extended table: floor(S / 2^22) with
+  // S = 2^21 + sum T*iv over u8 T lies in [vmin, vmax] below.  For Pillow's
+  // bicubic (a = -0.5) the negative lobes of the normalised filter sum to at
+  // most 1/8 (2x upscale phase), i.e. v in [-32, 287]; checked, not assumed
+  {
+    const AxisTable& tv = *P->tv;
+    for (int o = 0; o < tv.out; ++o) {
+      int64_t pos = 0, neg = 0;
+      for (int k = 0; k < tv.cnt[o]; ++k) {
+        const int64_t w = tv.iw[static_cast<size_t>(o) * tv.ksize + k];
+        (w > 0 ? pos : neg) += w;
+      }
+      const int64_t vmax = ((1 << 21) + 255 * pos) >> 22, vmin = ((1 << 21) + 255 * neg) >> 22;
+      if (vmin < -kLutLo || vmax >= 256 + kLutLo)
+        return fail(FC_ERR_UNSUPPORTED, "vertical resize weights reach outside the normalisation table");
+    }
+  }
   MmaTables m;
   build_mma_tables(P, sw, &m);
   if (m.ksh > kMaxKS || m.ksv > kMaxKS)
@@ -200,7 +217,13 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
   if (e == cudaSuccess) e = upload(&t.vcnt, P->tv->cnt);
   if (e == cudaSuccess) e = upload(&t.vys, m.vys);
   if (e == cudaSuccess) e = upload(&t.vfr, m.vfr);
-  if (e == cudaSuccess) e = upload(&t.lut, P->lut_dev);
+  // extended normalisation table (kernel: kLutLo entries below v = 0 and above
+  // v = 255 repeat the end values, so the V pass needs no clamp)
+  std::vector<uint32_t> lut_ext(3 * kLutN);
+  for (int c = 0; c < 3; ++c)
+    for (int i = 0; i < kLutN; ++i)
+      lut_ext[c * kLutN + i] = P->lut_dev[c * 256 + std::min(255, std::max(0, i - kLutLo))];
+  if (e == cudaSuccess) e = upload(&t.lut, lut_ext);
   if (e != cudaSuccess) {
     cudaFree(t.hx); cudaFree(t.hxs); cudaFree(t.hfr); cudaFree(t.vx); cudaFree(t.vcnt); cudaFree(t.vys);
     cudaFree(t.vfr); cudaFree(t.lut);
@@ -220,7 +243,7 @@ struct Geometry {
 };
 
 static size_t smem_bytes(int stages, int SWP, int RAWW, int TRW) {
-  return 3072 + 128 + static_cast<size_t>(stages) * 48 * RAWW + static_cast<size_t>(6) * kChunkRows * SWP +
+  return kLutBytes + 128 + static_cast<size_t>(stages) * 48 * RAWW + static_cast<size_t>(6) * kChunkRows * SWP +
          static_cast<size_t>(TRW) * kRingStride * 4;
 }
 
