@@ -187,8 +187,9 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
   }
   // every V output must land inside the extended table: floor(S / 2^22) with
   // S = 2^21 + sum T*iv over u8 T lies in [vmin, vmax] below.  For Pillow's
-  // bicubic (a = -0.5) the negative lobes of the normalised filter sum to at
-  // most 1/8 (2x upscale phase), i.e. v in [-32, 287]; checked, not assumed
+  // bicubic (a = -0.5) the negative lobes of the normalised filter sum to about
+  // 1/8 at most (2x upscale phase): v in [-34, 289] over tests/test_plan.py's
+  // sweep; checked here per plan, not assumed
   {
     const AxisTable& tv = *P->tv;
     for (int o = 0; o < tv.out; ++o) {

@@ -11,6 +11,8 @@ import os
 import random
 import re
 
+import numpy as np
+
 import pytest
 
 import synth
@@ -257,3 +259,31 @@ def test_graft_entry_build_runs():
     sys.path.insert(0, ROOT)
     ge = importlib.import_module("__graft_entry__")
     ge.build()
+
+
+def test_bicubic_output_range_fits_extended_table():
+    """The V pass indexes the normalisation table at floor(S / 2^22) without a
+    clamp (fc_fused.cuh kLutLo = 48: entries for v in [-48, 303]).  That needs
+    every reachable Pillow-bicubic output (R4: S = 2^21 + sum px*iw, px in
+    [0, 255]) inside the table.  Checked on the oracle's own coefficients over
+    up- and downscales (the product checks the same bound per plan at launch)."""
+    import random
+
+    from oracle import oracle
+
+    rng = random.Random(7)
+    pairs = [(1080, 560), (720, 560), (2160, 560), (480, 476), (240, 280), (1080, 224), (2160, 28),
+             (7, 28), (28, 56), (100, 201), (13, 1000)]
+    pairs += [(rng.randint(2, 4000), rng.randint(28, 2000)) for _ in range(200)]
+    lo, hi = 0, 255
+    for n_in, n_out in pairs:
+        _, cnt, iw = oracle.resize_coeffs(n_in, n_out)
+        pos = np.where(iw > 0, iw, 0).astype(np.int64).sum(axis=1)
+        neg = np.where(iw < 0, iw, 0).astype(np.int64).sum(axis=1)
+        lo = min(lo, int((((1 << 21) + 255 * neg) >> 22).min()))
+        hi = max(hi, int((((1 << 21) + 255 * pos) >> 22).max()))
+    assert -48 <= lo and hi <= 303, (lo, hi)
+    # the negative lobes of the a = -0.5 kernel integrate to 1/12 and, sampled
+    # at a 2x upscale's half-pixel phase, sum to 1/8 of the normalised weights:
+    # about [-32, 287]; integer rounding of small filters adds a little (M: [-34, 289])
+    assert lo >= -40 and hi <= 295, (lo, hi)
