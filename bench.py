@@ -196,7 +196,7 @@ def run_ours(args):
     # gather moves 1176-byte rows, the encoder expands them to tokens
     u8x = world > 1 and args.exchange == "u8"
     cfg = fc.ModelCfg(world_size=world, sample_fps=wl.sample_fps, token_dtype="u8" if u8x else args.tokens,
-                      color=args.color)
+                      color=args.color, surface_format=args.surface)
     tok_bytes = 2 if args.tokens == "bf16" else 4
     plan0 = fc.Plan(meta, cfg)
     rp = plan0.rank(rank)
@@ -204,16 +204,17 @@ def run_ours(args):
     # this rank's frames (global indices) -- only those are materialised
     my_frames = plan0.sampled_indices[rp["sampled_begin"]:rp["sampled_begin"] + rp["sampled_count"]]
     hosts = [synth.frames_nv12(wl, my_frames, "natural", clip=c) for c in range(clips)]
+    if args.surface == "i420":  # the same samples as planar Y, U, V surfaces
+        hosts = [{f: synth.nv12_to_i420(y, uv, wl.width, noise_seed=f) for f, (y, uv) in h.items()} for h in hosts]
 
     def stack_device(h):
-        """One contiguous device Y stack and UV stack per request (frames in
-        index order); surfaces point into them."""
+        """One contiguous device stack per plane (Y, UV -- or Y, U, V for I420)
+        per request (frames in index order); surfaces point into them."""
         fr = sorted(h)
         if not fr:
             return {}, None
-        Y = torch.from_numpy(np.stack([h[f][0] for f in fr])).cuda()
-        UV = torch.from_numpy(np.stack([h[f][1] for f in fr])).cuda()
-        return {f: (Y[i], UV[i]) for i, f in enumerate(fr)}, (Y, UV)
+        planes = tuple(torch.from_numpy(np.stack([h[f][p] for f in fr])).cuda() for p in range(len(h[fr[0]])))
+        return {f: tuple(pl[i] for pl in planes) for i, f in enumerate(fr)}, planes
 
     stacks = [stack_device(h) for h in hosts]
     devs = [d for d, _ in stacks]
@@ -320,14 +321,15 @@ def run_ours(args):
     # the last read-back.
     from cuda.bindings import runtime as cudart
 
-    pinned = [(torch.from_numpy(np.stack([h[f][0] for f in sorted(h)])).pin_memory(),
-               torch.from_numpy(np.stack([h[f][1] for f in sorted(h)])).pin_memory()) if h else None for h in hosts]
+    pinned = [tuple(torch.from_numpy(np.stack([h[f][p] for f in sorted(h)])).pin_memory()
+                    for p in range(len(next(iter(h.values()))))) if h else None for h in hosts]
     stacks2 = [stack_device(h) for h in hosts]
     surfs2 = [fc.SurfaceTable.from_tensors(d, wl.num_frames) for d, _ in stacks2]
     sets = [([st for _, st in stacks], surfs), ([st for _, st in stacks2], surfs2)]
     res_host = torch.empty((clips, 1176), dtype=tdt).pin_memory()
     W, H = wl.width, wl.height
-    h2d = sum(len(h) * (W * H + W * (H // 2)) for h in hosts)
+    h2d = sum(len(h) * (W * H + W * (H // 2)) for h in hosts)  # NV12 and I420 carry the same bytes
+    widths = (W, W // 2, W // 2) if args.surface == "i420" else (W, W)  # visible bytes per plane row
     e2e_steps = max(3, min(args.steps, 10))
     cstream = torch.cuda.Stream()
     up_done = [torch.cuda.Event(), torch.cuda.Event()]
@@ -340,8 +342,8 @@ def run_ours(args):
         for pc, st in zip(pinned, dv_set):
             if pc is None:
                 continue
-            for src, dst in zip(pc, st):  # Y stack, UV stack: one 2-D copy each (W bytes per row)
-                err, = cudart.cudaMemcpy2DAsync(dst.data_ptr(), dst.stride(1), src.data_ptr(), src.stride(1), W,
+            for src, dst, wb in zip(pc, st, widths):  # one 2-D copy per plane stack (visible bytes per row)
+                err, = cudart.cudaMemcpy2DAsync(dst.data_ptr(), dst.stride(1), src.data_ptr(), src.stride(1), wb,
                                                 src.shape[0] * src.shape[1], H2D, cstream.cuda_stream)
                 assert err == cudart.cudaError_t.cudaSuccess, err
         up_done[k & 1].record(cstream)
@@ -394,7 +396,7 @@ def run_ours(args):
             abytes = clips * max(algorithmic_bytes(plan0, wl, r, 1 if u8x else tok_bytes) for r in plan0.ranks())
             kern_for_roof = kern_max
         achieved = abytes / (kern_for_roof * 1e-3) / 1e9
-        same_kernel = world == 1 and args.tokens == "f32" and args.color == "bt601"
+        same_kernel = world == 1 and args.tokens == "f32" and args.color == "bt601" and args.surface == "nv12"
         traffic = load_traffic(args.config) if same_kernel else None
         # second roofline: the kernel is bound by instruction issue;
         # warp instructions per launch from the committed ncu capture of this config
@@ -415,7 +417,7 @@ def run_ours(args):
             "config": {"workload": f"{args.config}: {wl.note}", "frames": n_all, "requests": clips,
                        "resized_hw": list(plan0.resized), "grid_thw": list(plan0.grid_thw),
                        "token_bytes": clips * plan0.token_rows * 1176 * tok_bytes, "parallelism": f"gop-dp{world}",
-                       "color": args.color,
+                       "color": args.color, "surface": args.surface,
                        "l2": "per-step inputs+outputs (1.19 GB for c2) exceed the 126 MB L2; no flush",
                        "kernel_ms_avg": round(kern_max if world > 1 else kern_avg, 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -459,6 +461,8 @@ def main():
                     help="N>1 exchange format: u8 codes + encoder-side expand (default), or the tokens themselves")
     ap.add_argument("--color", default="bt601", choices=["bt601", "bt709", "bt601_full", "bt709_full"],
                     help="YUV->RGB matrix (NEXT-4 variant; the BASELINE metric is bt601)")
+    ap.add_argument("--surface", default="nv12", choices=["nv12", "i420"],
+                    help="decoded surface layout: NV12 (interleaved chroma) or I420 (planar U, V)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -38,7 +38,8 @@
 extern "C" {
 #endif
 
-#define FC_ABI_VERSION 2  /* 2: token_dtype + color in fc_model_cfg; tokens as void* */
+#define FC_ABI_VERSION 3  /* 2: token_dtype + color in fc_model_cfg; tokens as void*
+                             3: surface_format in fc_model_cfg, v plane in the surface */
 #define FC_TOKEN_COLS 1176 /* 3 channels * 2 (temporal patch) * 14 * 14 */
 
 typedef enum {
@@ -102,6 +103,14 @@ typedef enum {
   FC_COLOR_BT709_FULL = 3     /* 256, 403 / -48, -120 / 475 */
 } fc_color;
 
+/* Decoded-surface layout (north star: "decoded NV12/YUV420 GOP surfaces").
+ * Both are 8-bit 4:2:0 with nearest 2x2 chroma; they differ only in where the
+ * chroma bytes live, so both give the same RGB (R3/R15) for the same samples. */
+typedef enum {
+  FC_SURFACE_NV12 = 0, /* Y plane + one interleaved U,V plane (NVDEC's output, default) */
+  FC_SURFACE_I420 = 1  /* Y plane + separate U and V planes (planar YUV420, "I420") */
+} fc_surface_format;
+
 /* Model / preprocessing configuration (Qwen2-VL video processor defaults,
  * filled by fc_model_cfg_default). */
 typedef struct {
@@ -127,6 +136,7 @@ typedef struct {
   int32_t encoder_rank;        /* rank that receives the gathered tokens (default 0) */
   fc_token_dtype token_dtype;  /* FC_TOKENS_F32 (default) or FC_TOKENS_BF16 */
   fc_color color;              /* FC_COLOR_BT601_LIMITED (default) */
+  fc_surface_format surface_format; /* FC_SURFACE_NV12 (default) or FC_SURFACE_I420 (ABI 3) */
 } fc_model_cfg;
 
 void fc_model_cfg_default(fc_model_cfg* cfg);
@@ -179,15 +189,22 @@ typedef struct {
 
 fc_status fc_plan_rank(const fc_plan_t* plan, int32_t rank, fc_rank_plan* out);
 
-/* One decoded NV12 frame in device memory: luma plane y (height rows x
- * pitch_y bytes) and interleaved U,V plane uv (height/2 rows x pitch_uv
- * bytes).  Both pointers 16-byte aligned; both pitches multiples of 16 and
- * >= width.  Surfaces must stay valid until the enqueued work completes. */
+/* One decoded frame in device memory (layout: the plan's cfg.surface_format).
+ *   FC_SURFACE_NV12: luma plane y (height rows x pitch_y bytes) and the
+ *     interleaved U,V plane uv (height/2 rows x pitch_uv bytes, >= width);
+ *     v is ignored (NULL).
+ *   FC_SURFACE_I420: luma plane y, U plane uv and V plane v (height/2 rows x
+ *     pitch_uv bytes each, >= width/2; U and V share the pitch).
+ * All plane pointers 16-byte aligned; pitches multiples of 16 and >= width
+ * (y) / the chroma width above.  Surfaces must stay valid until the enqueued
+ * work completes. */
 typedef struct {
   const uint8_t* y;
   const uint8_t* uv;
   int64_t pitch_y, pitch_uv;
+  const uint8_t* v;  /* ABI 3: V plane of an I420 surface, else NULL */
 } fc_nv12_surface;
+typedef fc_nv12_surface fc_yuv_surface;
 
 /* fc_preprocess -- Alg. 1 l.21-22 (convert_AVframes_to_tensor_and_resize)
  * for rank `rank`: one fused kernel launch on `stream` computing, for the

@@ -344,6 +344,22 @@ def codes_from_resized(rs: np.ndarray) -> np.ndarray:
     return out
 
 
+def i420_chroma_to_nv12(u: np.ndarray, v: np.ndarray, width: int) -> np.ndarray:
+    """Planar U, V rows (I420) -> the interleaved U,V rows of NV12 holding the
+    same samples: uv[r][2i] = U[r][i], uv[r][2i+1] = V[r][i] (the two layouts
+    are the same 4:2:0 samples; north star "NV12/YUV420 surfaces")."""
+    cw = width // 2
+    uv = np.empty((u.shape[0], width), np.uint8)
+    uv[:, 0::2] = u[:, :cw]
+    uv[:, 1::2] = v[:, :cw]
+    return uv
+
+
+def preprocess_i420(frames, width: int, height: int, w2: int, h2: int, **kw):
+    """O7..O11 on I420 frames (y, u, v): chroma interleaved, then `preprocess`."""
+    return preprocess([(y, i420_chroma_to_nv12(u, v, width)) for y, u, v in frames], width, height, w2, h2, **kw)
+
+
 def preprocess(frames: list[tuple[np.ndarray, np.ndarray]], width: int, height: int, w2: int, h2: int,
                mean=CLIP_MEAN, std=CLIP_STD, rescale: float = 1 / 255, want_rgb: bool = False,
                nthreads: int = 1, matrix: str = "bt601"):

@@ -65,6 +65,7 @@ class ModelCfg:
     rescale_factor: float | None = None
     token_dtype: str = "f32"        # "f32" (HF output) | "bf16" (R16) | "u8" (codes; NEXT-1 exchange format)
     color: str = "bt601"            # "bt601" (R3) | "bt709" | "bt601_full" | "bt709_full" (R15)
+    surface_format: str = "nv12"    # "nv12" (interleaved chroma) | "i420" (planar U, V)
 
     def to_c(self):
         c = _native.ModelCfgC()
@@ -74,6 +75,7 @@ class ModelCfg:
         c.sampling = _native.SAMPLING[self.sampling]
         c.token_dtype = _native.TOKEN_DTYPES[self.token_dtype]
         c.color = _native.COLORS[self.color]
+        c.surface_format = _native.SURFACES[self.surface_format]
         c.sample_fps = self.sample_fps
         c.num_frames = self.num_frames
         c.min_frames = self.min_frames
@@ -156,10 +158,15 @@ class SurfaceTable:
         self.n = num_frames
         self._keep: dict[int, tuple] = {}
 
-    def set(self, frame: int, y, uv) -> None:
-        """y: uint8 [H, pitch_y] device tensor; uv: uint8 [H/2, pitch_uv]."""
-        self.arr[frame] = _native.Nv12SurfaceC(y.data_ptr(), uv.data_ptr(), y.stride(0), uv.stride(0))
-        self._keep[frame] = (y, uv)
+    def set(self, frame: int, y, uv, v=None) -> None:
+        """NV12: y uint8 [H, pitch_y] device tensor, uv uint8 [H/2, pitch_uv]
+        (interleaved U,V).  I420: uv = the U plane and v = the V plane, both
+        uint8 [H/2, pitch_uv] (same pitch)."""
+        if v is not None and v.stride(0) != uv.stride(0):
+            raise ValueError("I420 U and V planes must share the pitch")
+        self.arr[frame] = _native.Nv12SurfaceC(y.data_ptr(), uv.data_ptr(), y.stride(0), uv.stride(0),
+                                               v.data_ptr() if v is not None else None)
+        self._keep[frame] = (y, uv, v)
 
     @classmethod
     def from_tensors(cls, frames: dict | Sequence, num_frames: int | None = None) -> "SurfaceTable":
@@ -169,7 +176,7 @@ class SurfaceTable:
         t = cls(n)
         for k, v in items:
             if v is not None:
-                t.set(k, v[0], v[1])
+                t.set(k, *v)
         return t
 
 

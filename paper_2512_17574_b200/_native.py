@@ -15,13 +15,14 @@ LIB_PATH = os.path.join(HERE, f"libfc_{os.environ['FC_LIB_VARIANT']}.so" if os.e
                         else "libfc.so")
 
 FC_TOKEN_COLS = 1176
-ABI_VERSION = 2  # include/fc.h FC_ABI_VERSION this binding marshals for
+ABI_VERSION = 3  # include/fc.h FC_ABI_VERSION this binding marshals for
 STATUS = {0: "FC_OK", 1: "FC_ERR_INVALID_ARG", 2: "FC_ERR_EMPTY_SELECTION", 3: "FC_ERR_ASPECT_RATIO",
           4: "FC_ERR_UNSUPPORTED", 5: "FC_ERR_MISSING_SURFACE", 6: "FC_ERR_RANK", 7: "FC_ERR_OOM",
           8: "FC_ERR_CUDA", 9: "FC_ERR_NCCL"}
 SAMPLING = {"fps_stride": 0, "linspace": 1, "explicit": 2}
 TOKEN_DTYPES = {"f32": 0, "bf16": 1, "u8": 2}
 COLORS = {"bt601": 0, "bt709": 1, "bt601_full": 2, "bt709_full": 3}
+SURFACES = {"nv12": 0, "i420": 1}
 
 
 class FcError(RuntimeError):
@@ -49,7 +50,8 @@ class ModelCfgC(ctypes.Structure):
                 ("resized_height", ctypes.c_int32), ("resized_width", ctypes.c_int32),
                 ("image_mean", ctypes.c_float * 3), ("image_std", ctypes.c_float * 3),
                 ("rescale_factor", ctypes.c_double), ("world_size", ctypes.c_int32),
-                ("encoder_rank", ctypes.c_int32), ("token_dtype", ctypes.c_int), ("color", ctypes.c_int)]
+                ("encoder_rank", ctypes.c_int32), ("token_dtype", ctypes.c_int), ("color", ctypes.c_int),
+                ("surface_format", ctypes.c_int)]
 
 
 class PagedTokensC(ctypes.Structure):
@@ -74,7 +76,7 @@ class RankPlanC(ctypes.Structure):
 
 class Nv12SurfaceC(ctypes.Structure):
     _fields_ = [("y", ctypes.c_void_p), ("uv", ctypes.c_void_p), ("pitch_y", ctypes.c_int64),
-                ("pitch_uv", ctypes.c_int64)]
+                ("pitch_uv", ctypes.c_int64), ("v", ctypes.c_void_p)]
 
 
 EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_get", "fc_plan_sampled_indices",

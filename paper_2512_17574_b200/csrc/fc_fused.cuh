@@ -88,9 +88,12 @@ struct Params {
   uint32_t page_shift, page_mask, page_rows;
   void* const* tokj;  // device: per-job token base (batch launches) or null -> tokens
   const CUtensorMap* tmg;  // device copy of the maps (launches past kMaxInlineFrames frames) or null -> tm
-  unsigned long long* cta_t;
-  int smap;           // 1: strip-synchronous work mapping (grid = a multiple of nstrips)  // FC_CTA_TIMES experiments: per CTA {start, end, smid} (ns) or null
-  CUtensorMap tm[2 * kMaxInlineFrames];  // per frame: Y plane (box BW x 16), UV plane (box BW x 8)
+  unsigned long long* cta_t;  // FC_CTA_TIMES experiments: per CTA {start, end, smid} (ns) or null
+  int smap;           // 1: strip-synchronous work mapping (CTA b owns strip b % nstrips)
+  int sxmask;         // strip source-window start alignment: ~15, or ~31 for I420 (TMA box starts 16-B aligned)
+  // tensor maps per frame: Y (box BW x 16) + UV (box BW x 8) for NV12, or
+  // Y + U + V (boxes BW/2 x 8) for I420 -- up to 2 * kMaxInlineFrames maps inline
+  CUtensorMap tm[2 * kMaxInlineFrames];
 };
 
 // Walk of one CTA's work: contiguous (pair, strip, band) items, split into
@@ -117,19 +120,35 @@ __device__ __forceinline__ bool next_run(const Params& p, int& cur, int i1, int 
   return true;
 }
 
+// Raw-stage byte offset of the chroma of (sub-box, luma row rr, byte column xo
+// within the sub-box): NV12 -> the interleaved U,V pair row; I420 -> the U row
+// (the V row is 4*BW bytes further)
+template <bool I420>
+__device__ __forceinline__ int chroma_offset(const Params& p, int base, int sub, int rr, int xo) {
+  return I420 ? base + sub * 8 * p.BW + (rr >> 1) * (p.BW >> 1) + (xo >> 1)
+                : base + (sub * 8 + (rr >> 1)) * p.BW + xo;
+}
+
 // Issue the TMA tensor copies of one 16-row chunk into a raw stage (one
 // thread): per frame of the pair, NX boxes of Y (BW x 16 rows) then NX boxes
 // of UV (BW x 8 rows), after arming the stage's full barrier with their bytes.
+template <bool I420>
 __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, int k, uint8_t* raw, uint64_t* bar) {
   const CUtensorMap* tm = p.tmg != nullptr ? p.tmg : p.tm;
+  constexpr int mpf = I420 ? 3 : 2;  // maps per frame: Y, UV (NV12) or Y, U, V (I420)
   fence_proxy_async();
   mbar_arrive_expect_tx(bar, static_cast<uint32_t>(2 * 24 * p.BW * p.NX));
   for (int f = 0; f < 2; ++f)
     for (int pl = 0; pl < 2; ++pl)
       for (int sub = 0; sub < p.NX; ++sub) {
         uint8_t* dst = raw + f * 24 * p.BW * p.NX + (pl ? 16 * p.BW * p.NX + sub * 8 * p.BW : sub * 16 * p.BW);
-        tma_load_2d(dst, &tm[2 * (2 * pair + f) + pl], SX0 + sub * p.BW,
-                    pl ? k * (kChunkRows / 2) : k * kChunkRows, bar);
+        const CUtensorMap* m = &tm[mpf * (2 * pair + f) + pl];
+        if (pl && I420) {  // U rows then V rows, BW/2 bytes each, in the sub-box's 8*BW bytes
+          tma_load_2d(dst, m, (SX0 >> 1) + sub * (p.BW >> 1), k * (kChunkRows / 2), bar);
+          tma_load_2d(dst + 4 * p.BW, m + 1, (SX0 >> 1) + sub * (p.BW >> 1), k * (kChunkRows / 2), bar);
+        } else {
+          tma_load_2d(dst, m, SX0 + sub * p.BW, pl ? k * (kChunkRows / 2) : k * kChunkRows, bar);
+        }
       }
 }
 
@@ -146,7 +165,7 @@ __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, 
 // Work items are (pair, strip, band) triples; CTA b takes [b*T/G, (b+1)*T/G).
 // Strips are whole merge blocks, so every token row is written by one CTA in
 // one band (no partial-sector merging across CTAs in L2).
-template <int KSH, int KSV, bool DBG, int TOK, bool PAGED = false>
+template <int KSH, int KSV, bool DBG, int TOK, bool PAGED = false, bool I420 = false>
 // Narrow-window instances (KSH = KSV = 1: c2, c3, c5) fit 64 registers without
 // spills and run 4 CTAs/SM (with 2 TMA stages); wider windows keep 80 / 3.
 __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
@@ -214,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
     const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
     const int xb = 16 * q, sub = xb >> p.bwshift, xo = xb & p.bwmask;
     cy[e] = f * RAWF + (sub * 16 + rr) * p.BW + xo;
-    cuv[e] = f * RAWF + 16 * p.BW * p.NX + (sub * 8 + (rr >> 1)) * p.BW + xo;
+    cuv[e] = chroma_offset<I420>(p, f * RAWF + 16 * p.BW * p.NX, sub, rr, xo);
     crgb[e] = ((f * 3) * CH + rr) * SWP + xb;
   }
   const uint32_t rgb_s = smem_u32(rgb);
@@ -236,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
   int cur = i0;
   while (next_run(p, cur, i1, sfix, r)) {
     const int X0 = r.strip * p.sw;
-    const int SX0 = __ldg(p.hx + X0) & ~15;
+    const int SX0 = __ldg(p.hx + X0) & p.sxmask;  // 16-aligned (NV12) / 32-aligned (I420: U, V boxes at SX0/2)
     const int npatch = min(p.sw / 14, (p.W2 - X0) / 14);  // valid patches in this strip
     const bool hact = warp < p.htiles;
     // H-pass B fragments of this warp's output tile (constant over the strip)
@@ -269,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
     // run consumed all it issued, before the barrier that ended its last band)
     if (issuer)
       for (int j = 0; j < NS && r.kfirst + j < r.klast; ++j)
-        issue_chunk(p, r.pair, SX0, r.kfirst + j, raw + ((seq + j) & smask) * 2 * RAWF, &full[(seq + j) & smask]);
+        issue_chunk<I420>(p, r.pair, SX0, r.kfirst + j, raw + ((seq + j) & smask) * 2 * RAWF, &full[(seq + j) & smask]);
     for (int hb_ = r.hb0; hb_ < r.hb1; ++hb_) {
       const int yo0 = hb_ * 28;
       const int kneed = min(p.nchunks, (__ldg(p.vx + yo0 + 27) + __ldg(p.vcnt + yo0 + 27) + CH - 1) / CH);
@@ -281,7 +300,15 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
         // ---- a5: NV12 -> RGB planes, 16 pixels per item
         auto convert = [&](int oy, int ouv, int orgb, int e) {
             const uint4 Yv = *reinterpret_cast<const uint4*>(rawb + oy);
-            const uint4 UVv = *reinterpret_cast<const uint4*>(rawb + ouv);
+            uint4 UVv;
+            if constexpr (I420) {  // interleave 8 U and 8 V bytes into NV12 order [U0 V0 U1 V1 ...]
+              const uint2 u = *reinterpret_cast<const uint2*>(rawb + ouv);
+              const uint2 v = *reinterpret_cast<const uint2*>(rawb + ouv + 4 * p.BW);
+              UVv = make_uint4(__byte_perm(u.x, v.x, 0x5140), __byte_perm(u.x, v.x, 0x7362),
+                               __byte_perm(u.y, v.y, 0x5140), __byte_perm(u.y, v.y, 0x7362));
+            } else {
+              UVv = *reinterpret_cast<const uint4*>(rawb + ouv);
+            }
             uint4 Rv, Gv, Bv;
             yuv2rgb_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
             yuv2rgb_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
@@ -318,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
             for (int it = tid; it < citems; it += kComputeThreads) {
               const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
               const int xb = 16 * q, sub = xb >> p.bwshift, xo = xb & p.bwmask;
-              convert(f * RAWF + (sub * 16 + rr) * p.BW + xo, f * RAWF + 16 * p.BW * p.NX + (sub * 8 + (rr >> 1)) * p.BW + xo,
+              convert(f * RAWF + (sub * 16 + rr) * p.BW + xo, chroma_offset<I420>(p, f * RAWF + 16 * p.BW * p.NX, sub, rr, xo),
                       ((f * 3) * CH + rr) * SWP + xb, (it - tid) / kComputeThreads);
             }
           }
@@ -326,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
         bar_sync(1, kComputeThreads);              // RGB planes complete; raw stage free
         // refill the stage just converted with chunk k + nstages; the issuing
         // warp owns no H tile, so this runs beside the H pass, off the critical path
-        if (issuer && k + NS < r.klast) issue_chunk(p, r.pair, SX0, k + NS, raw + buf * 2 * RAWF, &full[buf]);
+        if (issuer && k + NS < r.klast) issue_chunk<I420>(p, r.pair, SX0, k + NS, raw + buf * 2 * RAWF, &full[buf]);
         // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of 3 for ILP
         if (hact) {
           const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + 2 * (g & 1);  // bytes of rows 2g, 2g+1
@@ -496,13 +523,15 @@ struct Instance {
   int ksh, ksv;
   KernelFn fn, fn_dbg, fn_bf16, fn_u8;  // fp32 tokens / + parity-test dumps / bf16 tokens / u8 codes
   KernelFn fn_paged, fn_paged_bf16;     // NEXT-2: fp32 / bf16 tokens into a paged pool
+  KernelFn fn_i420, fn_i420_dbg;        // I420 surfaces: fp32 tokens / + parity-test dumps
 };
 
 // One translation unit per KSH instantiates its instances (parallel build).
 #define FC_INST(A, B)                                                                                  \
   Instance{A, B, fc_fused_kernel<A, B, false, FC_TOKENS_F32>, fc_fused_kernel<A, B, true, FC_TOKENS_F32>, \
            fc_fused_kernel<A, B, false, FC_TOKENS_BF16>, fc_fused_kernel<A, B, false, FC_TOKENS_U8>,   \
-           fc_fused_kernel<A, B, false, FC_TOKENS_F32, true>, fc_fused_kernel<A, B, false, FC_TOKENS_BF16, true>}
+           fc_fused_kernel<A, B, false, FC_TOKENS_F32, true>, fc_fused_kernel<A, B, false, FC_TOKENS_BF16, true>, \
+           fc_fused_kernel<A, B, false, FC_TOKENS_F32, false, true>, fc_fused_kernel<A, B, true, FC_TOKENS_F32, false, true>}
 void instances_ksh1(Instance* out);  // out[0..3] = KSV 1..4
 void instances_ksh2(Instance* out);
 void instances_ksh3(Instance* out);

@@ -238,7 +238,7 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
 
 struct Geometry {
   int sw, htiles, SWPN, SWP, BW, NX, TR, TRW, nstrips, nchunks;
-  KernelFn fn, fn_dbg, fn_bf16, fn_u8, fn_paged, fn_paged_bf16;
+  KernelFn fn, fn_dbg, fn_bf16, fn_u8, fn_paged, fn_paged_bf16, fn_i420, fn_i420_dbg;
   size_t smem;   // at nstages
   int nstages;   // raw TMA stages: 4, or 2 when that buys another CTA per SM (wide-window configs)
 };
@@ -260,17 +260,20 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
   int need = 16, taps = 16;
   for (int s = 0; s < nstrips; ++s) {
     const int X0 = s * SW, X1 = std::min(X0 + SW, P->w2);
-    const int SX0 = th.xmin[X0] & ~15;
+    const int SX0 = th.xmin[X0] & (P->cfg.surface_format == FC_SURFACE_I420 ? ~31 : ~15);  // == the kernel's sxmask
     for (int i = 0; i < g->htiles && X0 + 8 * i < X1; ++i)
       need = std::max(need, (th.xmin[X0 + 8 * i] & ~3) - SX0 + 32 * dt->ksh);
     for (int o = X0; o < X1; ++o) taps = std::max(taps, th.xmin[o] + th.cnt[o] - SX0);
   }
-  need = std::max(need, (taps + 15) / 16 * 16);  // the converted width (SWPN) fits every row
+  // converted width; I420 loads U and V boxes of SWPN/2 bytes, which TMA wants
+  // in multiples of 16
+  const int cq = P->cfg.surface_format == FC_SURFACE_I420 ? 32 : 16;
+  need = std::max(need, (taps + cq - 1) / cq * cq);  // the converted width (SWPN) fits every row
   // round up to 8 mod 16: H-pass lanes g read rows 2g, 2g+1, and with a row
   // stride of 4m+2 words the rows 2g of the 8 lane groups hit distinct bank quads
   const int swp8 = (need + 7) / 8 * 8;
   const int swpb = swp8 % 16 == 8 ? swp8 : swp8 + 8;
-  g->SWPN = ((taps + 15) / 16) * 16;
+  g->SWPN = ((taps + cq - 1) / cq) * cq;
   g->SWP = swpb;
   g->NX = (g->SWPN + 255) / 256;                       // TMA boxes are at most 256 wide
   g->BW = g->NX == 1 ? g->SWPN : 256;
@@ -299,6 +302,8 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
       g->fn_u8 = in.fn_u8;
       g->fn_paged = in.fn_paged;
       g->fn_paged_bf16 = in.fn_paged_bf16;
+      g->fn_i420 = in.fn_i420;
+      g->fn_i420_dbg = in.fn_i420_dbg;
     }
   }
   if (!g->fn) return fail(FC_ERR_UNSUPPORTED, "no kernel instance for this resize window");
@@ -414,15 +419,18 @@ static fc_status rank_frames(const fc_plan_s* P, int32_t rank, const fc_nv12_sur
   for (int64_t i = 0; i < rp.sampled_count; ++i) frames->push_back(P->sampled[rp.sampled_begin + i]);
   for (int64_t i = 0; i < rp.pad_frames; ++i) frames->push_back(frames->back());
   const int W = P->meta.width;
+  const bool i420 = P->cfg.surface_format == FC_SURFACE_I420;
+  const int cw = i420 ? W / 2 : W;  // chroma plane bytes per row
   for (int64_t f : *frames) {
     if (f >= num_surfaces) return fail(FC_ERR_MISSING_SURFACE, "surface array too short for frame " + std::to_string(f));
     const fc_nv12_surface& s = surfaces[f];
-    if (!s.y || !s.uv) return fail(FC_ERR_MISSING_SURFACE, "NULL surface for frame " + std::to_string(f));
-    if ((reinterpret_cast<uintptr_t>(s.y) & 15) || (reinterpret_cast<uintptr_t>(s.uv) & 15))
+    if (!s.y || !s.uv || (i420 && !s.v)) return fail(FC_ERR_MISSING_SURFACE, "NULL surface for frame " + std::to_string(f));
+    if ((reinterpret_cast<uintptr_t>(s.y) & 15) || (reinterpret_cast<uintptr_t>(s.uv) & 15) ||
+        (i420 && (reinterpret_cast<uintptr_t>(s.v) & 15)))
       return fail(FC_ERR_UNSUPPORTED, "surface planes must be 16-byte aligned");
-    if ((s.pitch_y & 15) || (s.pitch_uv & 15) || s.pitch_y < W || s.pitch_uv < W || s.pitch_y > INT32_MAX ||
+    if ((s.pitch_y & 15) || (s.pitch_uv & 15) || s.pitch_y < W || s.pitch_uv < cw || s.pitch_y > INT32_MAX ||
         s.pitch_uv > INT32_MAX)
-      return fail(FC_ERR_UNSUPPORTED, "pitches must be multiples of 16 and >= width");
+      return fail(FC_ERR_UNSUPPORTED, "pitches must be multiples of 16, pitch_y >= width, pitch_uv >= chroma width");
   }
   return FC_OK;
 }
@@ -491,7 +499,11 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
     return fail(FC_ERR_UNSUPPORTED, "debug dumps are built for fp32 tokens only");
   if (paged && (td == FC_TOKENS_U8 || jobs.size() != 1))
     return fail(FC_ERR_UNSUPPORTED, "paged output: one job, F32 or BF16 tokens");
-  KernelFn fn = (dbg_src || dbg_rs)      ? g.fn_dbg
+  const bool i420 = P->cfg.surface_format == FC_SURFACE_I420;
+  if (i420 && (td != FC_TOKENS_F32 || paged))
+    return fail(FC_ERR_UNSUPPORTED, "I420 surfaces: fp32 tokens, linear output (other variants are built for NV12)");
+  KernelFn fn = i420                     ? ((dbg_src || dbg_rs) ? g.fn_i420_dbg : g.fn_i420)
+                : (dbg_src || dbg_rs)    ? g.fn_dbg
                 : paged                ? (td == FC_TOKENS_BF16 ? g.fn_paged_bf16 : g.fn_paged)
                 : td == FC_TOKENS_BF16 ? g.fn_bf16
                 : td == FC_TOKENS_U8   ? g.fn_u8
@@ -565,15 +577,23 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
     prm.page_rows = static_cast<uint32_t>(paged->page_rows);
     prm.page_first = paged->first_offset;
   }
-  const bool inline_maps = jobs.size() == 1 && nf <= kMaxInlineFrames;
-  std::vector<CUtensorMap> maps(inline_maps ? 0 : 2 * nf);
+  // tensor maps per frame: Y + interleaved UV (NV12), or Y + U + V (I420)
+  const int mpf = i420 ? 3 : 2;
+  prm.sxmask = i420 ? ~31 : ~15;  // TMA box starts must be 16-byte aligned: SX0 (Y) and SX0/2 (U, V)
+  const bool inline_maps = jobs.size() == 1 && mpf * nf <= 2 * kMaxInlineFrames;
+  std::vector<CUtensorMap> maps(inline_maps ? 0 : mpf * nf);
   CUtensorMap* mp = inline_maps ? prm.tm : maps.data();
   for (size_t j = 0; j < jobs.size(); ++j)
     for (int64_t i = 0; i < nfj; ++i) {
       const fc_nv12_surface& sf = jobs[j].surfaces[jobs[j].frames[i]];
       const int64_t fi = static_cast<int64_t>(j) * nfj + i;
-      st = tensor_map(sf.y, sf.pitch_y, H, g.BW, kChunkRows, &mp[2 * fi]);
-      if (st == FC_OK) st = tensor_map(sf.uv, sf.pitch_uv, H / 2, g.BW, kChunkRows / 2, &mp[2 * fi + 1]);
+      st = tensor_map(sf.y, sf.pitch_y, H, g.BW, kChunkRows, &mp[mpf * fi]);
+      if (i420) {
+        if (st == FC_OK) st = tensor_map(sf.uv, sf.pitch_uv, H / 2, g.BW / 2, kChunkRows / 2, &mp[mpf * fi + 1]);
+        if (st == FC_OK) st = tensor_map(sf.v, sf.pitch_uv, H / 2, g.BW / 2, kChunkRows / 2, &mp[mpf * fi + 2]);
+      } else if (st == FC_OK) {
+        st = tensor_map(sf.uv, sf.pitch_uv, H / 2, g.BW, kChunkRows / 2, &mp[mpf * fi + 1]);
+      }
       if (st != FC_OK) return st;
     }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -734,6 +754,7 @@ fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* rank
     const fc_plan_s &A = *jp[a], &B = *jp[b];
     return A.meta.width == B.meta.width && A.meta.height == B.meta.height && A.w2 == B.w2 && A.h2 == B.h2 &&
            A.cfg.token_dtype == B.cfg.token_dtype && A.cfg.color == B.cfg.color && A.lut_dev == B.lut_dev &&
+           A.cfg.surface_format == B.cfg.surface_format &&
            jobs[a].frames.size() == jobs[b].frames.size();
   };
   std::vector<Job> group;

@@ -461,6 +461,8 @@ fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t*
     return fail(FC_ERR_UNSUPPORTED, "unknown token_dtype");
   if (c.color < FC_COLOR_BT601_LIMITED || c.color > FC_COLOR_BT709_FULL)
     return fail(FC_ERR_UNSUPPORTED, "unknown color matrix");
+  if (c.surface_format != FC_SURFACE_NV12 && c.surface_format != FC_SURFACE_I420)
+    return fail(FC_ERR_UNSUPPORTED, "unknown surface format");
 
   fc_plan_s* P = new (std::nothrow) fc_plan_s();
   if (!P) return fail(FC_ERR_OOM, "plan allocation failed");

@@ -122,6 +122,22 @@ def frames_nv12(wl: Workload, indices, kind: str = "natural", clip: int = 0) -> 
     return {int(i): frame_nv12(wl.width, wl.height, int(i), kind, seed, wl.pitch) for i in indices}
 
 
+def nv12_to_i420(y: np.ndarray, uv: np.ndarray, width: int, pitch_c: int | None = None, noise_seed: int = 0):
+    """The same samples as planar I420: (y, u, v) with U = the even bytes and
+    V = the odd bytes of the interleaved chroma rows (data movement only).  The
+    chroma planes get pitch `pitch_c` (default pitch_for(width/2)) with noise in
+    the padding, which must never matter."""
+    cw = width // 2
+    pc = pitch_c or pitch_for(cw)
+    rng = np.random.default_rng(noise_seed)
+    u = rng.integers(0, 256, (uv.shape[0], pc), dtype=np.uint8)
+    v = rng.integers(0, 256, (uv.shape[0], pc), dtype=np.uint8)
+    u[:, :cw] = uv[:, 0:2 * cw:2]
+    v[:, :cw] = uv[:, 1:2 * cw:2]
+    return y, u, v
+
+
 def to_device(frames: dict, device="cuda") -> dict:
+    """Host planes -> device tensors; works for NV12 (y, uv) and I420 (y, u, v) tuples."""
     import torch
-    return {k: (torch.from_numpy(y).to(device), torch.from_numpy(uv).to(device)) for k, (y, uv) in frames.items()}
+    return {k: tuple(torch.from_numpy(p).to(device) for p in planes) for k, planes in frames.items()}

@@ -249,6 +249,30 @@ def test_nv12_chroma_siting(oracle):
     np.testing.assert_array_equal(red, exp)
 
 
+def test_i420_planar_chroma_per_pixel(oracle):
+    """I420 (planar U, V; north star "NV12/YUV420 surfaces"): every RGB pixel of
+    the oracle's I420 path equals the closed-form BT.601 of (Y[y][x],
+    U[y/2][x/2], V[y/2][x/2]) computed here pixel by pixel -- pins the planar
+    chroma addressing (which plane is U, the 2x2 siting) independently of the
+    NV12 interleave."""
+    rng = np.random.default_rng(5)
+    W, H = 14, 10
+    y = rng.integers(0, 256, (H, 16), dtype=np.uint8)
+    u = rng.integers(0, 256, (H // 2, 16), dtype=np.uint8)
+    v = rng.integers(0, 256, (H // 2, 16), dtype=np.uint8)
+    rgb = oracle.nv12_to_rgb(y, oracle.i420_chroma_to_nv12(u, v, W), W, H)
+    for yy in range(H):
+        for xx in range(W):
+            assert tuple(rgb[yy, xx]) == oracle.bt601_pixel(int(y[yy, xx]), int(u[yy // 2, xx // 2]),
+                                                             int(v[yy // 2, xx // 2])), (yy, xx)
+    # and the whole path: I420 tokens == NV12 tokens of the same samples
+    import synth
+    fr = [synth.frame_nv12(64, 48, i, "uniform", 3) for i in range(3)]
+    fi = [synth.nv12_to_i420(yy, uv, 64, noise_seed=i) for i, (yy, uv) in enumerate(fr)]
+    np.testing.assert_array_equal(oracle.preprocess_i420(fi, 64, 48, 56, 56).view(np.uint32),
+                                  oracle.preprocess(fr, 64, 48, 56, 56).view(np.uint32))
+
+
 # ------------------------------------------------------------------ O8
 RESIZE_SHAPES = [(320, 240, 392, 280), (1920, 1080, 1008, 560), (1280, 720, 1008, 560), (3840, 2160, 1008, 560),
                  (854, 480, 840, 476), (1280, 720, 728, 392), (1920, 1080, 1316, 728), (1920, 1080, 1932, 1092),

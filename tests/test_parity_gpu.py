@@ -504,3 +504,49 @@ def test_cuda_graph_capture_replay(fc, oracle, cuda):
     torch.cuda.synchronize()
     ref2 = oracle.preprocess([host2[i] for i in idx], W, H, w2, h2)
     np.testing.assert_array_equal(out.cpu().numpy().view(np.uint32), ref2.view(np.uint32))
+
+
+# ------------------------------------------------------ I420 surfaces
+@pytest.mark.parametrize("shape", [(320, 240, None), (1920, 1080, None), (3840, 2160, None), (200, 120, (56, 84)),
+                                   (1920, 1080, (224, 224))])
+@pytest.mark.parametrize("kind", ["uniform", "edges"])
+def test_i420_surfaces(fc, oracle, cuda, shape, kind):
+    """Planar YUV420 (I420) surfaces: Y + separate U and V planes with their
+    own pitch (3 TMA maps per frame).  RGB intermediates bit-exact and tokens
+    vs the oracle's I420 path; incl. 4K (two TMA boxes per row)."""
+    W, H, h2w2 = shape
+    extra = dict(resized_height=h2w2[0], resized_width=h2w2[1]) if h2w2 else {}
+    plan = make_plan(fc, W, H, 40, [0, 20], sampling="explicit", explicit_indices=[1, 9, 22, 33, 35],
+                     surface_format="i420", **extra)
+    idx = plan.sampled_indices
+    host = {i: synth.nv12_to_i420(*synth.frame_nv12(W, H, i, kind, 17), W, noise_seed=i) for i in idx}
+    surf = fc.SurfaceTable.from_tensors(synth.to_device(host), 40)
+    h2, w2 = plan.resized
+    ref_tok, ref_src, ref_rs = oracle.preprocess_i420([host[i] for i in idx], W, H, w2, h2, want_rgb=True)
+    tok, src, rs = fc.preprocess_debug(plan, 0, surf)
+    cuda.cuda.synchronize()
+    np.testing.assert_array_equal(src.cpu().numpy(), ref_src[list(range(5)) + [4]])
+    np.testing.assert_array_equal(rs.cpu().numpy(), ref_rs[list(range(5)) + [4]])
+    got = tok.cpu().numpy()
+    assert tol_check(got, ref_tok, f"i420 {W}x{H}") == got.size
+
+
+def test_i420_full_c2_bench_launch(fc, oracle, cuda):
+    """c2 (60 s 1080p, 120 frames) from I420 surfaces in the bench's launch
+    configuration (one launch, strip-synchronous mapping), sampled pairs vs
+    the oracle."""
+    import torch
+    wl = synth.CONFIGS["c2"]
+    plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
+                   fc.ModelCfg(surface_format="i420"))
+    idx = plan.sampled_indices
+    host = {i: synth.nv12_to_i420(*f, wl.width, noise_seed=i)
+            for i, f in synth.frames_nv12(wl, idx, "natural").items()}
+    surf = fc.SurfaceTable.from_tensors(synth.to_device(host), wl.num_frames)
+    out = fc.preprocess(plan, 0, surf)
+    torch.cuda.synchronize()
+    h2, w2 = plan.resized
+    rpp = plan.token_rows // plan.grid_thw[0]
+    for t in (0, 29, 59):
+        ref = oracle.preprocess_i420([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2)
+        assert tol_check(out[t * rpp:(t + 1) * rpp].cpu().numpy(), ref, f"c2 i420 pair {t}") == ref.size

@@ -203,7 +203,32 @@ def test_missing_surface_reported(fc):
     assert fc._native.STATUS[st] == "FC_ERR_MISSING_SURFACE"
 
 
-@pytest.mark.parametrize("field,value", [("token_dtype", 3), ("color", 4), ("color", -1)])
+@pytest.mark.parametrize("planes,status", [
+    ("y u v", "FC_ERR_CUDA"),                  # valid I420 surfaces reach the device check (no GPU here)
+    ("y u -", "FC_ERR_MISSING_SURFACE"),       # no V plane
+    ("y u v+8", "FC_ERR_UNSUPPORTED"),         # V plane not 16-byte aligned
+    ("y u v pitch16", "FC_ERR_UNSUPPORTED"),   # chroma pitch < width / 2
+])
+def test_i420_surface_validation(fc, planes, status):
+    """I420 surfaces (ABI 3: U in `uv`, V in `v`, shared chroma pitch >= W/2)
+    are validated before any device work."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    p = plan_of(fc, 64, 48, 100, [0, 50], sampling="explicit", explicit_indices=[0, 10], surface_format="i420")
+    buf = (ctypes.c_uint8 * (48 * 64 * 3 + 256))()
+    base = (ctypes.addressof(buf) + 15) & ~15
+    ub, vb = base + 48 * 64, base + 48 * 64 + 24 * 64
+    surf = fc.SurfaceTable(100)
+    for i in (0, 10):
+        v = None if planes.endswith("-") else vb + (8 if planes.endswith("v+8") else 0)
+        surf.arr[i] = fc._native.Nv12SurfaceC(base, ub, 64, 16 if planes.endswith("pitch16") else 32, v)
+    out = (ctypes.c_float * (p.token_rows * 1176))()
+    st = fc.lib().fc_preprocess(p.handle, 0, surf.arr, 100, ctypes.cast(out, ctypes.c_void_p), None, None)
+    assert fc._native.STATUS[st] == status, fc.lib().fc_last_error()
+
+
+@pytest.mark.parametrize("field,value", [("token_dtype", 3), ("color", 4), ("color", -1), ("surface_format", 2)])
 def test_unknown_variant_enums_rejected(fc, field, value):
     """NEXT-4 variant enums are validated by fc_plan (S:34 structured errors)."""
     meta = fc.VideoMeta(64, 48, 100, (30, 1), [0, 50])
@@ -219,9 +244,9 @@ def test_model_cfg_struct_matches_abi(fc):
     """The ctypes mirror of fc_model_cfg has the C layout: fc_model_cfg_default
     fills the trailing fields with their documented defaults."""
     c = fc._native.ModelCfgC()
-    c.token_dtype, c.color = 9, 9
+    c.token_dtype, c.color, c.surface_format = 9, 9, 9
     fc.lib().fc_model_cfg_default(ctypes.byref(c))
-    assert (c.token_dtype, c.color, c.world_size, c.encoder_rank) == (0, 0, 1, 0)
+    assert (c.token_dtype, c.color, c.surface_format, c.world_size, c.encoder_rank) == (0, 0, 0, 1, 0)
     assert abs(c.rescale_factor - 1 / 255) < 1e-15 and c.patch_size == 14
 
 

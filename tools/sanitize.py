@@ -1,6 +1,6 @@
 """Small runs of every kernel path for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck): fused kernel fp32 + debug + bf16 + u8 codes, a batch,
-a >120-frame launch (device descriptor), and fc_expand_tokens."""
+a >120-frame launch (device descriptor), I420 surfaces, and fc_expand_tokens."""
 import os
 import sys
 
@@ -14,6 +14,8 @@ import synth  # noqa: E402
 def run(W, H, N, gops, **cfg):
     plan = fc.Plan(fc.VideoMeta(W, H, N, (30, 1), gops), fc.ModelCfg(**cfg))
     host = {i: synth.frame_nv12(W, H, i, "natural", 3) for i in plan.sampled_indices}
+    if cfg.get("surface_format") == "i420":
+        host = {i: synth.nv12_to_i420(y, uv, W, noise_seed=i) for i, (y, uv) in host.items()}
     dev = synth.to_device(host)
     surf = fc.SurfaceTable.from_tensors(dev, N)
     return plan, surf, dev
@@ -35,5 +37,8 @@ fc.preprocess(planL, 0, surfL)  # 130 frames: tensor maps in the device descript
 plan224, surf224, _ = run(1920, 1080, 8, [0], sampling="explicit", explicit_indices=[0, 3],
                           resized_height=224, resized_width=224)
 fc.preprocess(plan224, 0, surf224)  # KSH=KSV=3, 28-column strips
+planI, surfI, _ = run(640, 360, 60, [0, 30], sample_fps=2.0, surface_format="i420")
+fc.preprocess(planI, 0, surfI)  # I420: Y, U, V tensor maps
+fc.preprocess_debug(planI, 0, surfI)
 torch.cuda.synchronize()
 print("sanitize workload done")
