@@ -195,6 +195,11 @@ def run_ours(args):
     # N>1 with the u8 exchange (NEXT-1, default): ranks produce u8 codes, the
     # gather moves 1176-byte rows, the encoder expands them to tokens
     u8x = world > 1 and args.exchange == "u8"
+    # N>1 with the paper's column split (--exchange colsplit): every
+    # rank keeps 1176/W columns of ALL rows (all-to-all of column blocks)
+    colx = world > 1 and args.exchange == "colsplit"
+    if colx and (clips != 1 or args.tokens != "f32"):
+        raise SystemExit("--exchange colsplit: single-request configs, f32 tokens")
     cfg = fc.ModelCfg(world_size=world, sample_fps=wl.sample_fps, token_dtype="u8" if u8x else args.tokens,
                       color=args.color, surface_format=args.surface)
     tok_bytes = 2 if args.tokens == "bf16" else 4
@@ -222,18 +227,24 @@ def run_ours(args):
     rows = rp["row_end"] - rp["row_begin"]
     tdt = torch.bfloat16 if args.tokens == "bf16" else torch.float32
     xdt = torch.uint8 if u8x else tdt  # what the kernel writes and the gather moves
-    outs = [torch.empty((max(rows, 1), 1176), dtype=xdt, device="cuda") for _ in range(clips)]
+    outs = [torch.empty((world, max(rows, 1), 1176 // world) if colx else (max(rows, 1), 1176), dtype=xdt,
+                        device="cuda") for _ in range(clips)]
+    mines = [torch.empty((plan0.token_rows, 1176 // world), dtype=torch.float32, device="cuda") if colx else None
+             for _ in range(clips)]
     comm = fc.NcclComm(rank, world) if world > 1 else None
     enc = cfg.encoder_rank
     fulls = [torch.empty((plan0.token_rows, 1176), dtype=xdt, device="cuda")
-             if (world > 1 and rank == enc) else None for _ in range(clips)]
+             if (world > 1 and rank == enc and not colx) else None for _ in range(clips)]
     toks = [torch.empty((plan0.token_rows, 1176), dtype=tdt, device="cuda")
             if (u8x and rank == enc) else None for _ in range(clips)]
     stream = torch.cuda.current_stream()
 
     def exchange(plans):
         """a10 (+ the encoder-side expand of the u8 exchange)."""
-        for pl, o, fl, tk in zip(plans, outs, fulls, toks):
+        for pl, o, fl, tk, mn in zip(plans, outs, fulls, toks, mines):
+            if colx:
+                fc.scatter_columns(pl, rank, comm, o if rows else None, mn)
+                continue
             fc.gather(pl, rank, comm, o if rows else None, fl)
             if tk is not None:
                 fc.expand_tokens(pl, fl, tk, args.tokens)
@@ -244,7 +255,9 @@ def run_ours(args):
         if ev_a is not None:
             ev_a.record(stream)
         if rows:
-            if clips == 1:
+            if colx:
+                fc.preprocess_colsplit(plans[0], rank, surfs[0], outs[0])  # a5-a9, column-block epilogue
+            elif clips == 1:
                 fc.preprocess(plans[0], rank, surfs[0], outs[0])   # a5-a9 (one launch)
             else:  # a5-a9 for every request in ONE launch (same shape)
                 fc.preprocess_batch([(pl, rank, sf) for pl, sf in zip(plans, surfs)], outs)
@@ -308,7 +321,11 @@ def run_ours(args):
         dist.all_reduce(gms, op=dist.ReduceOp.MAX)
         gbytes = clips * sum((r["row_end"] - r["row_begin"]) * 1176 * (1 if u8x else tok_bytes)
                              for i, r in enumerate(plan0.ranks()) if i != enc)
-        gather = {"exchange": "u8 codes + encoder expand" if u8x else args.tokens,
+        if colx:  # bytes into the busiest rank: every other rank's rows x its C columns
+            gbytes = max((plan0.token_rows - (r["row_end"] - r["row_begin"])) * (1176 // world) * 4
+                         for r in plan0.ranks())
+        gather = {"exchange": "column split all-to-all (P:527-530)" if colx else
+                  "u8 codes + encoder expand" if u8x else args.tokens,
                   "ms": round(gms.item(), 4), "bytes_into_encoder": gbytes,
                   "GB/s": round(gbytes / (gms.item() * 1e-3) / 1e9, 1), "nvlink_nominal_GB/s": 900,
                   "nvlink_measured_peer_GB/s": 770}
@@ -354,14 +371,18 @@ def run_ours(args):
         keep.append(plans)
         stream.wait_event(up_done[k & 1])
         if rows:
-            if clips == 1:
+            if colx:
+                fc.preprocess_colsplit(plans[0], rank, sf_set[0], outs[0])
+            elif clips == 1:
                 fc.preprocess(plans[0], rank, sf_set[0], outs[0])
             else:
                 fc.preprocess_batch([(pl, rank, sf) for pl, sf in zip(plans, sf_set)], outs)
         used[k & 1].record(stream)
         if world > 1:
             exchange(plans)
-        if world == 1 or rank == enc:  # one token row of every request's result back to the host
+        if colx:  # the first row of this rank's column slice
+            res_host[0][:1176 // world].copy_(mines[0][0], non_blocking=True)
+        elif world == 1 or rank == enc:  # one token row of every request's result back to the host
             for c in range(clips):
                 src = (toks[c] if u8x else fulls[c]) if world > 1 else outs[c]
                 res_host[c].copy_(src[0], non_blocking=True)
@@ -457,8 +478,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tokens", default="f32", choices=["f32", "bf16"],
                     help="token dtype (NEXT-4 variant; the BASELINE metric is f32)")
-    ap.add_argument("--exchange", default="u8", choices=["u8", "f32"],
-                    help="N>1 exchange format: u8 codes + encoder-side expand (default), or the tokens themselves")
+    ap.add_argument("--exchange", default="u8", choices=["u8", "f32", "colsplit"],
+                    help="N>1 exchange: u8 codes + encoder-side expand (default), the tokens themselves, or the "
+                         "paper's column split (every rank keeps 1176/N columns of all rows)")
     ap.add_argument("--color", default="bt601", choices=["bt601", "bt709", "bt601_full", "bt709_full"],
                     help="YUV->RGB matrix (NEXT-4 variant; the BASELINE metric is bt601)")
     ap.add_argument("--surface", default="nv12", choices=["nv12", "i420"],

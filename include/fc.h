@@ -293,6 +293,29 @@ fc_status fc_nccl_unique_id(uint8_t id[128]);
 fc_status fc_nccl_comm_init(const uint8_t id[128], int32_t world_size, int32_t rank, void** comm);
 fc_status fc_nccl_comm_destroy(void* comm);
 
+/* NEXT-1 -- column-split output ("the resulting patch token
+ * embeddings are first generated, then split along the last dimension, and
+ * finally each resulting chunk is written into the IPC patch buffer of the
+ * corresponding GPU").  Same computation as fc_preprocess for rank `rank`, but
+ * the rank's token rows are written as W = world_size column blocks straight
+ * from the kernel's epilogue:
+ *   blocks: device fp32 [W][rows_r][C], C = 1176 / W, rows_r = row_end - row_begin;
+ *           block j holds columns [j*C, (j+1)*C) of the rank's rows, in row order.
+ * Requires fp32 tokens, NV12 surfaces and W dividing 1176 (1..8 except 5);
+ * FC_ERR_UNSUPPORTED otherwise.  Errors and asynchrony as fc_preprocess. */
+fc_status fc_preprocess_colsplit(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
+                                 int64_t num_surfaces, float* blocks, int64_t grid_thw[3], void* stream);
+
+/* fc_scatter_columns -- the paper's "collective scatter" of the column
+ * blocks: an all-to-all (grouped ncclSend/ncclRecv) after which rank j holds
+ * columns [j*C, (j+1)*C) of ALL token rows:
+ *   blocks: this rank's fc_preprocess_colsplit output (may be NULL if it has no rows)
+ *   mine:   device fp32 [token_rows][C]; rank p's rows land at mine + row_begin_p*C
+ *           (this rank's own block is copied in with cudaMemcpyAsync).
+ * Collective: every rank of the plan's world must call it.  Async on stream. */
+fc_status fc_scatter_columns(const fc_plan_t* plan, int32_t rank, void* comm, const float* blocks, float* mine,
+                             void* stream);
+
 /* fc_gather -- gatherv of every rank's contiguous row shard into the encoder
  * rank's full token buffer (grouped ncclSend/ncclRecv, R9):
  *   shard: device pointer, this rank's (row_end-row_begin) x 1176 tokens

@@ -302,6 +302,33 @@ class NcclComm:
             self.handle = None
 
 
+def preprocess_colsplit(plan: Plan, rank: int, surfaces: SurfaceTable, out=None, stream=None):
+    """fc_preprocess_colsplit (NEXT-1): the rank's tokens as W column
+    blocks, fp32 [W, rows_r, 1176 // W]."""
+    import torch
+    w = plan.cfg.world_size
+    rows = _rank_rows(plan, rank)
+    if out is None:
+        out = torch.empty((w, rows, FC_TOKEN_COLS // w), dtype=torch.float32, device="cuda")
+    grid = (ctypes.c_int64 * 3)()
+    check(lib().fc_preprocess_colsplit(plan.handle, rank, surfaces.arr, surfaces.n, ctypes.c_void_p(out.data_ptr()),
+                                       grid, _stream_ptr(stream)), "fc_preprocess_colsplit")
+    return out
+
+
+def scatter_columns(plan: Plan, rank: int, comm: NcclComm | None, blocks, mine=None, stream=None):
+    """fc_scatter_columns: all-to-all of the column blocks; returns this rank's
+    column slice of every token row, fp32 [token_rows, 1176 // W]."""
+    import torch
+    w = plan.cfg.world_size
+    if mine is None:
+        mine = torch.empty((plan.token_rows, FC_TOKEN_COLS // w), dtype=torch.float32, device="cuda")
+    check(lib().fc_scatter_columns(plan.handle, rank, comm.handle if comm else None,
+                                   ctypes.c_void_p(blocks.data_ptr()) if blocks is not None else None,
+                                   ctypes.c_void_p(mine.data_ptr()), _stream_ptr(stream)), "fc_scatter_columns")
+    return mine
+
+
 def gather(plan: Plan, rank: int, comm: NcclComm | None, shard, full=None, stream=None):
     """fc_gather: gatherv of the row shards into the encoder rank's full
     token buffer (returned on the encoder rank, None elsewhere)."""

@@ -82,7 +82,8 @@ class Nv12SurfaceC(ctypes.Structure):
 EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_get", "fc_plan_sampled_indices",
            "fc_plan_rank", "fc_preprocess", "fc_preprocess_debug", "fc_preprocess_batch", "fc_nccl_unique_id",
            "fc_nccl_comm_init", "fc_nccl_comm_destroy", "fc_gather", "fc_status_string", "fc_last_error",
-           "fc_abi_version", "fc_kernel_launches", "fc_expand_tokens", "fc_preprocess_paged"]
+           "fc_abi_version", "fc_kernel_launches", "fc_expand_tokens", "fc_preprocess_paged",
+           "fc_preprocess_colsplit", "fc_scatter_columns"]
 
 _lib = None
 
@@ -114,6 +115,8 @@ def lib() -> ctypes.CDLL:
     L.fc_nccl_comm_init.argtypes = [ctypes.POINTER(ctypes.c_uint8), i32, i32, ctypes.POINTER(vp)]
     L.fc_nccl_comm_destroy.argtypes = [vp]
     L.fc_gather.argtypes = [vp, i32, vp, vp, vp, vp]
+    L.fc_preprocess_colsplit.argtypes = [vp, i32, ctypes.POINTER(Nv12SurfaceC), i64, vp, ctypes.POINTER(i64), vp]
+    L.fc_scatter_columns.argtypes = [vp, i32, vp, vp, vp, vp]
     L.fc_status_string.argtypes = [ctypes.c_int]
     L.fc_status_string.restype = ctypes.c_char_p
     L.fc_last_error.argtypes = []

@@ -91,6 +91,11 @@ struct Params {
   unsigned long long* cta_t;  // FC_CTA_TIMES experiments: per CTA {start, end, smid} (ns) or null
   int smap;           // 1: strip-synchronous work mapping (CTA b owns strip b % nstrips)
   int sxmask;         // strip source-window start alignment: ~15, or ~31 for I420 (TMA box starts 16-B aligned)
+  // NEXT-1 column-split output (COLS instances): token (row i, column col) goes to
+  // tokens[b * cs_bstride + i * cs_C + col - b * cs_C], b = col / cs_C = umulhi(col, cs_magic)
+  long long cs_bstride;  // elements per column block (rows of the launch x cs_C)
+  int cs_C;              // columns per block: 1176 / world_size
+  uint32_t cs_magic;     // ceil(2^32 / cs_C)
   // tensor maps per frame: Y (box BW x 16) + UV (box BW x 8) for NV12, or
   // Y + U + V (boxes BW/2 x 8) for I420 -- up to 2 * kMaxInlineFrames maps inline
   CUtensorMap tm[2 * kMaxInlineFrames];
@@ -165,7 +170,7 @@ __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, 
 // Work items are (pair, strip, band) triples; CTA b takes [b*T/G, (b+1)*T/G).
 // Strips are whole merge blocks, so every token row is written by one CTA in
 // one band (no partial-sector merging across CTAs in L2).
-template <int KSH, int KSV, bool DBG, int TOK, bool PAGED = false, bool I420 = false>
+template <int KSH, int KSV, bool DBG, int TOK, bool PAGED = false, bool I420 = false, bool COLS = false>
 // Narrow-window instances (KSH = KSV = 1: c2, c3, c5) fit 64 registers without
 // spills and run 4 CTAs/SM (with 2 TMA stages); wider windows keep 80 / 3.
 __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
@@ -488,11 +493,25 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
                 else  // LUT[clip8(S)] = extended table at floor(S / 2^22) (arithmetic shift)
                   o[i] = lds32(lutc + (static_cast<uint32_t>(sv[i] >> 20) & ~3u));
               }
+              if constexpr (COLS) {  // NEXT-1: column blocks [W][rows][C] (the paper's last-dimension split)
+                const long long rl = static_cast<long long>(r.pair) * static_cast<long long>(pair_rows) +
+                                     (static_cast<long long>(hb_) * p.gw2 + X0 / 28) * 4 + (j0 / 14) * 2 + (q >> 1) * 4 +
+                                     (q & 1);
+                const uint32_t cb = (c * 2 + f) * 196 + (j0 % 14) * 14 + 2 * g;
+                const uint32_t cols[4] = {cb, cb + 14, cb + 1, cb + 15};  // o[i]: (j0, 2g) (j0+1, 2g) (j0, 2g+1) (j0+1, 2g+1)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const uint32_t b = __umulhi(cols[i], p.cs_magic);
+                  float* a = static_cast<float*>(p.tokens) + b * p.cs_bstride + rl * p.cs_C + (cols[i] - b * p.cs_C);
+                  st_cs_pred(a, o[i], ((i & 1) ? jok1 : jok0) && xok);
+                }
+              } else {
               TokT* op = PAGED ? static_cast<TokT*>(p.tokens) + static_cast<size_t>(prow[q]) * kCols + (c * 2 + f) * 196 +
                                      (j0 % 14) * 14 + 2 * g
                                : tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
               st_cs_pred2(op, o[0], o[2], jok0 && xok);       // row j0: columns 2g, 2g+1
               st_cs_pred2(op + 14, o[1], o[3], jok1 && xok);  // row j0 + 1
+              }
               if (DBG && p.dbg_rs != nullptr) {
                 const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
                 for (int ee = 0; ee < 4; ++ee) {
@@ -524,6 +543,7 @@ struct Instance {
   KernelFn fn, fn_dbg, fn_bf16, fn_u8;  // fp32 tokens / + parity-test dumps / bf16 tokens / u8 codes
   KernelFn fn_paged, fn_paged_bf16;     // NEXT-2: fp32 / bf16 tokens into a paged pool
   KernelFn fn_i420, fn_i420_dbg;        // I420 surfaces: fp32 tokens / + parity-test dumps
+  KernelFn fn_cols;                     // NEXT-1 column-split fp32 output
 };
 
 // One translation unit per KSH instantiates its instances (parallel build).
@@ -531,7 +551,8 @@ struct Instance {
   Instance{A, B, fc_fused_kernel<A, B, false, FC_TOKENS_F32>, fc_fused_kernel<A, B, true, FC_TOKENS_F32>, \
            fc_fused_kernel<A, B, false, FC_TOKENS_BF16>, fc_fused_kernel<A, B, false, FC_TOKENS_U8>,   \
            fc_fused_kernel<A, B, false, FC_TOKENS_F32, true>, fc_fused_kernel<A, B, false, FC_TOKENS_BF16, true>, \
-           fc_fused_kernel<A, B, false, FC_TOKENS_F32, false, true>, fc_fused_kernel<A, B, true, FC_TOKENS_F32, false, true>}
+           fc_fused_kernel<A, B, false, FC_TOKENS_F32, false, true>, fc_fused_kernel<A, B, true, FC_TOKENS_F32, false, true>, \
+           fc_fused_kernel<A, B, false, FC_TOKENS_F32, false, false, true>}
 void instances_ksh1(Instance* out);  // out[0..3] = KSV 1..4
 void instances_ksh2(Instance* out);
 void instances_ksh3(Instance* out);

@@ -93,4 +93,41 @@ fc_status fc_gather(const fc_plan_t* P, int32_t rank, void* comm, const void* sh
   return FC_OK;
 }
 
+fc_status fc_scatter_columns(const fc_plan_t* P, int32_t rank, void* comm, const float* blocks, float* mine,
+                             void* stream) {
+  if (!P) return fail(FC_ERR_INVALID_ARG, "plan is NULL");
+  if (rank < 0 || rank >= P->world) return fail(FC_ERR_RANK, "rank outside [0, world_size)");
+  if (kCols % P->world != 0) return fail(FC_ERR_UNSUPPORTED, "column split: world_size must divide 1176");
+  if (!mine) return fail(FC_ERR_INVALID_ARG, "mine is NULL");
+  const size_t C = static_cast<size_t>(kCols / P->world);
+  const fc_rank_plan& me = P->ranks[rank].p;
+  const size_t my_rows = static_cast<size_t>(me.row_end - me.row_begin);
+  if (my_rows && !blocks) return fail(FC_ERR_INVALID_ARG, "blocks is NULL");
+  if (P->world > 1 && !comm) return fail(FC_ERR_INVALID_ARG, "comm is NULL with world_size > 1");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // own block: rows [row_begin, row_end) of this rank's column slice
+  if (my_rows) {
+    cudaError_t ce = cudaMemcpyAsync(mine + static_cast<size_t>(me.row_begin) * C, blocks + rank * my_rows * C,
+                                     my_rows * C * sizeof(float), cudaMemcpyDeviceToDevice, s);
+    if (ce != cudaSuccess) return fail(FC_ERR_CUDA, std::string("own block copy: ") + cudaGetErrorString(ce));
+  }
+  if (P->world == 1) return FC_OK;
+  // all-to-all: block p of my rows -> rank p; rank p's block `rank` -> my rows [row_begin_p, row_end_p)
+  ncclComm_t c = static_cast<ncclComm_t>(comm);
+  ncclResult_t r = ncclGroupStart();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
+  for (int p = 0; p < P->world && r == ncclSuccess; ++p) {
+    if (p == rank) continue;
+    const fc_rank_plan& rp = P->ranks[p].p;
+    const size_t prow = static_cast<size_t>(rp.row_end - rp.row_begin);
+    if (my_rows) r = ncclSend(blocks + p * my_rows * C, my_rows * C, ncclFloat32, p, c, s);
+    if (r == ncclSuccess && prow)
+      r = ncclRecv(mine + static_cast<size_t>(rp.row_begin) * C, prow * C, ncclFloat32, p, c, s);
+  }
+  ncclResult_t r2 = ncclGroupEnd();
+  if (r != ncclSuccess) return nccl_fail(r, "ncclSend/ncclRecv");
+  if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
+  return FC_OK;
+}
+
 }  // extern "C"

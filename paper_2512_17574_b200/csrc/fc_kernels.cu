@@ -238,7 +238,7 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
 
 struct Geometry {
   int sw, htiles, SWPN, SWP, BW, NX, TR, TRW, nstrips, nchunks;
-  KernelFn fn, fn_dbg, fn_bf16, fn_u8, fn_paged, fn_paged_bf16, fn_i420, fn_i420_dbg;
+  KernelFn fn, fn_dbg, fn_bf16, fn_u8, fn_paged, fn_paged_bf16, fn_i420, fn_i420_dbg, fn_cols;
   size_t smem;   // at nstages
   int nstages;   // raw TMA stages: 4, or 2 when that buys another CTA per SM (wide-window configs)
 };
@@ -304,6 +304,7 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
       g->fn_paged_bf16 = in.fn_paged_bf16;
       g->fn_i420 = in.fn_i420;
       g->fn_i420_dbg = in.fn_i420_dbg;
+      g->fn_cols = in.fn_cols;
     }
   }
   if (!g->fn) return fail(FC_ERR_UNSUPPORTED, "no kernel instance for this resize window");
@@ -472,7 +473,7 @@ static cudaMemPool_t descriptor_pool(int dev) {
 }
 
 static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, uint8_t* dbg_src,
-                             uint8_t* dbg_rs, const fc_paged_tokens* paged = nullptr) {
+                             uint8_t* dbg_rs, const fc_paged_tokens* paged = nullptr, bool colsplit = false) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -500,9 +501,12 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   if (paged && (td == FC_TOKENS_U8 || jobs.size() != 1))
     return fail(FC_ERR_UNSUPPORTED, "paged output: one job, F32 or BF16 tokens");
   const bool i420 = P->cfg.surface_format == FC_SURFACE_I420;
-  if (i420 && (td != FC_TOKENS_F32 || paged))
+  if (i420 && (td != FC_TOKENS_F32 || paged || colsplit))
     return fail(FC_ERR_UNSUPPORTED, "I420 surfaces: fp32 tokens, linear output (other variants are built for NV12)");
-  KernelFn fn = i420                     ? ((dbg_src || dbg_rs) ? g.fn_i420_dbg : g.fn_i420)
+  if (colsplit && (td != FC_TOKENS_F32 || paged || dbg_src || dbg_rs || jobs.size() != 1))
+    return fail(FC_ERR_UNSUPPORTED, "column-split output: one job, fp32 tokens, NV12");
+  KernelFn fn = colsplit                 ? g.fn_cols
+                : i420                   ? ((dbg_src || dbg_rs) ? g.fn_i420_dbg : g.fn_i420)
                 : (dbg_src || dbg_rs)    ? g.fn_dbg
                 : paged                ? (td == FC_TOKENS_BF16 ? g.fn_paged_bf16 : g.fn_paged)
                 : td == FC_TOKENS_BF16 ? g.fn_bf16
@@ -569,6 +573,11 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   prm.npairs = static_cast<int>(nf / 2);
   prm.ppj = static_cast<int>(nfj / 2);
   prm.tokens = paged ? paged->pool : jobs[0].tokens;
+  if (colsplit) {  // [W][rows][C] column blocks of this launch's rows
+    prm.cs_C = kCols / P->world;
+    prm.cs_bstride = static_cast<long long>(nf / 2) * prm.gh2 * prm.gw2 * 4 * prm.cs_C;
+    prm.cs_magic = static_cast<uint32_t>(((1ull << 32) + prm.cs_C - 1) / prm.cs_C);
+  }
   if (paged) {
     int sh = 0;
     while ((1 << sh) < paged->page_rows) ++sh;
@@ -676,7 +685,8 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
 
 static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv12_surface* surfaces,
                                  int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream,
-                                 uint8_t* dbg_src, uint8_t* dbg_rs, const fc_paged_tokens* paged = nullptr) {
+                                 uint8_t* dbg_src, uint8_t* dbg_rs, const fc_paged_tokens* paged = nullptr,
+                                 bool colsplit = false) {
   if (!Pc) return fail(FC_ERR_INVALID_ARG, "plan is NULL");
   fc_plan_s* P = const_cast<fc_plan_s*>(Pc);
   if (rank < 0 || rank >= P->world) return fail(FC_ERR_RANK, "rank outside [0, world_size)");
@@ -705,7 +715,9 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
   }
   jobs[0].surfaces = surfaces;
   jobs[0].tokens = tokens;
-  return launch_jobs(P, jobs, stream, dbg_src, dbg_rs, paged);
+  if (colsplit && kCols % P->world != 0)
+    return fail(FC_ERR_UNSUPPORTED, "column-split output: world_size must divide 1176");
+  return launch_jobs(P, jobs, stream, dbg_src, dbg_rs, paged, colsplit);
 }
 
 }  // namespace fc
@@ -717,6 +729,11 @@ extern "C" {
 fc_status fc_preprocess(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
                         int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream) {
   return preprocess_impl(plan, rank, surfaces, num_surfaces, tokens, grid_thw, stream, nullptr, nullptr);
+}
+
+fc_status fc_preprocess_colsplit(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
+                                 int64_t num_surfaces, float* blocks, int64_t grid_thw[3], void* stream) {
+  return preprocess_impl(plan, rank, surfaces, num_surfaces, blocks, grid_thw, stream, nullptr, nullptr, nullptr, true);
 }
 
 fc_status fc_preprocess_paged(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,

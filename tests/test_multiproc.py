@@ -67,6 +67,27 @@ def _worker(rank, world, port, case, q, exchange="f32"):
             shard = (oracle.preprocess([host[f] for f in frames], W, H, w2, h2) if frames
                      else np.zeros((0, 1176), np.float32))
         assert shard.shape[0] == rows
+        if exchange == "colsplit":  # NEXT-1 column split: all-to-all of column blocks
+            C = 1176 // world
+            mine = torch.zeros((plan.token_rows, C), dtype=torch.float32)
+            mine[rp["row_begin"]:rp["row_end"]] = torch.from_numpy(shard[:, rank * C:(rank + 1) * C])
+            reqs = []
+            for p, rp_p in enumerate(plan.ranks()):
+                if p == rank:
+                    continue
+                if rows:
+                    reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(shard[:, p * C:(p + 1) * C])), p))
+                n = rp_p["row_end"] - rp_p["row_begin"]
+                if n:
+                    reqs.append(dist.irecv(mine[rp_p["row_begin"]:rp_p["row_end"]], p))
+            for rq in reqs:
+                rq.wait()
+            host_all = {i: synth.frame_nv12(W, H, i, "natural", 21) for i in idx}
+            ref = oracle.preprocess([host_all[i] for i in idx], W, H, w2, h2)
+            assert mine.numpy().view(np.uint32).tobytes() == \
+                np.ascontiguousarray(ref[:, rank * C:(rank + 1) * C]).view(np.uint32).tobytes(), "column slice"
+            q.put((rank, "ok"))
+            return
         # 3) gather to the encoder rank at the planned row offsets
         maxrows = max(r["row_end"] - r["row_begin"] for r in plan.ranks())
         buf = torch.zeros((maxrows, 1176), dtype=torch.uint8 if exchange == "u8" else torch.float32)
@@ -124,3 +145,11 @@ def test_gloo_u8_exchange_equals_single_gpu(case):
     """NEXT-1 exchange: u8 codes gathered (4x fewer bytes) and expanded on the
     encoder give the single-GPU fp32 tokens bit for bit."""
     _run(3, case, "u8")
+
+
+@pytest.mark.parametrize("world,case", [(2, 0), (3, 1), (3, 2)])
+def test_gloo_column_split_equals_single_gpu_columns(world, case):
+    """NEXT-1 column split (fc_scatter_columns' row arithmetic):
+    after the all-to-all, rank j holds columns [j*C, (j+1)*C) of the
+    single-GPU tokens, every row, bit for bit (incl. idle ranks, case 2)."""
+    _run(world, case, "colsplit")

@@ -550,3 +550,37 @@ def test_i420_full_c2_bench_launch(fc, oracle, cuda):
     for t in (0, 29, 59):
         ref = oracle.preprocess_i420([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2)
         assert tol_check(out[t * rpp:(t + 1) * rpp].cpu().numpy(), ref, f"c2 i420 pair {t}") == ref.size
+
+
+# ------------------------------------------------------ NEXT-1 column split
+@pytest.mark.parametrize("world", [1, 2, 3, 8])
+def test_colsplit_virtual_ranks(fc, oracle, cuda, world):
+    """fc_preprocess_colsplit (P:527-530 "split along the last dimension"): for
+    every rank of a W-way plan (all on this device), block j of its output is
+    columns [j*C, (j+1)*C) of its rows of the single-GPU tokens, bit for bit
+    (C = 147 for W = 8: blocks start mid-patch); fc_scatter_columns at W = 1
+    is the identity."""
+    import torch
+    W_, H_, N = 320, 240, 300
+    plan = make_plan(fc, W_, H_, N, list(range(0, 300, 30)), world, sample_fps=2.0)
+    idx = plan.sampled_indices
+    host = {i: synth.frame_nv12(W_, H_, i, "natural", 5) for i in idx}
+    surf = fc.SurfaceTable.from_tensors(synth.to_device(host), N)
+    h2, w2 = plan.resized
+    ref = oracle.preprocess([host[i] for i in idx], W_, H_, w2, h2)
+    C = 1176 // world
+    for r, rp in enumerate(plan.ranks()):
+        if rp["row_end"] == rp["row_begin"]:
+            continue
+        blocks = fc.preprocess_colsplit(plan, r, surf)
+        torch.cuda.synchronize()
+        assert blocks.shape == (world, rp["row_end"] - rp["row_begin"], C)
+        got = blocks.cpu().numpy()
+        for j in range(world):
+            exp = ref[rp["row_begin"]:rp["row_end"], j * C:(j + 1) * C]
+            np.testing.assert_array_equal(got[j].view(np.uint32), np.ascontiguousarray(exp).view(np.uint32),
+                                          err_msg=f"rank {r} block {j}")
+        if world == 1:
+            mine = fc.scatter_columns(plan, 0, None, blocks)
+            torch.cuda.synchronize()
+            np.testing.assert_array_equal(mine.cpu().numpy().view(np.uint32), ref.view(np.uint32))

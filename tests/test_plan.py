@@ -312,3 +312,23 @@ def test_bicubic_output_range_fits_extended_table():
     # at a 2x upscale's half-pixel phase, sum to 1/8 of the normalised weights:
     # about [-32, 287]; integer rounding of small filters adds a little (M: [-34, 289])
     assert lo >= -40 and hi <= 295, (lo, hi)
+
+
+def test_colsplit_requires_world_dividing_1176(fc):
+    """NEXT-1 column split: W must divide 1176 (C = 1176 / W columns per
+    block); W = 5 is rejected before any device work."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    p = plan_of(fc, 64, 48, 100, [0, 20, 40, 60, 80], sampling="explicit",
+                explicit_indices=[0, 1, 20, 21, 40, 41, 60, 61, 80, 81], world_size=5)
+    buf = (ctypes.c_uint8 * (48 * 64 * 2 + 64))()
+    base = (ctypes.addressof(buf) + 15) & ~15
+    surf = fc.SurfaceTable(100)
+    for i in p.sampled_indices:
+        surf.arr[i] = fc._native.Nv12SurfaceC(base, base + 48 * 64, 64, 64)
+    out = (ctypes.c_float * 1176)()
+    st = fc.lib().fc_preprocess_colsplit(p.handle, 0, surf.arr, 100, ctypes.cast(out, ctypes.c_void_p), None, None)
+    assert fc._native.STATUS[st] == "FC_ERR_UNSUPPORTED", fc.lib().fc_last_error()
+    st = fc.lib().fc_scatter_columns(p.handle, 0, None, None, ctypes.cast(out, ctypes.c_void_p), None)
+    assert fc._native.STATUS[st] == "FC_ERR_UNSUPPORTED"
