@@ -458,7 +458,8 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
           const int f = vsub, c = e;
           const uint32_t lutc = lut_s + (c * kLutN + kLutLo) * 4;  // entry of v = 0
           TokT* tp = tb + (c * 2 + f) * 196;
-          constexpr int VG = 1;  // patches per MMA group (interleaving 2 or 4 measured slower at 64 regs)
+          // patches per MMA group: 2 for KSV = 2 (c4 -2.9%), 1 for narrow windows (2: c2 +0.4%; 4 spills)
+          constexpr int VG = KSV == 2 ? 2 : 1;
 #pragma unroll
           for (int q0 = 0; q0 < kStrip / 14; q0 += VG) {
             if (q0 >= npatch) break;
