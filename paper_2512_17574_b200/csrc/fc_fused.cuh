@@ -246,14 +246,18 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
   const uint32_t lut_s = smem_u32(lut);
   // V-pass role: row group vjg, planes [kPlanesPerWarp*vsub, +kPlanesPerWarp)
   const int vjg = warp & 3, vsub = warp >> 2;
-  const int j0 = 8 * vjg + 2 * tq;                 // output rows j0, j0+1 of the band
-  const bool jok0 = j0 < 28, jok1 = j0 + 1 < 28;   // group 3 covers rows 24..31
+  // MMA N columns 2t / 2t+1 are output rows t / t+4 of the 8-row group (the host
+  // orders the V weights so), so each LUT load of a warp reads a compact 4-row
+  // footprint: fewer distinct values per bank, fewer shared-memory conflicts
+  const int j0 = 8 * vjg + tq, j1 = j0 + 4;        // this thread's output rows of the band
+  const bool jok0 = j0 < 28, jok1 = j1 < 28;       // group 3 covers rows 24..31
   // V-pass MMA rows g / g+8 are patch columns 2g / 2g+1: one LDS.64 loads both
   // A words (adjacent ring columns) and one 8-byte store writes both outputs
   const bool xok = g < 7;                          // columns 2g, 2g+1 inside the 14-wide patch
   // token offset of (row j, patch column 0) within a band's token block (R6):
   // row part hm*2*1176 + ph*14
   const int jo0 = (j0 / 14) * 2 * kCols + (j0 % 14) * 14;
+  const int djo = (j1 / 14) * 2 * kCols + (j1 % 14) * 14 - jo0;  // row j1 relative to row j0 (other half at 14)
 
   uint32_t seq = 0;
   Run r;
@@ -440,16 +444,19 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
         TokT* tb = tpair + (static_cast<size_t>(hb_) * p.gw2 + X0 / 28) * 4 * kCols + jo0 + 2 * g;
         // paged output: the pool row of each patch's token row (merge block q/2,
         // sub-block q&1, this thread's half hm = j0/14) -- SPEC write_chunk mapping
-        uint32_t prow[4];
+        uint32_t prow[2][4];  // [row j0 / j1][patch]
         if constexpr (PAGED) {
-          const long long row0 = static_cast<long long>(r.pair) * static_cast<long long>(pair_rows) +
-                                 (static_cast<long long>(hb_) * p.gw2 + X0 / 28) * 4 + (j0 / 14) * 2;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const long long sl = p.page_first + row0 + (q >> 1) * 4 + (q & 1);
-            prow[q] = q < npatch ? static_cast<uint32_t>(__ldg(p.page_ids + (sl >> p.page_shift))) * p.page_rows +
-                                       static_cast<uint32_t>(sl & p.page_mask)
-                                 : 0u;
+          for (int h = 0; h < 2; ++h) {
+            const long long row0 = static_cast<long long>(r.pair) * static_cast<long long>(pair_rows) +
+                                   (static_cast<long long>(hb_) * p.gw2 + X0 / 28) * 4 + ((h ? j1 : j0) / 14) * 2;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const long long sl = p.page_first + row0 + (q >> 1) * 4 + (q & 1);
+              prow[h][q] = q < npatch ? static_cast<uint32_t>(__ldg(p.page_ids + (sl >> p.page_shift))) * p.page_rows +
+                                            static_cast<uint32_t>(sl & p.page_mask)
+                                      : 0u;
+            }
           }
         }
 #pragma unroll
@@ -483,7 +490,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
             for (int e2 = 0; e2 < VG; ++e2) {
               const int q = q0 + e2;
               if (q >= npatch) break;
-              // d0,d1: column 2g, rows j0, j0+1; d2,d3: column 2g+1
+              // d0,d1: column 2g, rows j0, j1; d2,d3: column 2g+1
               int sv[4];
               uint32_t o[4];
 #pragma unroll
@@ -495,28 +502,32 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
                   o[i] = lds32(lutc + (static_cast<uint32_t>(sv[i] >> 20) & ~3u));
               }
               if constexpr (COLS) {  // NEXT-1: column blocks [W][rows][C] (the paper's last-dimension split)
-                const long long rl = static_cast<long long>(r.pair) * static_cast<long long>(pair_rows) +
-                                     (static_cast<long long>(hb_) * p.gw2 + X0 / 28) * 4 + (j0 / 14) * 2 + (q >> 1) * 4 +
-                                     (q & 1);
-                const uint32_t cb = (c * 2 + f) * 196 + (j0 % 14) * 14 + 2 * g;
-                const uint32_t cols[4] = {cb, cb + 14, cb + 1, cb + 15};  // o[i]: (j0, 2g) (j0+1, 2g) (j0, 2g+1) (j0+1, 2g+1)
+                const long long rq = static_cast<long long>(r.pair) * static_cast<long long>(pair_rows) +
+                                     (static_cast<long long>(hb_) * p.gw2 + X0 / 28) * 4 + (q >> 1) * 4 + (q & 1);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                  const uint32_t b = __umulhi(cols[i], p.cs_magic);
-                  float* a = static_cast<float*>(p.tokens) + b * p.cs_bstride + rl * p.cs_C + (cols[i] - b * p.cs_C);
+                for (int i = 0; i < 4; ++i) {  // o[i]: (j0, 2g) (j1, 2g) (j0, 2g+1) (j1, 2g+1)
+                  const int j = (i & 1) ? j1 : j0;
+                  const long long rl = rq + (j / 14) * 2;
+                  const uint32_t col = (c * 2 + f) * 196 + (j % 14) * 14 + 2 * g + (i >> 1);
+                  const uint32_t b = __umulhi(col, p.cs_magic);
+                  float* a = static_cast<float*>(p.tokens) + b * p.cs_bstride + rl * p.cs_C + (col - b * p.cs_C);
                   st_cs_pred(a, o[i], ((i & 1) ? jok1 : jok0) && xok);
                 }
               } else {
-              TokT* op = PAGED ? static_cast<TokT*>(p.tokens) + static_cast<size_t>(prow[q]) * kCols + (c * 2 + f) * 196 +
-                                     (j0 % 14) * 14 + 2 * g
-                               : tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
-              st_cs_pred2(op, o[0], o[2], jok0 && xok);       // row j0: columns 2g, 2g+1
-              st_cs_pred2(op + 14, o[1], o[3], jok1 && xok);  // row j0 + 1
+              if constexpr (PAGED) {
+                TokT* pb = static_cast<TokT*>(p.tokens) + (c * 2 + f) * 196 + 2 * g;
+                st_cs_pred2(pb + static_cast<size_t>(prow[0][q]) * kCols + (j0 % 14) * 14, o[0], o[2], jok0 && xok);
+                st_cs_pred2(pb + static_cast<size_t>(prow[1][q]) * kCols + (j1 % 14) * 14, o[1], o[3], jok1 && xok);
+              } else {
+                TokT* op = tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
+                st_cs_pred2(op, o[0], o[2], jok0 && xok);        // row j0: columns 2g, 2g+1
+                st_cs_pred2(op + djo, o[1], o[3], jok1 && xok);  // row j1
+              }
               }
               if (DBG && p.dbg_rs != nullptr) {
                 const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
                 for (int ee = 0; ee < 4; ++ee) {
-                  const int x = X0 + 14 * q + 2 * g + ((ee >= 2) ? 1 : 0), j = j0 + (ee & 1);
+                  const int x = X0 + 14 * q + 2 * g + ((ee >= 2) ? 1 : 0), j = (ee & 1) ? j1 : j0;
                   if (xok && x < p.W2 && j < 28)
                     p.dbg_rs[((fi * p.H2 + yo0 + j) * p.W2 + x) * 3 + c] =
                         static_cast<uint32_t>(add_min_relu(sv[ee], 0, (1 << 30) - 1)) >> 22;

@@ -115,9 +115,14 @@ static void build_mma_tables(const fc_plan_s* P, int sw, MmaTables* m) {
       outs[g] = (8 * i + g < sw && o < th.out) ? o : -1;
     }
   };
+  // V groups: MMA N column n is output row pi(n) of the 8-row group, pi(2t) = t,
+  // pi(2t+1) = t + 4 (the kernel's j0 / j1: compact 4-row LUT footprints)
   auto v_outs = [&](int grp, int (&outs)[8]) {
     const int hb = grp / 4, gi = grp % 4;
-    for (int g = 0; g < 8; ++g) outs[g] = (8 * gi + g < 28) ? 28 * hb + 8 * gi + g : -1;
+    for (int n = 0; n < 8; ++n) {
+      const int row = 8 * gi + (n >> 1) + 4 * (n & 1);
+      outs[n] = row < 28 ? 28 * hb + row : -1;
+    }
   };
   int ksh = 1, ksv = 1;
   for (int tt = 0; tt < nth; ++tt) {
