@@ -157,13 +157,15 @@ __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, 
       }
 }
 
-// Persistent fused kernel, 8 warps, 3 CTAs/SM.  Per 16-row chunk:
-//   lane 0 of warp 7 refills the raw stage just converted with the chunk 4
-//       ahead (2-D TMA, mbarrier expect_tx) beside the H pass;
+// Persistent fused kernel, 8 warps, 4 CTAs/SM (narrow windows) or 2-3.  Per
+// 16-row chunk:
+//   lane 0 of warp 7 refills the raw stage just converted with the chunk
+//       nstages ahead (2-D TMA, mbarrier expect_tx) beside the H pass;
 //   all warps: a5 colour (dp2a) -> RGB planes; barrier;
 //   warps 0..6: a6 horizontal pass, warp w owns output tile w (8 columns) of
-//       the strip; three byte-plane MMAs per 16 rows x 8 outputs -> u8 ring
-//       (4 source rows per 32-bit word); barrier.
+//       the strip; three byte-plane MMAs per 16 rows x 8 outputs (MMA rows
+//       g / g+8 = source rows 2g / 2g+1) -> saturating pack -> u8 ring (4
+//       source rows per 32-bit word, one 16-bit store per column pair); barrier.
 // Per band: a7 vertical pass, warp w owns 8-row group (w&3) and the three
 // channels of frame w>>2; one MMA tile per 14-column patch, then a8 table +
 // a9 patch-order stores; barrier.
@@ -280,7 +282,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
           hb[k][pl][1] = __ldg(f + (k * 3 + pl) * 64 + 1);
         }
     }
-    // A-fragment byte addresses in an RGB plane: rows g, g+8; columns xs + 4t (+16)
+    // A-fragment byte addresses in an RGB plane: rows 2g, 2g+1; columns xs + 4t (+16)
     // H-pass MMA rows g / g+8 are source rows 2g / 2g+1 of the chunk, so each
     // thread's two rows of one output column are adjacent bytes of one ring word
     // (SWP = 8 mod 16: rows 2g of the 8 lane groups fall in distinct bank quads)
