@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
-              *os.environ.get("FC_NVCC_DEFS", "").split(),  # A/B experiments only (e.g. -DFC_NO_I420)
+              *os.environ.get("FC_NVCC_DEFS", "").split(),  # extra -D flags for A/B experiment builds only
               "-I", INCLUDE, "-I", CSRC, "-I", inc]
     cmds, objs = [], []
     for src in SOURCES:
