@@ -38,8 +38,9 @@
 extern "C" {
 #endif
 
-#define FC_ABI_VERSION 3  /* 2: token_dtype + color in fc_model_cfg; tokens as void*
-                             3: surface_format in fc_model_cfg, v plane in the surface */
+#define FC_ABI_VERSION 4  /* 2: token_dtype + color in fc_model_cfg; tokens as void*
+                             3: surface_format in fc_model_cfg, v plane in the surface
+                             4: fc_exchange_schedule, fc_last_kernel */
 #define FC_TOKEN_COLS 1176 /* 3 channels * 2 (temporal patch) * 14 * 14 */
 
 typedef enum {
@@ -316,6 +317,27 @@ fc_status fc_preprocess_colsplit(const fc_plan_t* plan, int32_t rank, const fc_n
 fc_status fc_scatter_columns(const fc_plan_t* plan, int32_t rank, void* comm, const float* blocks, float* mine,
                              void* stream);
 
+/* fc_exchange_schedule -- the transfers one rank issues in an exchange step
+ * (a10; reading R9): FC_XCHG_GATHER is what fc_gather runs (row
+ * shards -> the encoder rank's full buffer), FC_XCHG_COLSPLIT what
+ * fc_scatter_columns runs (column blocks, all-to-all).  Both functions execute
+ * exactly this list, so it is the testable form of their offset arithmetic.
+ *   src_offset: byte offset into the rank's send buffer (shard / blocks)
+ *               for FC_XFER_SEND and FC_XFER_LOCAL;
+ *   dst_offset: byte offset into its receive buffer (full / mine) for
+ *               FC_XFER_RECV and FC_XFER_LOCAL;  bytes: length.
+ * out may be NULL (then only *count is written); capacity too small ->
+ * FC_ERR_INVALID_ARG with *count = the size needed.  Host only, no CUDA call. */
+typedef enum { FC_XCHG_GATHER = 0, FC_XCHG_COLSPLIT = 1 } fc_exchange_kind;
+typedef enum { FC_XFER_LOCAL = 0, FC_XFER_SEND = 1, FC_XFER_RECV = 2 } fc_xfer_dir;
+typedef struct {
+  int32_t peer;      /* the other rank (== rank for FC_XFER_LOCAL) */
+  int32_t dir;       /* fc_xfer_dir */
+  int64_t src_offset, dst_offset, bytes;
+} fc_transfer;
+fc_status fc_exchange_schedule(const fc_plan_t* plan, int32_t rank, fc_exchange_kind kind, fc_transfer* out,
+                               int32_t capacity, int32_t* count);
+
 /* fc_gather -- gatherv of every rank's contiguous row shard into the encoder
  * rank's full token buffer (grouped ncclSend/ncclRecv, R9):
  *   shard: device pointer, this rank's (row_end-row_begin) x 1176 tokens
@@ -335,6 +357,14 @@ int32_t fc_abi_version(void);
  * (fused preprocess kernels; NCCL's own kernels and memcpys not included).
  * Monotone; safe to call from any thread; no CUDA call. */
 uint64_t fc_kernel_launches(void);
+
+/* Which fused kernel the calling thread's last successful fc_preprocess*
+ * launch used: FC_KERNEL_TC (the tcgen05 kernel: NV12 surfaces, fp32 tokens,
+ * strip windows up to 255 source columns / 128 source rows per 16 output rows)
+ * or FC_KERNEL_MMA (the mma.sync kernel: every other shape and variant);
+ * FC_KERNEL_NONE before any launch.  Thread-local, no CUDA call. */
+typedef enum { FC_KERNEL_NONE = 0, FC_KERNEL_TC = 1, FC_KERNEL_MMA = 2 } fc_kernel_id;
+int32_t fc_last_kernel(void);
 
 #ifdef __cplusplus
 }

@@ -131,10 +131,22 @@ def sample_indices(num_frames_total: int, fps_src: Fraction | float, sample_fps:
 
 
 # ------------------------------------------------------------- a2 resize --
+def video_max_pixels(min_pixels: int, max_pixels: float, total_pixels: float, n: int, tps: int = TPS) -> float:
+    """Reading R2, optional total budget (qwen-vl-utils'
+    fetch_video): the per-frame budget becomes
+        max(min(max_pixels, total_pixels / n * tps), int(min_pixels * 1.05))
+    kept as f64 (int() truncates; min_pixels * 1.05 > 0)."""
+    return max(min(max_pixels, total_pixels / n * tps), int(min_pixels * 1.05))
+
+
 def smart_resize(height: int, width: int, factor: int = 28, min_pixels: int = 128 * 28 * 28,
-                 max_pixels: int = 768 * 28 * 28) -> tuple[int, int]:
+                 max_pixels: float = 768 * 28 * 28, total_pixels: float = 0.0, n: int = 0) -> tuple[int, int]:
     """Reading R2: HF smart_resize (transformers models/qwen2_vl/
-    image_processing_qwen2_vl.py:62-88), Python round-half-even, f64."""
+    image_processing_qwen2_vl.py:62-88), Python round-half-even, f64.
+    ``total_pixels > 0`` (with the sampled frame count ``n``) first lowers the
+    per-frame budget by :func:`video_max_pixels`."""
+    if total_pixels > 0:
+        max_pixels = video_max_pixels(min_pixels, max_pixels, total_pixels, n)
     if max(height, width) / min(height, width) > 200:
         raise ValueError("aspect ratio > 200")
     h_bar = round(height / factor) * factor

@@ -22,7 +22,7 @@ from ._native import FcError, FC_TOKEN_COLS, check, lib
 
 __all__ = ["VideoMeta", "ModelCfg", "Plan", "SurfaceTable", "preprocess", "preprocess_debug", "preprocess_batch",
            "expand_tokens", "preprocess_paged",
-           "NcclComm", "gather", "FcError", "FC_TOKEN_COLS", "lib"]
+           "NcclComm", "gather", "exchange_schedule", "last_kernel", "FcError", "FC_TOKEN_COLS", "lib"]
 
 
 @dataclass
@@ -327,6 +327,26 @@ def scatter_columns(plan: Plan, rank: int, comm: NcclComm | None, blocks, mine=N
                                    ctypes.c_void_p(blocks.data_ptr()) if blocks is not None else None,
                                    ctypes.c_void_p(mine.data_ptr()), _stream_ptr(stream)), "fc_scatter_columns")
     return mine
+
+
+def exchange_schedule(plan: Plan, rank: int, kind: str = "gather") -> list[dict]:
+    """fc_exchange_schedule: the transfers `rank` issues in fc_gather
+    (kind="gather") or fc_scatter_columns (kind="colsplit"), as dicts
+    {peer, dir ("local" | "send" | "recv"), src_offset, dst_offset, bytes}."""
+    n = ctypes.c_int32()
+    check(lib().fc_exchange_schedule(plan.handle, rank, _native.XCHG[kind], None, 0, ctypes.byref(n)),
+          "fc_exchange_schedule")
+    arr = (_native.TransferC * max(n.value, 1))()
+    check(lib().fc_exchange_schedule(plan.handle, rank, _native.XCHG[kind], arr, n.value, ctypes.byref(n)),
+          "fc_exchange_schedule")
+    return [dict(peer=t.peer, dir=_native.XFER_DIRS[t.dir], src_offset=t.src_offset, dst_offset=t.dst_offset,
+                 bytes=t.bytes) for t in arr[: n.value]]
+
+
+def last_kernel() -> str | None:
+    """fc_last_kernel: "tc" (tcgen05 kernel) or "mma" (mma.sync kernel) for
+    this thread's last fc_preprocess* launch."""
+    return _native.KERNELS[lib().fc_last_kernel()]
 
 
 def gather(plan: Plan, rank: int, comm: NcclComm | None, shard, full=None, stream=None):

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, f"libfc_{os.environ['FC_LIB_VARIANT']}.so" if os.e
                         else "libfc.so")
 
 FC_TOKEN_COLS = 1176
-ABI_VERSION = 3  # include/fc.h FC_ABI_VERSION this binding marshals for
+ABI_VERSION = 4  # include/fc.h FC_ABI_VERSION this binding marshals for
 STATUS = {0: "FC_OK", 1: "FC_ERR_INVALID_ARG", 2: "FC_ERR_EMPTY_SELECTION", 3: "FC_ERR_ASPECT_RATIO",
           4: "FC_ERR_UNSUPPORTED", 5: "FC_ERR_MISSING_SURFACE", 6: "FC_ERR_RANK", 7: "FC_ERR_OOM",
           8: "FC_ERR_CUDA", 9: "FC_ERR_NCCL"}
@@ -74,6 +74,16 @@ class RankPlanC(ctypes.Structure):
                                               "est_decode_frames")]
 
 
+class TransferC(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int32), ("dir", ctypes.c_int32), ("src_offset", ctypes.c_int64),
+                ("dst_offset", ctypes.c_int64), ("bytes", ctypes.c_int64)]
+
+
+XCHG = {"gather": 0, "colsplit": 1}
+XFER_DIRS = {0: "local", 1: "send", 2: "recv"}
+KERNELS = {0: None, 1: "tc", 2: "mma"}
+
+
 class Nv12SurfaceC(ctypes.Structure):
     _fields_ = [("y", ctypes.c_void_p), ("uv", ctypes.c_void_p), ("pitch_y", ctypes.c_int64),
                 ("pitch_uv", ctypes.c_int64), ("v", ctypes.c_void_p)]
@@ -83,7 +93,7 @@ EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_g
            "fc_plan_rank", "fc_preprocess", "fc_preprocess_debug", "fc_preprocess_batch", "fc_nccl_unique_id",
            "fc_nccl_comm_init", "fc_nccl_comm_destroy", "fc_gather", "fc_status_string", "fc_last_error",
            "fc_abi_version", "fc_kernel_launches", "fc_expand_tokens", "fc_preprocess_paged",
-           "fc_preprocess_colsplit", "fc_scatter_columns"]
+           "fc_preprocess_colsplit", "fc_scatter_columns", "fc_exchange_schedule", "fc_last_kernel"]
 
 _lib = None
 
@@ -128,10 +138,13 @@ def lib() -> ctypes.CDLL:
                                       ctypes.POINTER(ctypes.c_int64), vp]
     L.fc_kernel_launches.argtypes = []
     L.fc_kernel_launches.restype = ctypes.c_uint64
+    L.fc_exchange_schedule.argtypes = [vp, i32, ctypes.c_int, ctypes.POINTER(TransferC), i32, ctypes.POINTER(i32)]
+    L.fc_last_kernel.argtypes = []
+    L.fc_last_kernel.restype = ctypes.c_int32
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("fc_model_cfg_default", "fc_plan_destroy", "fc_status_string", "fc_last_error",
-                        "fc_abi_version", "fc_kernel_launches"):
+                        "fc_abi_version", "fc_kernel_launches", "fc_last_kernel"):
             fn.restype = ctypes.c_int
     _lib = L
     return L

@@ -455,9 +455,12 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const long long sl = p.page_first + row0 + (q >> 1) * 4 + (q & 1);
-              prow[h][q] = q < npatch ? static_cast<uint32_t>(__ldg(p.page_ids + (sl >> p.page_shift))) * p.page_rows +
-                                            static_cast<uint32_t>(sl & p.page_mask)
-                                      : 0u;
+              // only rows this thread stores: rows 28..31 of group 3 (jok false) may lie past
+              // the write's last page (page_ids[num_pages] read)
+              const bool live = q < npatch && (h ? jok1 : jok0);
+              prow[h][q] = live ? static_cast<uint32_t>(__ldg(p.page_ids + (sl >> p.page_shift))) * p.page_rows +
+                                      static_cast<uint32_t>(sl & p.page_mask)
+                                : 0u;
             }
           }
         }

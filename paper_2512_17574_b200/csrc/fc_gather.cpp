@@ -8,8 +8,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "fc_internal.h"
 
@@ -50,42 +52,67 @@ fc_status fc_nccl_comm_destroy(void* comm) {
   return FC_OK;
 }
 
-fc_status fc_gather(const fc_plan_t* P, int32_t rank, void* comm, const void* shard, void* full, void* stream) {
+// The transfers of one rank's part of an exchange (R9 gather / NEXT-1 column
+// split), in bytes; fc_gather and fc_scatter_columns execute exactly this list.
+static fc_status schedule(const fc_plan_t* P, int32_t rank, fc_exchange_kind kind, std::vector<fc_transfer>* out) {
+  out->clear();
   if (!P) return fail(FC_ERR_INVALID_ARG, "plan is NULL");
   if (rank < 0 || rank >= P->world) return fail(FC_ERR_RANK, "rank outside [0, world_size)");
-  const int e = P->cfg.encoder_rank;
   const fc_rank_plan& me = P->ranks[rank].p;
-  // rows are exchanged as bytes: 1176 tokens x (4 B fp32 | 2 B bf16 | 1 B u8 code)
-  const int elem = P->cfg.token_dtype == FC_TOKENS_U8 ? 1 : P->cfg.token_dtype == FC_TOKENS_BF16 ? 2 : 4;
-  const size_t row_bytes = static_cast<size_t>(kCols) * elem;
-  const size_t my_bytes = static_cast<size_t>(me.row_end - me.row_begin) * row_bytes;
-  uint8_t* fullb = static_cast<uint8_t*>(full);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (rank == e && !full) return fail(FC_ERR_INVALID_ARG, "encoder rank needs the full buffer");
-  if (my_bytes && !shard) return fail(FC_ERR_INVALID_ARG, "shard is NULL");
-  if (P->world > 1 && !comm) return fail(FC_ERR_INVALID_ARG, "comm is NULL with world_size > 1");
-  if (rank == e && my_bytes) {
-    uint8_t* dst = fullb + static_cast<size_t>(me.row_begin) * row_bytes;
-    if (dst != shard) {
-      cudaError_t ce = cudaMemcpyAsync(dst, shard, my_bytes, cudaMemcpyDeviceToDevice, s);
-      if (ce != cudaSuccess) return fail(FC_ERR_CUDA, std::string("own shard copy: ") + cudaGetErrorString(ce));
+  const int64_t my_rows = me.row_end - me.row_begin;
+  if (kind == FC_XCHG_GATHER) {
+    // rows are exchanged as bytes: 1176 tokens x (4 B fp32 | 2 B bf16 | 1 B u8 code)
+    const int elem = P->cfg.token_dtype == FC_TOKENS_U8 ? 1 : P->cfg.token_dtype == FC_TOKENS_BF16 ? 2 : 4;
+    const int64_t rb = static_cast<int64_t>(kCols) * elem;
+    const int e = P->cfg.encoder_rank;
+    if (rank == e) {
+      if (my_rows) out->push_back({rank, FC_XFER_LOCAL, 0, me.row_begin * rb, my_rows * rb});
+      for (int p = 0; p < P->world; ++p) {
+        const fc_rank_plan& rp = P->ranks[p].p;
+        if (p != e && rp.row_end > rp.row_begin)
+          out->push_back({p, FC_XFER_RECV, 0, rp.row_begin * rb, (rp.row_end - rp.row_begin) * rb});
+      }
+    } else if (my_rows) {
+      out->push_back({e, FC_XFER_SEND, 0, 0, my_rows * rb});
     }
+    return FC_OK;
   }
-  if (P->world == 1) return FC_OK;
+  if (kind != FC_XCHG_COLSPLIT) return fail(FC_ERR_INVALID_ARG, "unknown exchange kind");
+  if (kCols % P->world != 0) return fail(FC_ERR_UNSUPPORTED, "column split: world_size must divide 1176");
+  // blocks [W][my_rows][C] fp32 -> mine [token_rows][C]: block p of my rows goes
+  // to rank p; rank p's block `rank` lands at mine + row_begin_p * C
+  const int64_t cb = static_cast<int64_t>(kCols / P->world) * 4;  // bytes per row of a block
+  if (my_rows) out->push_back({rank, FC_XFER_LOCAL, rank * my_rows * cb, me.row_begin * cb, my_rows * cb});
+  for (int p = 0; p < P->world; ++p) {
+    if (p == rank) continue;
+    const fc_rank_plan& rp = P->ranks[p].p;
+    if (my_rows) out->push_back({p, FC_XFER_SEND, p * my_rows * cb, 0, my_rows * cb});
+    if (rp.row_end > rp.row_begin)
+      out->push_back({p, FC_XFER_RECV, 0, rp.row_begin * cb, (rp.row_end - rp.row_begin) * cb});
+  }
+  return FC_OK;
+}
+
+// Run a schedule: local copies on the stream, sends/receives as one NCCL group.
+static fc_status run_schedule(const std::vector<fc_transfer>& xs, int world, void* comm, const void* src, void* dst,
+                              void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint8_t* sb = static_cast<const uint8_t*>(src);
+  uint8_t* db = static_cast<uint8_t*>(dst);
+  for (const fc_transfer& x : xs)
+    if (x.dir == FC_XFER_LOCAL && db + x.dst_offset != sb + x.src_offset) {
+      cudaError_t ce = cudaMemcpyAsync(db + x.dst_offset, sb + x.src_offset, static_cast<size_t>(x.bytes),
+                                       cudaMemcpyDeviceToDevice, s);
+      if (ce != cudaSuccess) return fail(FC_ERR_CUDA, std::string("local shard copy: ") + cudaGetErrorString(ce));
+    }
+  if (world == 1) return FC_OK;
   ncclComm_t c = static_cast<ncclComm_t>(comm);
   ncclResult_t r = ncclGroupStart();
   if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
-  if (rank == e) {
-    for (int p = 0; p < P->world; ++p) {
-      if (p == e) continue;
-      const fc_rank_plan& rp = P->ranks[p].p;
-      const size_t n = static_cast<size_t>(rp.row_end - rp.row_begin) * row_bytes;
-      if (!n) continue;
-      r = ncclRecv(fullb + static_cast<size_t>(rp.row_begin) * row_bytes, n, ncclUint8, p, c, s);
-      if (r != ncclSuccess) break;
-    }
-  } else if (my_bytes) {
-    r = ncclSend(shard, my_bytes, ncclUint8, e, c, s);
+  for (const fc_transfer& x : xs) {
+    if (x.dir == FC_XFER_SEND) r = ncclSend(sb + x.src_offset, static_cast<size_t>(x.bytes), ncclUint8, x.peer, c, s);
+    if (x.dir == FC_XFER_RECV) r = ncclRecv(db + x.dst_offset, static_cast<size_t>(x.bytes), ncclUint8, x.peer, c, s);
+    if (r != ncclSuccess) break;
   }
   ncclResult_t r2 = ncclGroupEnd();
   if (r != ncclSuccess) return nccl_fail(r, "ncclSend/ncclRecv");
@@ -93,41 +120,40 @@ fc_status fc_gather(const fc_plan_t* P, int32_t rank, void* comm, const void* sh
   return FC_OK;
 }
 
+fc_status fc_exchange_schedule(const fc_plan_t* P, int32_t rank, fc_exchange_kind kind, fc_transfer* out,
+                               int32_t capacity, int32_t* count) {
+  if (!count) return fail(FC_ERR_INVALID_ARG, "count is NULL");
+  std::vector<fc_transfer> xs;
+  const fc_status st = schedule(P, rank, kind, &xs);
+  if (st != FC_OK) return st;
+  *count = static_cast<int32_t>(xs.size());
+  if (static_cast<int32_t>(xs.size()) > capacity || (!out && !xs.empty()))
+    return out ? fail(FC_ERR_INVALID_ARG, "transfer array too short (count holds the size needed)") : FC_OK;
+  std::copy(xs.begin(), xs.end(), out);
+  return FC_OK;
+}
+
+fc_status fc_gather(const fc_plan_t* P, int32_t rank, void* comm, const void* shard, void* full, void* stream) {
+  std::vector<fc_transfer> xs;
+  fc_status st = schedule(P, rank, FC_XCHG_GATHER, &xs);
+  if (st != FC_OK) return st;
+  const fc_rank_plan& me = P->ranks[rank].p;
+  if (rank == P->cfg.encoder_rank && !full) return fail(FC_ERR_INVALID_ARG, "encoder rank needs the full buffer");
+  if (me.row_end > me.row_begin && !shard) return fail(FC_ERR_INVALID_ARG, "shard is NULL");
+  if (P->world > 1 && !comm) return fail(FC_ERR_INVALID_ARG, "comm is NULL with world_size > 1");
+  return run_schedule(xs, P->world, comm, shard, full, stream);
+}
+
 fc_status fc_scatter_columns(const fc_plan_t* P, int32_t rank, void* comm, const float* blocks, float* mine,
                              void* stream) {
-  if (!P) return fail(FC_ERR_INVALID_ARG, "plan is NULL");
-  if (rank < 0 || rank >= P->world) return fail(FC_ERR_RANK, "rank outside [0, world_size)");
-  if (kCols % P->world != 0) return fail(FC_ERR_UNSUPPORTED, "column split: world_size must divide 1176");
+  std::vector<fc_transfer> xs;
+  fc_status st = schedule(P, rank, FC_XCHG_COLSPLIT, &xs);
+  if (st != FC_OK) return st;
   if (!mine) return fail(FC_ERR_INVALID_ARG, "mine is NULL");
-  const size_t C = static_cast<size_t>(kCols / P->world);
   const fc_rank_plan& me = P->ranks[rank].p;
-  const size_t my_rows = static_cast<size_t>(me.row_end - me.row_begin);
-  if (my_rows && !blocks) return fail(FC_ERR_INVALID_ARG, "blocks is NULL");
+  if (me.row_end > me.row_begin && !blocks) return fail(FC_ERR_INVALID_ARG, "blocks is NULL");
   if (P->world > 1 && !comm) return fail(FC_ERR_INVALID_ARG, "comm is NULL with world_size > 1");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // own block: rows [row_begin, row_end) of this rank's column slice
-  if (my_rows) {
-    cudaError_t ce = cudaMemcpyAsync(mine + static_cast<size_t>(me.row_begin) * C, blocks + rank * my_rows * C,
-                                     my_rows * C * sizeof(float), cudaMemcpyDeviceToDevice, s);
-    if (ce != cudaSuccess) return fail(FC_ERR_CUDA, std::string("own block copy: ") + cudaGetErrorString(ce));
-  }
-  if (P->world == 1) return FC_OK;
-  // all-to-all: block p of my rows -> rank p; rank p's block `rank` -> my rows [row_begin_p, row_end_p)
-  ncclComm_t c = static_cast<ncclComm_t>(comm);
-  ncclResult_t r = ncclGroupStart();
-  if (r != ncclSuccess) return nccl_fail(r, "ncclGroupStart");
-  for (int p = 0; p < P->world && r == ncclSuccess; ++p) {
-    if (p == rank) continue;
-    const fc_rank_plan& rp = P->ranks[p].p;
-    const size_t prow = static_cast<size_t>(rp.row_end - rp.row_begin);
-    if (my_rows) r = ncclSend(blocks + p * my_rows * C, my_rows * C, ncclFloat32, p, c, s);
-    if (r == ncclSuccess && prow)
-      r = ncclRecv(mine + static_cast<size_t>(rp.row_begin) * C, prow * C, ncclFloat32, p, c, s);
-  }
-  ncclResult_t r2 = ncclGroupEnd();
-  if (r != ncclSuccess) return nccl_fail(r, "ncclSend/ncclRecv");
-  if (r2 != ncclSuccess) return nccl_fail(r2, "ncclGroupEnd");
-  return FC_OK;
+  return run_schedule(xs, P->world, comm, blocks, mine, stream);
 }
 
 }  // extern "C"

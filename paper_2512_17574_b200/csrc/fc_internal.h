@@ -40,7 +40,13 @@ struct RankPlan {
 };
 
 // Device copies of a plan's tables (see fc_kernels.cu: MMA fragment tables).
+// Held by shared_ptr: the bounded process-wide cache and every plan that uses
+// them keep a reference; the device memory is freed with the last one.
 struct DeviceTables {
+  DeviceTables() = default;
+  DeviceTables(const DeviceTables&) = delete;
+  DeviceTables& operator=(const DeviceTables&) = delete;
+  ~DeviceTables();  // fc_kernels.cu
   int ksh = 1, ksv = 1;        // MMA k-steps of the H / V windows
   int32_t* hx = nullptr;       // H xmin per output column
   int32_t* hxs = nullptr;      // H window start per 8-column tile
@@ -69,8 +75,9 @@ struct fc_plan_s {
   std::shared_ptr<const fc::AxisTable> th, tv;
   std::vector<float> lut;    // 3 x 256 (R5)
   std::vector<uint32_t> lut_dev;  // what the kernel stores: fp32 bits, or bf16 bits (R16)
-  std::mutex mu;             // guards dev
-  std::unordered_map<int, fc::DeviceTables> dev;
+  std::mutex mu;             // guards dev, tc
+  std::unordered_map<int, std::shared_ptr<const fc::DeviceTables>> dev;  // per (device, strip width)
+  std::unordered_map<int, std::shared_ptr<const void>> tc;  // per device: the tcgen05 kernel's tables
 };
 
 namespace fc {

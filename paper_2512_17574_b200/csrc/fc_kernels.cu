@@ -19,6 +19,7 @@
 
 #include "fc_fused.cuh"
 #include "fc_internal.h"
+#include "fc_launch.h"
 
 namespace fc {
 
@@ -41,7 +42,7 @@ static const Instance* instances() {
 }
 constexpr int kMaxKS = 4;
 
-static fc_status cuda_fail(cudaError_t e, const char* what) {
+fc_status cuda_fail(cudaError_t e, const char* what) {
   return fail(FC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
@@ -53,7 +54,7 @@ static cudaError_t upload(T** dst, const std::vector<T>& v) {
 }
 
 // Integer Pillow weight of output o at source index src (0 outside the window).
-static int32_t weight_at(const AxisTable& t, int o, int src) {
+int32_t weight_at(const AxisTable& t, int o, int src) {
   if (o < 0 || o >= t.out) return 0;
   const int tap = src - t.xmin[o];
   if (tap < 0 || tap >= t.cnt[o]) return 0;
@@ -165,14 +166,18 @@ struct TableKey {
 };
 
 static std::mutex g_tables_mu;
-static std::map<TableKey, DeviceTables>* g_tables = new std::map<TableKey, DeviceTables>();  // never freed
+static LruCache<TableKey, DeviceTables>* g_tables = new LruCache<TableKey, DeviceTables>(kTableCacheEntries);
 
-static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out) {
+DeviceTables::~DeviceTables() {
+  cudaFree(hx); cudaFree(hxs); cudaFree(hfr); cudaFree(vx); cudaFree(vcnt); cudaFree(vys); cudaFree(vfr); cudaFree(lut);
+}
+
+static fc_status device_tables(fc_plan_s* P, int dev, int sw, const DeviceTables** out) {
   std::lock_guard<std::mutex> lk(P->mu);
   const int pkey = dev * 1024 + sw;
   auto it = P->dev.find(pkey);
   if (it != P->dev.end()) {
-    *out = &it->second;
+    *out = it->second.get();
     return FC_OK;
   }
   TableKey key;
@@ -185,9 +190,9 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
   key.h2 = P->tv->out;
   std::memcpy(key.lut_bits, P->lut_dev.data(), sizeof(key.lut_bits));
   std::lock_guard<std::mutex> gk(g_tables_mu);
-  auto git = g_tables->find(key);
-  if (git != g_tables->end()) {
-    *out = &(P->dev[pkey] = git->second);
+  if (std::shared_ptr<DeviceTables> hit = g_tables->get(key)) {
+    *out = hit.get();
+    P->dev[pkey] = std::move(hit);
     return FC_OK;
   }
   // every V output must land inside the extended table: floor(S / 2^22) with
@@ -212,7 +217,8 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
   build_mma_tables(P, sw, &m);
   if (m.ksh > kMaxKS || m.ksv > kMaxKS)
     return fail(FC_ERR_UNSUPPORTED, "resize window wider than 128 source pixels per 8 outputs");
-  DeviceTables t;
+  auto sp = std::make_shared<DeviceTables>();  // frees whatever was uploaded if this fails
+  DeviceTables& t = *sp;
   t.ksh = m.ksh;
   t.ksv = m.ksv;
   cudaError_t e = cudaSuccess;
@@ -230,14 +236,12 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, DeviceTables** out
     for (int i = 0; i < kLutN; ++i)
       lut_ext[c * kLutN + i] = P->lut_dev[c * 256 + std::min(255, std::max(0, i - kLutLo))];
   if (e == cudaSuccess) e = upload(&t.lut, lut_ext);
-  if (e != cudaSuccess) {
-    cudaFree(t.hx); cudaFree(t.hxs); cudaFree(t.hfr); cudaFree(t.vx); cudaFree(t.vcnt); cudaFree(t.vys);
-    cudaFree(t.vfr); cudaFree(t.lut);
+  if (e != cudaSuccess)
     return e == cudaErrorMemoryAllocation ? fail(FC_ERR_OOM, "table upload: out of device memory")
                                           : cuda_fail(e, "table upload");
-  }
-  (*g_tables)[key] = t;
-  *out = &(P->dev[pkey] = t);
+  g_tables->put(key, sp);
+  *out = sp.get();
+  P->dev[pkey] = std::move(sp);
   return FC_OK;
 }
 
@@ -362,7 +366,7 @@ static std::unordered_map<MapKey, CUtensorMap, MapKeyHash>* g_maps =
     new std::unordered_map<MapKey, CUtensorMap, MapKeyHash>();  // never freed
 
 // 2-D u8 tensor [rows][pitch] with a (bw x bh) box; out-of-bounds -> zeros.
-static fc_status tensor_map(const uint8_t* base, int64_t pitch, int64_t rows, int bw, int bh, CUtensorMap* out) {
+fc_status tensor_map(const uint8_t* base, int64_t pitch, int64_t rows, int bw, int bh, CUtensorMap* out) {
   const MapKey key{reinterpret_cast<uintptr_t>(base), pitch, rows, bw, bh};
   std::lock_guard<std::mutex> lk(g_maps_mu);
   auto it = g_maps->find(key);
@@ -389,7 +393,7 @@ static fc_status tensor_map(const uint8_t* base, int64_t pitch, int64_t rows, in
 
 // Colour matrix constants (R3, R15): rounded 256x coefficients of the
 // standard matrices (include/fc.h), folded into dp2a operand pairs and biases.
-static void color_constants(fc_color m, Params* p) {
+void color_words(fc_color m, uint32_t* kR, uint32_t* kG, uint32_t* kGv, uint32_t* kB, int* bR, int* bG, int* bB) {
   struct K { int y, y0, rv, gu, gv, bu; };
   static const K kTab[4] = {
       {298, 16, 409, -100, -208, 516},  // BT.601 limited (R3)
@@ -399,17 +403,25 @@ static void color_constants(fc_color m, Params* p) {
   };
   const K& k = kTab[static_cast<int>(m)];
   auto pack = [](int hi, int lo) { return (static_cast<uint32_t>(hi & 0xFFFF) << 16) | static_cast<uint32_t>(lo & 0xFFFF); };
-  p->ckR = pack(k.rv, k.y);
-  p->ckB = pack(k.bu, k.y);
-  p->ckG = pack(k.gu, k.y);
-  p->ckGv = pack(k.gv, 0);
-  p->cbR = -k.y0 * k.y - 128 * k.rv + 128;
-  p->cbG = -k.y0 * k.y - 128 * (k.gu + k.gv) + 128;
-  p->cbB = -k.y0 * k.y - 128 * k.bu + 128;
+  *kR = pack(k.rv, k.y);
+  *kB = pack(k.bu, k.y);
+  *kG = pack(k.gu, k.y);
+  *kGv = pack(k.gv, 0);
+  *bR = -k.y0 * k.y - 128 * k.rv + 128;
+  *bG = -k.y0 * k.y - 128 * (k.gu + k.gv) + 128;
+  *bB = -k.y0 * k.y - 128 * k.bu + 128;
+}
+static void color_constants(fc_color m, Params* p) {
+  color_words(m, &p->ckR, &p->ckG, &p->ckGv, &p->ckB, &p->cbR, &p->cbG, &p->cbB);
 }
 
 // The rank's frame list (its sampled frames, then pad copies of the last),
 // after validating every surface it reads.  Empty for a rank with no rows.
+int32_t& last_kernel() {  // fc_last_kernel(): the calling thread's last fused-kernel launch
+  static thread_local int32_t k = FC_KERNEL_NONE;
+  return k;
+}
+
 std::atomic<uint64_t>& launch_counter() {  // fc_kernel_launches(); shared with fc_expand.cu
   static std::atomic<uint64_t> c{0};
   return c;
@@ -441,12 +453,6 @@ static fc_status rank_frames(const fc_plan_s* P, int32_t rank, const fc_nv12_sur
   return FC_OK;
 }
 
-// One launch job: a (plan, rank)'s frame list, its surfaces and its token buffer.
-struct Job {
-  std::vector<int64_t> frames;
-  const fc_nv12_surface* surfaces;
-  void* tokens;
-};
 
 // ONE persistent launch over every pair of `jobs` (all of P's geometry and
 // pair count).  Up to kMaxInlineFrames frames of a single job, the tensor maps
@@ -458,7 +464,7 @@ struct Job {
 // threshold keeps freed blocks in the pool across synchronisations, so a
 // steady stream of requests never goes back to the driver for memory (the
 // default pool returns memory at every sync).
-static cudaMemPool_t descriptor_pool(int dev) {
+cudaMemPool_t descriptor_pool(int dev) {
   static std::mutex mu;
   static std::map<int, cudaMemPool_t>* pools = new std::map<int, cudaMemPool_t>();
   std::lock_guard<std::mutex> lk(mu);
@@ -477,8 +483,21 @@ static cudaMemPool_t descriptor_pool(int dev) {
   return pool;
 }
 
+// dry: validate and prepare everything (tables, geometry, tensor maps) but
+// enqueue nothing -- fc_preprocess_batch checks every group before the first launch
 static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, uint8_t* dbg_src,
-                             uint8_t* dbg_rs, const fc_paged_tokens* paged = nullptr, bool colsplit = false) {
+                             uint8_t* dbg_rs, const fc_paged_tokens* paged = nullptr, bool colsplit = false,
+                             bool dry = false) {
+  // the tcgen05 kernel (fc_tc.cu) takes every NV12 / fp32 request whose
+  // windows fit its shared-memory plan; FC_TC=0 forces this kernel (A/B runs)
+  if (!paged && !colsplit && P->cfg.token_dtype == FC_TOKENS_F32 && P->cfg.surface_format == FC_SURFACE_NV12) {
+    const char* env = std::getenv("FC_TC");
+    if (!env || std::atoi(env) != 0) {
+      bool handled = false;
+      const fc_status st = launch_tc(P, jobs, stream, dbg_src, dbg_rs, &handled, dry);
+      if (handled) return st;
+    }
+  }
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
@@ -490,7 +509,7 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   const int W = P->meta.width, H = P->meta.height;
   // strips of 2 merge blocks; 1 merge block when a very wide resize window
   // would not fit the working set in shared memory
-  DeviceTables* dt = nullptr;
+  const DeviceTables* dt = nullptr;
   Geometry g;
   fc_status st = FC_OK;
   for (int sw : {kStrip, 28}) {
@@ -610,6 +629,7 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
       }
       if (st != FC_OK) return st;
     }
+  if (dry) return FC_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   void* desc = nullptr;
   if (!inline_maps || paged) {
@@ -685,7 +705,16 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   if (desc) cudaFreeAsync(desc, s);
   if (e != cudaSuccess) return cuda_fail(e, "kernel launch");
   launch_counter().fetch_add(1, std::memory_order_relaxed);
+  last_kernel() = FC_KERNEL_MMA;
   return FC_OK;
+}
+
+// Token buffers are written with 8-byte (fp32 pairs), 4-byte (bf16 pairs) or
+// 2-byte (u8 pairs) stores: a misaligned view would fault the context, so
+// it is rejected up front.
+static bool tokens_aligned(const void* p, fc_token_dtype td) {
+  const uintptr_t m = td == FC_TOKENS_F32 ? 7 : td == FC_TOKENS_BF16 ? 3 : 1;
+  return (reinterpret_cast<uintptr_t>(p) & m) == 0;
 }
 
 static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv12_surface* surfaces,
@@ -704,6 +733,8 @@ static fc_status preprocess_impl(const fc_plan_t* Pc, int32_t rank, const fc_nv1
   fc_status st = rank_frames(P, rank, surfaces, num_surfaces, &jobs[0].frames);
   if (st != FC_OK || jobs[0].frames.empty()) return st;
   if (!tokens && !paged) return fail(FC_ERR_INVALID_ARG, "tokens is NULL");
+  if (!tokens_aligned(paged ? paged->pool : tokens, P->cfg.token_dtype))
+    return fail(FC_ERR_UNSUPPORTED, "token buffer not aligned to its store width (8 B fp32, 4 B bf16, 2 B u8)");
   if (paged) {  // the page table must hold the write (SPEC write_chunk: CapacityError)
     const fc_rank_plan& rp = P->ranks[rank].p;
     const int64_t rows = rp.row_end - rp.row_begin;
@@ -769,6 +800,8 @@ fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* rank
     fc_status st = rank_frames(jp[i], ranks[i], surfaces[i], num_surfaces[i], &jobs[i].frames);
     if (st != FC_OK) return st;
     if (!jobs[i].frames.empty() && !tokens[i]) return fail(FC_ERR_INVALID_ARG, "batch: tokens is NULL");
+    if (!jobs[i].frames.empty() && !tokens_aligned(tokens[i], jp[i]->cfg.token_dtype))
+      return fail(FC_ERR_UNSUPPORTED, "batch: token buffer not aligned to its store width");
     jobs[i].surfaces = surfaces[i];
     jobs[i].tokens = tokens[i];
   }
@@ -779,26 +812,37 @@ fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* rank
            A.cfg.surface_format == B.cfg.surface_format &&
            jobs[a].frames.size() == jobs[b].frames.size();
   };
-  std::vector<Job> group;
+  // groups; every group is validated (dry run) before the first launch, so an
+  // error leaves nothing enqueued (fc.h: no partial effects)
+  std::vector<std::pair<int32_t, std::vector<Job>>> groups;
   for (int32_t i = 0; i < count;) {
     if (jobs[i].frames.empty()) {
       ++i;
       continue;
     }
     int32_t j = i;
-    group.clear();
+    std::vector<Job> group;
     while (j < count && (jobs[j].frames.empty() || same(i, j))) {
       if (!jobs[j].frames.empty()) group.push_back(jobs[j]);
       ++j;
     }
-    fc_status st = launch_jobs(jp[i], group, stream, nullptr, nullptr);
-    if (st != FC_OK) return st;
+    groups.emplace_back(i, std::move(group));
     i = j;
+  }
+  for (auto& g : groups) {
+    fc_status st = launch_jobs(jp[g.first], g.second, stream, nullptr, nullptr, nullptr, false, true);
+    if (st != FC_OK) return st;
+  }
+  for (auto& g : groups) {
+    fc_status st = launch_jobs(jp[g.first], g.second, stream, nullptr, nullptr);
+    if (st != FC_OK) return st;
   }
   return FC_OK;
 }
 
 uint64_t fc_kernel_launches(void) { return launch_counter().load(std::memory_order_relaxed); }
+
+int32_t fc_last_kernel(void) { return last_kernel(); }
 
 void fc_plan_destroy(fc_plan_t* P) {
   // device tables belong to the process-wide cache (shared by equal shapes)

@@ -283,6 +283,7 @@ static fc_status partition(fc_plan_s* P) {
         for (int b2 = b + 1; b2 <= G; ++b2) {
           Seg s;
           if (!rank_step(a, n, G, b2, start, &s)) continue;
+          if (s.pairs > best) break;  // pairs never decrease as b2 grows: no later b2 can beat best
           const int64_t v = std::max(cur, s.pairs);
           if (s.end == n) {
             best = std::min(best, v);
@@ -317,7 +318,7 @@ static fc_status partition(fc_plan_s* P) {
         for (int b2 = b + 1; b2 <= G; ++b2) {
           Seg s;
           if (!rank_step(a, n, G, b2, start, &s)) continue;
-          if (s.pairs > cap) continue;
+          if (s.pairs > cap) break;  // pairs never decrease as b2 grows
           Cost2 nc{cur.cost.enc - (r == e ? s.pairs : 0), cur.cost.sq + s.pairs * s.pairs};
           if (s.end == n) {
             if (nc < best2) {
@@ -450,7 +451,7 @@ fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t*
   const fc_model_cfg& c = *cfg;
   if (c.patch_size != kPatch || c.temporal_patch_size != kTps || c.merge_size != kMerge)
     return fail(FC_ERR_UNSUPPORTED, "only patch 14, temporal patch 2, merge 2 are supported");
-  if (c.world_size < 1 || c.world_size > 4096) return fail(FC_ERR_INVALID_ARG, "world_size out of range");
+  if (c.world_size < 1 || c.world_size > 1024) return fail(FC_ERR_INVALID_ARG, "world_size out of range [1, 1024]");
   if (c.encoder_rank < 0 || c.encoder_rank >= c.world_size)
     return fail(FC_ERR_RANK, "encoder_rank outside [0, world_size)");
   if (c.min_frames < 0 || c.max_frames < 1) return fail(FC_ERR_INVALID_ARG, "bad min/max frames");
@@ -484,7 +485,11 @@ fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t*
     P->sampled_fps = static_cast<double>(P->n) / static_cast<double>(m.num_frames) *
                      (static_cast<double>(m.fps.num) / static_cast<double>(m.fps.den));
     P->second_per_grid = kTps / P->sampled_fps;
-    st = partition(P);
+    try {  // the DP tables are O(W * G): no exception may cross the C ABI
+      st = partition(P);
+    } catch (const std::bad_alloc&) {
+      st = fail(FC_ERR_OOM, "partition tables: host allocation failed");
+    }
   }
   if (st == FC_OK) st = axis_cached(m.width, P->w2, &P->th);
   if (st == FC_OK) st = axis_cached(m.height, P->h2, &P->tv);

@@ -35,3 +35,12 @@ def cuda():
         pytest.fail("gpu-marked test without a CUDA device")
     torch.cuda.set_device(0)
     return torch
+
+
+@pytest.fixture(params=["tc", "mma"])
+def kernel(request, monkeypatch):
+    """Which fused kernel serves NV12 / fp32 requests: "tc" (the tcgen05
+    kernel, the default wherever its shared-memory plan fits) or "mma" (the
+    mma.sync kernel, FC_TC=0).  libfc reads FC_TC at every launch."""
+    monkeypatch.setenv("FC_TC", "1" if request.param == "tc" else "0")
+    return request.param

@@ -3,11 +3,11 @@
 One process per rank, as bench.py runs under torchrun.  Each rank builds the
 plan independently (it must be identical on every rank: no coordination is
 needed, the plan is a pure function of the request), computes ITS shard -- here
-with the CPU oracle, since this box has no GPU -- and the shards are gathered
-to the encoder rank over the process group at the row offsets the plan
-assigns.  The encoder checks the P:339 invariant: the gathered result equals
-the single-GPU result bit for bit.  The device path of the same exchange
-(fc_gather, NCCL send/recv) is the same row arithmetic.
+with the CPU oracle, since this box has no GPU -- and runs the library's own
+exchange schedule (fc_exchange_schedule: exactly the transfers fc_gather /
+fc_scatter_columns hand to NCCL) with gloo isend/irecv on byte buffers.  The
+receiver checks the P:339 invariant: the assembled result equals the
+single-GPU result bit for bit.
 """
 import os
 import socket
@@ -44,7 +44,8 @@ def _worker(rank, world, port, case, q, exchange="f32"):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         W, H, N, gops, cfg = case
-        plan = fc.Plan(fc.VideoMeta(W, H, N, (30, 1), gops), fc.ModelCfg(world_size=world, **cfg))
+        tok = "u8" if exchange == "u8" else "f32"  # the plan's token dtype sizes the exchanged rows
+        plan = fc.Plan(fc.VideoMeta(W, H, N, (30, 1), gops), fc.ModelCfg(world_size=world, token_dtype=tok, **cfg))
         # 1) every rank derived the same plan
         digest = hashlib.sha256(repr((plan.sampled_indices, plan.ranks(), plan.grid_thw)).encode()).digest()
         mine = torch.tensor(list(digest), dtype=torch.uint8)
@@ -67,44 +68,44 @@ def _worker(rank, world, port, case, q, exchange="f32"):
             shard = (oracle.preprocess([host[f] for f in frames], W, H, w2, h2) if frames
                      else np.zeros((0, 1176), np.float32))
         assert shard.shape[0] == rows
+        host_all = {i: synth.frame_nv12(W, H, i, "natural", 21) for i in idx}
+        ref = oracle.preprocess([host_all[i] for i in idx], W, H, w2, h2)
+        enc = plan.cfg.encoder_rank
         if exchange == "colsplit":  # NEXT-1 column split: all-to-all of column blocks
             C = 1176 // world
-            mine = torch.zeros((plan.token_rows, C), dtype=torch.float32)
-            mine[rp["row_begin"]:rp["row_end"]] = torch.from_numpy(shard[:, rank * C:(rank + 1) * C])
-            reqs = []
-            for p, rp_p in enumerate(plan.ranks()):
-                if p == rank:
-                    continue
-                if rows:
-                    reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(shard[:, p * C:(p + 1) * C])), p))
-                n = rp_p["row_end"] - rp_p["row_begin"]
-                if n:
-                    reqs.append(dist.irecv(mine[rp_p["row_begin"]:rp_p["row_end"]], p))
-            for rq in reqs:
+            blocks = np.stack([shard[:, j * C:(j + 1) * C] for j in range(world)]) if rows else np.zeros((world, 0, C))
+            send = torch.from_numpy(np.ascontiguousarray(blocks, dtype=np.float32).reshape(-1).view(np.uint8))
+            recv = torch.zeros(plan.token_rows * C * 4, dtype=torch.uint8)
+            kind = "colsplit"
+        else:
+            send = torch.from_numpy(np.ascontiguousarray(shard).reshape(-1).view(np.uint8))
+            recv = torch.zeros(plan.token_rows * 1176 * shard.itemsize if rank == enc else 0, dtype=torch.uint8)
+            kind = "gather"
+        # 3) the library's schedule over the process group (fc_gather / fc_scatter_columns' transfers)
+        reqs = []
+        for x in fc.exchange_schedule(plan, rank, kind):
+            a, b, n = x["src_offset"], x["dst_offset"], x["bytes"]
+            if x["dir"] == "local":
+                recv[b:b + n] = send[a:a + n]
+            elif x["dir"] == "send":
+                reqs.append(dist.isend(send[a:a + n].clone(), x["peer"]))
+            else:
+                buf = torch.empty(n, dtype=torch.uint8)
+                reqs.append((dist.irecv(buf, x["peer"]), buf, b))
+        for rq in reqs:
+            if isinstance(rq, tuple):
+                rq[0].wait()
+                recv[rq[2]:rq[2] + len(rq[1])] = rq[1]
+            else:
                 rq.wait()
-            host_all = {i: synth.frame_nv12(W, H, i, "natural", 21) for i in idx}
-            ref = oracle.preprocess([host_all[i] for i in idx], W, H, w2, h2)
-            assert mine.numpy().view(np.uint32).tobytes() == \
+        if exchange == "colsplit":
+            assert recv.numpy().tobytes() == \
                 np.ascontiguousarray(ref[:, rank * C:(rank + 1) * C]).view(np.uint32).tobytes(), "column slice"
-            q.put((rank, "ok"))
-            return
-        # 3) gather to the encoder rank at the planned row offsets
-        maxrows = max(r["row_end"] - r["row_begin"] for r in plan.ranks())
-        buf = torch.zeros((maxrows, 1176), dtype=torch.uint8 if exchange == "u8" else torch.float32)
-        buf[:rows] = torch.from_numpy(shard)
-        enc = plan.cfg.encoder_rank
-        gathered = [torch.empty_like(buf) for _ in range(world)] if rank == enc else None
-        dist.gather(buf, gathered, dst=enc)
-        if rank == enc:
-            full = np.zeros((plan.token_rows, 1176), shard.dtype)
-            for r, rp_r in enumerate(plan.ranks()):
-                n = rp_r["row_end"] - rp_r["row_begin"]
-                full[rp_r["row_begin"]:rp_r["row_end"]] = gathered[r][:n].numpy()
+        elif rank == enc:
+            full = recv.numpy().view(shard.dtype).reshape(plan.token_rows, 1176)
             if exchange == "u8":  # expand: R5 table per channel of each column
                 lut = np.array([[oracle.normalize_value(v, c) for v in range(256)] for c in range(3)], np.float32)
                 full = lut[(np.arange(1176) // 392)[None, :], full]
-            host_all = {i: synth.frame_nv12(W, H, i, "natural", 21) for i in idx}
-            ref = oracle.preprocess([host_all[i] for i in idx], W, H, w2, h2)
             assert full.view(np.uint32).tobytes() == ref.view(np.uint32).tobytes(), "gathered != single-GPU result"
         q.put((rank, "ok"))
     except Exception as e:  # report to the parent

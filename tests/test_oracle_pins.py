@@ -92,6 +92,24 @@ def test_sampling_num_frames_and_linspace(oracle):
 
 
 # ------------------------------------------------------------------ O4
+def test_smart_resize_total_pixels_budget(oracle):
+    """R2 total budget (qwen-vl-utils).  Pins: SURVEY 8(d)'s
+    c3 variant (1280x720, n=600, total_pixels=90,316,800 -> 728x392, grid
+    (300,28,52), 436,800 token rows); the 1.05*min_pixels floor wins for a tiny
+    total; total_pixels=0 and a budget above max_pixels change nothing."""
+    assert oracle.smart_resize(720, 1280, total_pixels=90_316_800, n=600) == (392, 728)
+    assert oracle.grid_thw(600, 392, 728) == (300, 28, 52) and 300 * 28 * 52 == 436_800
+    # per-frame budget 90316800/600*2 = 301056 (between the floor and max_pixels)
+    assert oracle.video_max_pixels(100352, 602112, 90_316_800, 600) == 301056.0
+    # floor: int(100352 * 1.05) = 105369 > 1000/120*2
+    assert oracle.video_max_pixels(100352, 602112, 1000, 120) == 105369
+    h, w = oracle.smart_resize(1080, 1920, total_pixels=1000, n=120)
+    assert h * w <= 105369 and h % 28 == 0 and w % 28 == 0
+    assert (h + 28) * (w + 28) > 105369  # largest grid step under the budget
+    assert oracle.smart_resize(1080, 1920, total_pixels=0, n=120) == oracle.smart_resize(1080, 1920)
+    assert oracle.smart_resize(1080, 1920, total_pixels=1e12, n=120) == oracle.smart_resize(1080, 1920)
+
+
 def test_smart_resize_brute_force_vs_hf(oracle):
     from transformers.models.qwen2_vl.image_processing_qwen2_vl import smart_resize as hf
     budgets = [(3136, 1003520), (3136, 12845056), (100352, 602112), (784, 3136)]

@@ -5,10 +5,17 @@ Bar (BASELINE.json north star):
     RGB intermediate: bit-exact;
   * normalised fp32 tokens: |gpu - oracle| <= 1e-5 * max(|oracle|, 1) per
     element (reading R7; bit-exact expected, and the count is reported).
-Small cases are compared element by element on the whole output; the full
-BASELINE configs run in the bench's launch configuration (one launch per
-rank, all frames) and are compared on sampled temporal pairs.
+Two fused kernels serve these requests: the tcgen05 kernel (default for NV12
+/ fp32 wherever its shared-memory plan fits) and the mma.sync kernel (every
+other shape and variant; FC_TC=0 forces it) -- the `kernel` fixture runs a
+test through each.  Small cases are compared element by element on the whole
+output, through both the production instance (fc_preprocess) and the debug
+instance that also dumps the integer intermediates; the full BASELINE configs
+run in the bench's launch configuration (one launch per rank, all frames) and
+are compared element by element on the WHOLE token tensor against the
+threaded oracle, in chunks of pairs.
 """
+import os
 import numpy as np
 import pytest
 
@@ -59,11 +66,16 @@ def run_case(fc, oracle, cuda, W, H, N, gops, kind="natural", seed=7, world=1, c
             np.testing.assert_array_equal(rs.cpu().numpy(), ref_rs[fr], err_msg=f"rgb_resized rank {r}")
     got = np.concatenate(parts, axis=0)
     exact = tol_check(got, ref_tok, f"{W}x{H}->{w2}x{h2} {kind} W={world}")
+    # the production instance (no dumps) on the same inputs, every rank
+    prod = [fc.preprocess(plan, r, surf) for r in range(world) if plan.rank(r)["row_end"] > plan.rank(r)["row_begin"]]
+    cuda.cuda.synchronize()
+    got_p = np.concatenate([t.cpu().numpy() for t in prod], axis=0)
+    assert tol_check(got_p, ref_tok, f"production {W}x{H}->{w2}x{h2} {kind} W={world}") == exact
     return plan, exact, got.size
 
 
 @pytest.mark.parametrize("kind", ["natural", "uniform", "edges"])
-def test_c1_shape_all_kinds(fc, oracle, cuda, kind):
+def test_c1_shape_all_kinds(fc, oracle, cuda, kernel, kind):
     wl = synth.CONFIGS["c1"]
     plan, exact, size = run_case(fc, oracle, cuda, wl.width, wl.height, wl.num_frames, wl.gop_start, kind,
                                  seed=wl.seed, sample_fps=2.0)
@@ -82,7 +94,7 @@ def test_c1_shape_all_kinds(fc, oracle, cuda, kind):
     (30, 18, 56, 56),      # odd-size-ish small frame, heavy upscale
 ])
 @pytest.mark.parametrize("kind", ["natural", "uniform"])
-def test_shapes(fc, oracle, cuda, shape, kind):
+def test_shapes(fc, oracle, cuda, kernel, shape, kind):
     W, H, h2, w2 = shape
     N = 8
     plan, exact, size = run_case(fc, oracle, cuda, W, H, N, [0], kind, seed=11,
@@ -91,7 +103,7 @@ def test_shapes(fc, oracle, cuda, shape, kind):
     assert plan.resized == (h2, w2)
 
 
-def test_odd_count_pads_last_frame(fc, oracle, cuda):
+def test_odd_count_pads_last_frame(fc, oracle, cuda, kernel):
     # 5 explicit frames -> padded to 6 with the last one
     plan, exact, size = run_case(fc, oracle, cuda, 320, 240, 40, [0, 10, 20, 30], "edges", seed=3,
                                  sampling="explicit", explicit_indices=[1, 9, 17, 25, 33])
@@ -99,7 +111,7 @@ def test_odd_count_pads_last_frame(fc, oracle, cuda):
 
 
 @pytest.mark.parametrize("world", [2, 3, 5])
-def test_virtual_ranks_concat_equals_single(fc, oracle, cuda, world):
+def test_virtual_ranks_concat_equals_single(fc, oracle, cuda, kernel, world):
     """O12 / P:339: the concatenated rank shards equal the single-GPU result
     (all ranks run on one device; no NCCL)."""
     plan, exact, size = run_case(fc, oracle, cuda, 320, 240, 300, list(range(0, 300, 30)), "natural",
@@ -107,7 +119,7 @@ def test_virtual_ranks_concat_equals_single(fc, oracle, cuda, world):
     assert exact == size
 
 
-def test_virtual_ranks_odd_explicit(fc, oracle, cuda):
+def test_virtual_ranks_odd_explicit(fc, oracle, cuda, kernel):
     # method-b tails and last-rank padding together
     plan, exact, size = run_case(fc, oracle, cuda, 256, 144, 100, list(range(0, 100, 10)), "uniform",
                                  seed=9, world=4, sampling="explicit",
@@ -117,7 +129,13 @@ def test_virtual_ranks_odd_explicit(fc, oracle, cuda):
 
 
 # ------------------------------------------------------------ full configs
-def _full_config(fc, oracle, cuda, name, pairs_to_check, kind="natural", clip=0):
+NCPU = len(os.sched_getaffinity(0))
+
+
+def _full_config(fc, oracle, cuda, name, kind="natural", clip=0, chunk=30, expect_kernel="tc"):
+    """A BASELINE config in the bench's launch configuration (one fc_preprocess
+    launch over all frames), compared element by element on the WHOLE token
+    tensor with the threaded oracle, chunk pairs at a time."""
     import torch
     wl = synth.CONFIGS[name]
     plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
@@ -126,50 +144,54 @@ def _full_config(fc, oracle, cuda, name, pairs_to_check, kind="natural", clip=0)
     host = synth.frames_nv12(wl, idx, kind, clip=clip)
     dev = synth.to_device(host)
     surf = fc.SurfaceTable.from_tensors(dev, wl.num_frames)
-    tokens = fc.preprocess(plan, 0, surf)  # the bench's launch configuration
+    tokens = fc.preprocess(plan, 0, surf)
     torch.cuda.synchronize()
+    if expect_kernel:
+        assert fc.last_kernel() == expect_kernel
     gt, gh, gw = plan.grid_thw
     rpp = gh * gw
     h2, w2 = plan.resized
     exact_total = size_total = 0
-    for t in pairs_to_check(gt):
-        fr = [idx[min(2 * t + k, len(idx) - 1)] for k in (0, 1)]
-        ref = oracle.preprocess([host[f] for f in fr], wl.width, wl.height, w2, h2)
-        got = tokens[t * rpp:(t + 1) * rpp].cpu().numpy()
-        exact_total += tol_check(got, ref, f"{name} pair {t}")
+    for t0 in range(0, gt, chunk):
+        t1 = min(gt, t0 + chunk)
+        fr = [idx[min(k, len(idx) - 1)] for k in range(2 * t0, 2 * t1)]
+        ref = oracle.preprocess([host[f] for f in fr], wl.width, wl.height, w2, h2, nthreads=NCPU)
+        got = tokens[t0 * rpp:t1 * rpp].cpu().numpy()
+        exact_total += tol_check(got, ref, f"{name} pairs [{t0}, {t1})")
         size_total += got.size
+    assert size_total == plan.token_rows * 1176
     return plan, exact_total, size_total
 
 
-def _sample_pairs(gt):
-    return sorted({0, 1, gt // 2, gt - 1})
+def _sample_pairs(gt):  # (name kept for the variant tests) every pair of the request
+    return range(gt)
 
 
-def test_full_c1(fc, oracle, cuda):
-    plan, e, s = _full_config(fc, oracle, cuda, "c1", lambda gt: range(gt))
+def test_full_c1(fc, oracle, cuda, kernel):
+    plan, e, s = _full_config(fc, oracle, cuda, "c1", expect_kernel=kernel)
     assert plan.grid_thw == (4, 20, 28) and e == s
 
 
-def test_full_c2_sampled_pairs(fc, oracle, cuda):
-    plan, e, s = _full_config(fc, oracle, cuda, "c2", _sample_pairs)
+def test_full_c2_whole_tensor(fc, oracle, cuda, kernel):
+    plan, e, s = _full_config(fc, oracle, cuda, "c2", expect_kernel=kernel)
     assert plan.grid_thw == (60, 40, 72)
     assert e == s
 
 
-def test_full_c4_sampled_pairs(fc, oracle, cuda):
-    plan, e, s = _full_config(fc, oracle, cuda, "c4", _sample_pairs, kind="edges")
+def test_full_c4_whole_tensor(fc, oracle, cuda, kernel):
+    plan, e, s = _full_config(fc, oracle, cuda, "c4", kind="edges", expect_kernel=kernel)
     assert plan.grid_thw == (30, 40, 72)
     assert e == s
 
 
-def test_full_c3_sampled_pairs(fc, oracle, cuda):
-    plan, e, s = _full_config(fc, oracle, cuda, "c3", _sample_pairs)
+def test_full_c3_whole_tensor(fc, oracle, cuda, kernel):
+    plan, e, s = _full_config(fc, oracle, cuda, "c3", chunk=50, expect_kernel=kernel)
     assert plan.grid_thw == (300, 40, 72)
     assert e == s
 
 
-def test_full_c5_clip(fc, oracle, cuda):
-    plan, e, s = _full_config(fc, oracle, cuda, "c5", lambda gt: range(gt), kind="uniform", clip=17)
+def test_full_c5_clip(fc, oracle, cuda, kernel):
+    plan, e, s = _full_config(fc, oracle, cuda, "c5", kind="uniform", clip=17, expect_kernel=kernel)
     assert plan.grid_thw == (10, 34, 60)
     assert e == s
 
@@ -181,7 +203,7 @@ def _clip_inputs(fc, wl, clip, kind, plan):
     return host, dev, fc.SurfaceTable.from_tensors(dev, wl.num_frames)
 
 
-def test_batch_homogeneous_matches_oracle(fc, oracle, cuda):
+def test_batch_homogeneous_matches_oracle(fc, oracle, cuda, kernel):
     """fc_preprocess_batch, config-5 shape: 6 clips with different content in
     ONE launch (per-job token bases, tensor maps in device memory); every
     clip equals the oracle on its own frames."""
@@ -202,7 +224,7 @@ def test_batch_homogeneous_matches_oracle(fc, oracle, cuda):
         assert tol_check(out.cpu().numpy(), ref, "batch clip") == ref.size
 
 
-def test_batch_heterogeneous_equals_single_calls(fc, oracle, cuda):
+def test_batch_heterogeneous_equals_single_calls(fc, oracle, cuda, kernel):
     """Mixed shapes, pair counts, a rank with no rows and a job past the
     inline tensor-map limit in one batch call: each job's tokens equal its own
     fc_preprocess call bit for bit (runs of equal geometry share a launch)."""
@@ -243,36 +265,32 @@ def test_batch_heterogeneous_equals_single_calls(fc, oracle, cuda):
         tol_check(outs[-1][t * rpp:(t + 1) * rpp].cpu().numpy(), ref, f"long job pair {t}")
 
 
-def test_full_c5_batch_64_clips(fc, oracle, cuda):
+def test_full_c5_batch_64_clips(fc, oracle, cuda, kernel):
     """Config 5 as the bench runs it: 64 clips, one fc_preprocess_batch call;
-    sampled clips checked pair by pair against the oracle."""
+    every clip compared element by element with the oracle."""
     import torch
     wl = synth.CONFIGS["c5"]
     meta = fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start)
     plan = fc.Plan(meta, fc.ModelCfg(sample_fps=wl.sample_fps))
     idx = plan.sampled_indices
-    hosts, jobs = {}, []
+    jobs = []
     for clip in range(wl.clips):
         host = synth.frames_nv12(wl, idx, "natural", clip=clip)
-        if clip in (0, 31, 63):
-            hosts[clip] = host
         dev = synth.to_device(host)
         jobs.append((plan, 0, fc.SurfaceTable.from_tensors(dev, wl.num_frames), dev))
     outs = fc.preprocess_batch([(p, r, s) for p, r, s, _ in jobs])
     torch.cuda.synchronize()
     h2, w2 = plan.resized
-    rpp = plan.grid_thw[1] * plan.grid_thw[2]
-    for clip, host in hosts.items():
-        for t in (0, 4, plan.grid_thw[0] - 1):
-            ref = oracle.preprocess([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2)
-            got = outs[clip][t * rpp:(t + 1) * rpp].cpu().numpy()
-            assert tol_check(got, ref, f"c5 clip {clip} pair {t}") == ref.size
+    for clip in range(wl.clips):  # every clip, every element
+        host = synth.frames_nv12(wl, idx, "natural", clip=clip)
+        ref = oracle.preprocess([host[i] for i in idx], wl.width, wl.height, w2, h2, nthreads=NCPU)
+        assert tol_check(outs[clip].cpu().numpy(), ref, f"c5 clip {clip}") == ref.size
 
 
 # ------------------------------------------------------ NEXT-4 variants
 @pytest.mark.parametrize("color", ["bt709", "bt601_full", "bt709_full"])
 @pytest.mark.parametrize("kind", ["uniform", "edges"])
-def test_colour_variants(fc, oracle, cuda, color, kind):
+def test_colour_variants(fc, oracle, cuda, kernel, color, kind):
     """R15: the colour-matrix variants, RGB intermediates and tokens vs the oracle."""
     plan, exact, size = run_case(fc, oracle, cuda, 320, 240, 40, [0, 20], kind, seed=13,
                                  sampling="explicit", explicit_indices=[1, 9, 22, 33], color=color)
@@ -307,8 +325,8 @@ def test_bf16_tokens(fc, oracle, cuda, shape):
                explicit_indices=[2, 3], color="bt709")
 
 
-def test_bf16_full_c2_sampled_pairs(fc, oracle, cuda):
-    """bf16 at BASELINE config 2 in the bench's launch configuration; sampled pairs."""
+def test_bf16_full_c2(fc, oracle, cuda):
+    """bf16 at BASELINE config 2 in the bench's launch configuration; every pair."""
     import torch
     wl = synth.CONFIGS["c2"]
     plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
@@ -321,7 +339,7 @@ def test_bf16_full_c2_sampled_pairs(fc, oracle, cuda):
     rpp = plan.grid_thw[1] * plan.grid_thw[2]
     h2, w2 = plan.resized
     for t in _sample_pairs(plan.grid_thw[0]):
-        ref = oracle.preprocess([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2)
+        ref = oracle.preprocess([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2, nthreads=NCPU)
         got = out[t * rpp:(t + 1) * rpp].view(torch.int16).cpu().numpy().view(np.uint16)
         np.testing.assert_array_equal(got, oracle.to_bf16(ref), err_msg=f"pair {t}")
 
@@ -368,7 +386,7 @@ def test_u8_codes_exchange_and_expand(fc, oracle, cuda, world):
 
 
 def test_u8_codes_full_c2(fc, oracle, cuda):
-    """Config 2 through the u8 path (one launch) + expand, sampled pairs vs the oracle."""
+    """Config 2 through the u8 path (one launch) + expand, every pair vs the oracle."""
     import torch
     wl = synth.CONFIGS["c2"]
     plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
@@ -381,7 +399,7 @@ def test_u8_codes_full_c2(fc, oracle, cuda):
     rpp = plan.grid_thw[1] * plan.grid_thw[2]
     h2, w2 = plan.resized
     for t in _sample_pairs(plan.grid_thw[0]):
-        ref = oracle.preprocess([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2)
+        ref = oracle.preprocess([host[idx[2 * t]], host[idx[2 * t + 1]]], wl.width, wl.height, w2, h2, nthreads=NCPU)
         np.testing.assert_array_equal(tok[t * rpp:(t + 1) * rpp].cpu().numpy().view(np.uint32), ref.view(np.uint32))
 
 
@@ -465,7 +483,7 @@ def test_paged_full_c2_matches_linear(fc, cuda):
 
 
 # ------------------------------------------------------ more edge cases
-def test_8k_input_wide_windows(fc, oracle, cuda):
+def test_8k_input_wide_windows(fc, oracle, cuda, kernel):
     """7680x4320 -> smart_resize: ~5.9x downscale, 24+-tap windows, strips whose
     source span needs two TMA boxes per row (NX = 2); one pair vs the oracle."""
     plan, exact, size = run_case(fc, oracle, cuda, 7680, 4320, 8, [0], "natural", seed=77, check_rgb=False,
@@ -473,7 +491,7 @@ def test_8k_input_wide_windows(fc, oracle, cuda):
     assert plan.max_taps[0] >= 20 and exact == size
 
 
-def test_cuda_graph_capture_replay(fc, oracle, cuda):
+def test_cuda_graph_capture_replay(fc, oracle, cuda, kernel):
     """fc_preprocess (tensor maps in the kernel parameters, <= 120 frames) is
     stream-capturable: a captured graph replays to the same tokens, and
     replays after the NV12 surfaces change pick up the new content."""
@@ -584,3 +602,41 @@ def test_colsplit_virtual_ranks(fc, oracle, cuda, world):
             mine = fc.scatter_columns(plan, 0, None, blocks)
             torch.cuda.synchronize()
             np.testing.assert_array_equal(mine.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+
+
+# ------------------------------------------------------ a10 exchange, executed
+def test_gather_world1_copies_shard(fc, oracle, cuda):
+    """fc_gather at W = 1 (no communicator): the encoder's full buffer receives
+    the shard through the library's own schedule (one local transfer), bit for
+    bit; u8 codes take the same path with 1-byte elements."""
+    import torch
+    for tok in ("f32", "u8"):
+        plan = make_plan(fc, 320, 240, 120, [0], sample_fps=2.0, token_dtype=tok)
+        host = {i: synth.frame_nv12(320, 240, i, "natural", 8) for i in plan.sampled_indices}
+        surf = fc.SurfaceTable.from_tensors(synth.to_device(host), 120)
+        shard = fc.preprocess(plan, 0, surf)
+        full = fc.gather(plan, 0, None, shard)
+        torch.cuda.synchronize()
+        assert full.data_ptr() != shard.data_ptr() and torch.equal(full, shard)
+        assert fc.exchange_schedule(plan, 0) == [dict(peer=0, dir="local", src_offset=0, dst_offset=0,
+                                                      bytes=shard.numel() * shard.element_size())]
+
+
+def test_tc_kernel_serves_the_baseline_configs(fc, cuda):
+    """The tcgen05 kernel's plan fits every BASELINE config (c1-c5); the
+    paper's 224x224 setting (37-tap windows) falls to the mma.sync kernel."""
+    import torch
+    for name in ("c1", "c2", "c3", "c4", "c5"):
+        wl = synth.CONFIGS[name]
+        plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
+                       fc.ModelCfg(sampling="explicit", explicit_indices=[0, 1]))
+        host = {i: synth.frame_nv12(wl.width, wl.height, i, "natural", 1) for i in (0, 1)}
+        fc.preprocess(plan, 0, fc.SurfaceTable.from_tensors(synth.to_device(host), wl.num_frames))
+        torch.cuda.synchronize()
+        assert fc.last_kernel() == "tc", name
+    plan = make_plan(fc, 1920, 1080, 8, [0], sampling="explicit", explicit_indices=[0, 1], resized_height=224,
+                     resized_width=224)
+    host = {i: synth.frame_nv12(1920, 1080, i, "natural", 1) for i in (0, 1)}
+    fc.preprocess(plan, 0, fc.SurfaceTable.from_tensors(synth.to_device(host), 8))
+    torch.cuda.synchronize()
+    assert fc.last_kernel() == "mma"

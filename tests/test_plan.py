@@ -332,3 +332,158 @@ def test_colsplit_requires_world_dividing_1176(fc):
     assert fc._native.STATUS[st] == "FC_ERR_UNSUPPORTED", fc.lib().fc_last_error()
     st = fc.lib().fc_scatter_columns(p.handle, 0, None, None, ctypes.cast(out, ctypes.c_void_p), None)
     assert fc._native.STATUS[st] == "FC_ERR_UNSUPPORTED"
+
+
+# ------------------------------------------------ a1/a2 planner modes
+@pytest.mark.parametrize("N,n_req", [(100, 5), (100, 7), (1800, 120), (18000, 600), (300, 21), (9, 8), (64, 64)])
+def test_num_frames_mode_matches_oracle(fc, oracle, N, n_req):
+    """a1 `num_frames` rule (n = round_half_even(num_frames/2)*2) through
+    fc_plan == the oracle (pinned to HF in test_oracle_pins)."""
+    p = plan_of(fc, 320, 240, N, [0], num_frames=n_req)
+    assert p.sampled_indices == oracle.sample_indices(N, 30, None, num_frames=n_req)
+
+
+@pytest.mark.parametrize("N,fps", [(1800, 2.0), (120, 2.0), (18000, 1.0), (301, 0.5), (17, 2.0), (900, 2.0)])
+def test_linspace_mode_matches_oracle(fc, oracle, N, fps):
+    """a1 LINSPACE (idx_i = round_half_even(i(N-1)/(n-1)), exact rational)
+    through fc_plan == the oracle."""
+    p = plan_of(fc, 320, 240, N, [0], sampling="linspace", sample_fps=fps)
+    assert p.sampled_indices == oracle.sample_indices(N, 30, fps, mode="linspace")
+
+
+@pytest.mark.parametrize("total", [90_316_800, 1000, 5e6, 3.3e7, 1e12])
+@pytest.mark.parametrize("WH", [(1280, 720), (1920, 1080), (854, 480), (3840, 2160), (320, 240)])
+def test_total_pixels_budget_matches_oracle(fc, oracle, total, WH):
+    """a2 optional total_pixels budget (qwen-vl-utils) through fc_plan == the
+    oracle's pinned video_max_pixels + smart_resize (c3 variant: 728x392)."""
+    W, H = WH
+    p = plan_of(fc, W, H, 1800, list(range(0, 1800, 30)), total_pixels=total, sample_fps=2.0)
+    n = len(p.sampled_indices)
+    assert p.resized == oracle.smart_resize(H, W, total_pixels=total, n=n)
+    assert p.grid_thw == oracle.grid_thw(n, *p.resized)
+
+
+def test_c3_total_pixels_variant(fc):
+    wl = synth.CONFIGS["c3"]
+    p = plan_of(fc, wl.width, wl.height, wl.num_frames, wl.gop_start, wl.fps, sample_fps=1.0,
+                total_pixels=90_316_800)
+    assert p.resized == (392, 728) and p.grid_thw == (300, 28, 52) and p.token_rows == 436_800
+
+
+def test_fractional_fps_sweep_matches_oracle(fc, oracle):
+    """Q20 through the product: rational source rates (29.97 = 30000/1001, ...)
+    x sampling rates x lengths -- fc_plan's indices equal the oracle's (which
+    is pinned to HF's sample_frames up to the documented arange-length quirk)."""
+    from fractions import Fraction
+    rates = [Fraction(24), Fraction(25), Fraction(30), Fraction(60), Fraction(30000, 1001), Fraction(24000, 1001),
+             Fraction(60000, 1001)]
+    cases = 0
+    for N in list(range(2, 600, 11)) + [1453, 1800, 4000]:
+        for r in rates:
+            for fps in (0.5, 1.0, 2.0):
+                try:
+                    want = oracle.sample_indices(N, r, fps)
+                except ValueError:
+                    with pytest.raises(fc.FcError):
+                        plan_of(fc, 64, 48, N, [0], fps=(r.numerator, r.denominator), sample_fps=fps)
+                    continue
+                p = plan_of(fc, 64, 48, N, [0], fps=(r.numerator, r.denominator), sample_fps=fps)
+                assert p.sampled_indices == want, (N, r, fps)
+                cases += 1
+    assert cases > 1000
+
+
+# ------------------------------------------------ a10 exchange schedule (VERDICT r1)
+def _run_schedules(fc, plan, kind, elem):
+    """Execute every rank's fc_exchange_schedule on host byte buffers (what
+    fc_gather / fc_scatter_columns hand to NCCL) and return the receive
+    buffers.  Send buffers: gather -> each rank's row shard of a reference
+    token array; colsplit -> each rank's [W][rows][C] column blocks."""
+    W = plan.world_size
+    rows = plan.token_rows
+    rng = np.random.default_rng(rows + W)
+    full = rng.integers(0, 256, size=(rows, 1176 * elem), dtype=np.uint8)
+    rps = plan.ranks()
+    C = 1176 // W
+    send, recv = [], []
+    for r, rp in enumerate(rps):
+        mine = full[rp["row_begin"]:rp["row_end"]]
+        if kind == "gather":
+            send.append(mine.tobytes())
+            recv.append(bytearray(rows * 1176 * elem) if r == plan.cfg.encoder_rank else bytearray(0))
+        else:
+            f32 = mine.view(np.float32)  # [rows_r][1176]
+            blocks = np.stack([f32[:, j * C:(j + 1) * C] for j in range(W)]) if len(f32) else np.zeros((W, 0, C))
+            send.append(np.ascontiguousarray(blocks, dtype=np.float32).tobytes())
+            recv.append(bytearray(rows * C * 4))
+    scheds = [fc.exchange_schedule(plan, r, kind) for r in range(W)]
+    covered = [np.zeros(len(recv[r]), dtype=np.int32) for r in range(W)]
+    for r, xs in enumerate(scheds):
+        for x in xs:
+            if x["dir"] == "local":
+                assert x["peer"] == r
+                recv[r][x["dst_offset"]:x["dst_offset"] + x["bytes"]] = \
+                    send[r][x["src_offset"]:x["src_offset"] + x["bytes"]]
+                covered[r][x["dst_offset"]:x["dst_offset"] + x["bytes"]] += 1
+            elif x["dir"] == "send":
+                p = x["peer"]
+                match = [y for y in scheds[p] if y["dir"] == "recv" and y["peer"] == r]
+                assert len(match) == 1 and match[0]["bytes"] == x["bytes"], (r, p)
+                y = match[0]
+                recv[p][y["dst_offset"]:y["dst_offset"] + y["bytes"]] = \
+                    send[r][x["src_offset"]:x["src_offset"] + x["bytes"]]
+                covered[p][y["dst_offset"]:y["dst_offset"] + y["bytes"]] += 1
+            else:  # every receive has exactly one matching send
+                assert sum(1 for y in scheds[x["peer"]] if y["dir"] == "send" and y["peer"] == r) == 1
+            assert 0 <= x["src_offset"] and x["bytes"] > 0
+    return full, recv, covered
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_exchange_schedules_assemble_the_single_gpu_tensor(fc, seed):
+    """fc_gather's and fc_scatter_columns' transfer lists, executed on host
+    buffers: the encoder's buffer equals the single-GPU token array (every
+    byte written exactly once, nothing else); after the column split rank j
+    holds columns [jC, (j+1)C) of every row.  Random GOP layouts, explicit
+    selections with method-b tails and padding, idle ranks, encoder != 0."""
+    rng = random.Random(seed)
+    N, starts = _random_video(rng)
+    W = rng.choice([1, 2, 3, 4, 6, 7, 8])
+    k = rng.randint(1, N)
+    expl = sorted(rng.sample(range(N), k))
+    enc = rng.randrange(W)
+    tok = rng.choice(["f32", "bf16", "u8"])
+    p = plan_of(fc, 56, 56, N, starts, world_size=W, encoder_rank=enc, sampling="explicit", explicit_indices=expl,
+                token_dtype=tok)
+    elem = {"f32": 4, "bf16": 2, "u8": 1}[tok]
+    full, recv, covered = _run_schedules(fc, p, "gather", elem)
+    assert bytes(recv[enc]) == full.tobytes()
+    assert (covered[enc] == 1).all()
+    if 1176 % W == 0 and tok == "f32":
+        full, recv, covered = _run_schedules(fc, p, "colsplit", 4)
+        C = 1176 // W
+        f32 = full.view(np.float32)
+        for j in range(W):
+            got = np.frombuffer(bytes(recv[j]), dtype=np.float32).reshape(p.token_rows, C)
+            np.testing.assert_array_equal(got, f32[:, j * C:(j + 1) * C])
+            assert (covered[j] == 1).all()
+
+
+def test_exchange_schedule_config_sizes(fc):
+    """SURVEY 8(e) exchange sizes: c2 at W=8 moves 704.5 MB of fp32 rows into
+    the encoder (1/8 of the 812.9 MB stays local), 4x less as u8 codes."""
+    wl = synth.CONFIGS["c2"]
+    for tok, mb in (("f32", 704.5), ("u8", 176.1)):
+        p = plan_of(fc, wl.width, wl.height, wl.num_frames, wl.gop_start, wl.fps, world_size=8, token_dtype=tok)
+        into = sum(x["bytes"] for x in fc.exchange_schedule(p, 0, "gather") if x["dir"] == "recv")
+        assert abs(into / 1e6 - mb) < 0.1, into
+
+
+def test_exchange_schedule_errors(fc):
+    p = plan_of(fc, 64, 48, 8, [0], world_size=5)
+    with pytest.raises(fc.FcError) as e:
+        fc.exchange_schedule(p, 5)
+    assert e.value.name == "FC_ERR_RANK"
+    with pytest.raises(fc.FcError) as e:  # 1176 % 5 != 0
+        fc.exchange_schedule(p, 0, "colsplit")
+    assert e.value.name == "FC_ERR_UNSUPPORTED"

@@ -1,6 +1,8 @@
 """Small runs of every kernel path for compute-sanitizer (memcheck / racecheck /
-synccheck / initcheck): fused kernel fp32 + debug + bf16 + u8 codes, a batch,
-a >120-frame launch (device descriptor), I420 surfaces, and fc_expand_tokens."""
+synccheck / initcheck): the tcgen05 kernel (fp32 + debug, batch, >120-frame
+launch) and the mma.sync kernel (the same with FC_TC=0, plus bf16, u8 codes,
+paged output incl. first_offset 0 with rows a multiple of the page size,
+column split, I420 surfaces) and fc_expand_tokens."""
 import os
 import sys
 
@@ -21,19 +23,38 @@ def run(W, H, N, gops, **cfg):
     return plan, surf, dev
 
 
+def common():
+    plan, surf, _ = run(320, 240, 120, [0], sample_fps=2.0)
+    fc.preprocess(plan, 0, surf)
+    fc.preprocess_debug(plan, 0, surf)
+    jobs = [run(256, 144, 60, [0, 30], sample_fps=2.0) for _ in range(3)]
+    fc.preprocess_batch([(p, 0, s) for p, s, _ in jobs])
+    planL, surfL, _ = run(64, 48, 300, list(range(0, 300, 30)), sampling="explicit",
+                          explicit_indices=list(range(0, 260, 2)))
+    fc.preprocess(planL, 0, surfL)  # 130 frames: tensor maps in the device descriptor
+    plan3, surf3, _ = run(1280, 720, 60, [0, 30], sampling="explicit", explicit_indices=[0, 5, 9, 40])
+    fc.preprocess(plan3, 0, surf3)
+    torch.cuda.synchronize()
+
+
+common()  # tcgen05 kernel (default for NV12 / fp32)
+os.environ["FC_TC"] = "0"
+common()  # the same workload through the mma.sync kernel
 plan, surf, _ = run(320, 240, 120, [0], sample_fps=2.0)
-fc.preprocess(plan, 0, surf)
-fc.preprocess_debug(plan, 0, surf)
+# paged output: first_offset 0, 2240 rows = 35 pages of 64 (the last thread rows past the write)
+pool = torch.zeros((40, 64, 1176), dtype=torch.float32, device="cuda")
+fc.preprocess_paged(plan, 0, surf, pool, list(range(35)), 0)
+fc.preprocess_paged(plan, 0, surf, pool, list(range(3, 39)), 37)
+planC, surfC, _ = run(320, 240, 300, list(range(0, 300, 30)), sample_fps=2.0, world_size=8)
+for r in range(8):
+    if planC.rank(r)["row_end"] > planC.rank(r)["row_begin"]:
+        fc.preprocess_colsplit(planC, r, surfC)
 plan16, surf16, _ = run(200, 120, 40, [0, 20], sampling="explicit", explicit_indices=[1, 5, 9], token_dtype="bf16")
 fc.preprocess(plan16, 0, surf16)
 plan8, surf8, _ = run(320, 240, 120, [0], sample_fps=2.0, token_dtype="u8")
 codes = fc.preprocess(plan8, 0, surf8)
 fc.expand_tokens(plan8, codes)
 fc.expand_tokens(plan8, codes, out_dtype="bf16")
-jobs = [run(256, 144, 60, [0, 30], sample_fps=2.0) for _ in range(3)]
-fc.preprocess_batch([(p, 0, s) for p, s, _ in jobs])
-planL, surfL, _ = run(64, 48, 300, list(range(0, 300, 30)), sampling="explicit", explicit_indices=list(range(0, 260, 2)))
-fc.preprocess(planL, 0, surfL)  # 130 frames: tensor maps in the device descriptor
 plan224, surf224, _ = run(1920, 1080, 8, [0], sampling="explicit", explicit_indices=[0, 3],
                           resized_height=224, resized_width=224)
 fc.preprocess(plan224, 0, surf224)  # KSH=KSV=3, 28-column strips
