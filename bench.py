@@ -192,6 +192,15 @@ def run_ours(args):
     wl = synth.CONFIGS[args.config]
     clips = wl.clips                              # c5: 64 independent requests per step
     meta = workload_meta(fc, wl)
+    # throughput mode (c5) at N>1 is "replicas only": whole clips
+    # are placed on GPUs by LPT on their pairs (fc_assign_requests), each GPU
+    # runs ONE batched launch over its clips, and nothing is exchanged
+    replicas = clips > 1 and world > 1
+    clip_ids = list(range(clips))
+    if replicas:
+        pairs = [fc.Plan(meta, fc.ModelCfg(sample_fps=wl.sample_fps)).grid_thw[0]] * clips
+        placement = fc.assign_requests(pairs, world)
+        clip_ids = [c for c in range(clips) if placement[c] == rank]
     # N>1 with the u8 exchange (NEXT-1, default): ranks produce u8 codes, the
     # gather moves 1176-byte rows, the encoder expands them to tokens
     u8x = world > 1 and args.exchange == "u8"
@@ -200,15 +209,20 @@ def run_ours(args):
     colx = world > 1 and args.exchange == "colsplit"
     if colx and (clips != 1 or args.tokens != "f32"):
         raise SystemExit("--exchange colsplit: single-request configs, f32 tokens")
-    cfg = fc.ModelCfg(world_size=world, sample_fps=wl.sample_fps, token_dtype="u8" if u8x else args.tokens,
-                      color=args.color, surface_format=args.surface)
+    if replicas:
+        u8x = colx = False
+    cfg = fc.ModelCfg(world_size=1 if replicas else world, sample_fps=wl.sample_fps,
+                      token_dtype="u8" if u8x else args.tokens, color=args.color, surface_format=args.surface)
     tok_bytes = 2 if args.tokens == "bf16" else 4
     plan0 = fc.Plan(meta, cfg)
-    rp = plan0.rank(rank)
+    rp = plan0.rank(0 if replicas else rank)
     n_all = plan0.num_sampled * clips
+    clips_all = clips
+    if replicas:
+        clips = len(clip_ids)  # this rank's clips
     # this rank's frames (global indices) -- only those are materialised
     my_frames = plan0.sampled_indices[rp["sampled_begin"]:rp["sampled_begin"] + rp["sampled_count"]]
-    hosts = [synth.frames_nv12(wl, my_frames, "natural", clip=c) for c in range(clips)]
+    hosts = [synth.frames_nv12(wl, my_frames, "natural", clip=c) for c in clip_ids]
     if args.surface == "i420":  # the same samples as planar Y, U, V surfaces
         hosts = [{f: synth.nv12_to_i420(y, uv, wl.width, noise_seed=f) for f, (y, uv) in h.items()} for h in hosts]
 
@@ -231,10 +245,11 @@ def run_ours(args):
                         device="cuda") for _ in range(clips)]
     mines = [torch.empty((plan0.token_rows, 1176 // world), dtype=torch.float32, device="cuda") if colx else None
              for _ in range(clips)]
-    comm = fc.NcclComm(rank, world) if world > 1 else None
+    comm = fc.NcclComm(rank, world) if world > 1 and not replicas else None
+    xrank = 0 if replicas else rank  # the plan rank this process runs
     enc = cfg.encoder_rank
     fulls = [torch.empty((plan0.token_rows, 1176), dtype=xdt, device="cuda")
-             if (world > 1 and rank == enc and not colx) else None for _ in range(clips)]
+             if (world > 1 and rank == enc and not colx and not replicas) else None for _ in range(clips)]
     toks = [torch.empty((plan0.token_rows, 1176), dtype=tdt, device="cuda")
             if (u8x and rank == enc) else None for _ in range(clips)]
     stream = torch.cuda.current_stream()
@@ -254,16 +269,16 @@ def run_ours(args):
         plans_keep.append(plans)
         if ev_a is not None:
             ev_a.record(stream)
-        if rows:
+        if rows and clips:
             if colx:
                 fc.preprocess_colsplit(plans[0], rank, surfs[0], outs[0])  # a5-a9, column-block epilogue
-            elif clips == 1:
-                fc.preprocess(plans[0], rank, surfs[0], outs[0])   # a5-a9 (one launch)
+            elif clips == 1 and not replicas:
+                fc.preprocess(plans[0], xrank, surfs[0], outs[0])   # a5-a9 (one launch)
             else:  # a5-a9 for every request in ONE launch (same shape)
-                fc.preprocess_batch([(pl, rank, sf) for pl, sf in zip(plans, surfs)], outs)
+                fc.preprocess_batch([(pl, xrank, sf) for pl, sf in zip(plans, surfs)], outs)
         if ev_b is not None:
             ev_b.record(stream)
-        if world > 1:
+        if world > 1 and not replicas:
             exchange(plans)                        # a10
         if len(plans_keep) > 64:
             del plans_keep[:32]                   # older plans' work has long completed
@@ -282,33 +297,38 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sevs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]  # step boundaries
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = fc.lib().fc_kernel_launches()
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         t0.record(stream)
         for k in range(args.steps):
+            sevs[k].record(stream)
             step(keep, *evs[k])
+        sevs[args.steps].record(stream)
         t1.record(stream)
         torch.cuda.synchronize()
     launches = fc.lib().fc_kernel_launches() - launches0
     if world > 1:
         dist.barrier()
     total_ms = t0.elapsed_time(t1)
-    kern_ms = [a.elapsed_time(b) for a, b in evs] if rows else [0.0]
+    kern_ms = [a.elapsed_time(b) for a, b in evs] if (rows and clips) else [0.0]
     kern_avg = sum(kern_ms) / len(kern_ms)
+    step_ms = [sevs[k].elapsed_time(sevs[k + 1]) for k in range(args.steps)]
     if os.environ.get("FC_BENCH_STEPS"):  # diagnostics: per-step kernel times
         print("kernel ms per step:", " ".join(f"{x:.3f}" for x in kern_ms), file=sys.stderr)
     # max over ranks
-    stats = torch.tensor([total_ms, kern_avg], dtype=torch.float64, device="cuda")
+    stats = torch.tensor([total_ms, kern_avg, statistics.median(step_ms), min(step_ms), statistics.median(kern_ms),
+                          min(kern_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.MAX)
-    total_ms, kern_max = stats.tolist()
+    total_ms, kern_max, step_med, step_min, kern_med, kern_min = stats.tolist()
     ms_per_step = total_ms / args.steps
 
     # gather alone (N>1), timed separately for the NVLink report
     gather = None
-    if world > 1:
+    if world > 1 and not replicas:
         g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dist.barrier()
         torch.cuda.synchronize()
@@ -370,21 +390,21 @@ def run_ours(args):
         plans = [fc.Plan(meta, cfg) for _ in range(clips)]
         keep.append(plans)
         stream.wait_event(up_done[k & 1])
-        if rows:
+        if rows and clips:
             if colx:
                 fc.preprocess_colsplit(plans[0], rank, sf_set[0], outs[0])
-            elif clips == 1:
-                fc.preprocess(plans[0], rank, sf_set[0], outs[0])
+            elif clips == 1 and not replicas:
+                fc.preprocess(plans[0], xrank, sf_set[0], outs[0])
             else:
-                fc.preprocess_batch([(pl, rank, sf) for pl, sf in zip(plans, sf_set)], outs)
+                fc.preprocess_batch([(pl, xrank, sf) for pl, sf in zip(plans, sf_set)], outs)
         used[k & 1].record(stream)
-        if world > 1:
+        if world > 1 and not replicas:
             exchange(plans)
         if colx:  # the first row of this rank's column slice
             res_host[0][:1176 // world].copy_(mines[0][0], non_blocking=True)
-        elif world == 1 or rank == enc:  # one token row of every request's result back to the host
+        elif world == 1 or replicas or rank == enc:  # one token row of every request's result back to the host
             for c in range(clips):
-                src = (toks[c] if u8x else fulls[c]) if world > 1 else outs[c]
+                src = (toks[c] if u8x else fulls[c]) if (world > 1 and not replicas) else outs[c]
                 res_host[c].copy_(src[0], non_blocking=True)
 
     for k in range(2):  # warm-up of both surface sets
@@ -407,6 +427,43 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = e2e_ms.item()
+
+    # e2e with the FULL result read back to the host every step (host -> host;
+    # the default e2e keeps the tokens on the GPU for the encoder and reads one
+    # row back).  Only where the result fits a 2 GiB pinned buffer.
+    full_rb = None
+    results = []
+    if colx:
+        results = [mines[0]]
+    elif world == 1 or replicas:
+        results = outs[:clips]
+    elif rank == enc:
+        results = [(toks[c] if u8x else fulls[c]) for c in range(clips)]
+    rb_bytes = sum(r.numel() * r.element_size() for r in results)
+    # the same decision on every rank (the exchange inside e2e_step is collective)
+    if clips_all * plan0.token_rows * 1176 * tok_bytes <= (2 << 30):
+        rb_host = [torch.empty(r.shape, dtype=r.dtype).pin_memory() for r in results]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        cstream.wait_event(f0)
+        upload(0)
+        for k in range(3):
+            if k + 1 < 3:
+                upload(k + 1)
+            e2e_step(k, keep)
+            for hst, r in zip(rb_host, results):
+                hst.copy_(r, non_blocking=True)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        frb = torch.tensor([f0.elapsed_time(f1) / 3], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(frb, op=dist.ReduceOp.MAX)
+        full_rb = {"value": round(n_all / (frb.item() * 1e-3), 2), "unit": "frames/s",
+                   "ms_per_step": round(frb.item(), 3), "h2d_bytes_per_step": None,
+                   "d2h_bytes_per_step": rb_bytes}
 
     if rank == 0:
         peak, peak_kind = load_peaks()
@@ -437,13 +494,19 @@ def run_ours(args):
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {wl.note}", "frames": n_all, "requests": clips,
                        "resized_hw": list(plan0.resized), "grid_thw": list(plan0.grid_thw),
-                       "token_bytes": clips * plan0.token_rows * 1176 * tok_bytes, "parallelism": f"gop-dp{world}",
+                       "token_bytes": clips_all * plan0.token_rows * 1176 * tok_bytes,
+                       "parallelism": (f"replicas{world} (whole clips, LPT)" if replicas else f"gop-dp{world}"),
                        "color": args.color, "surface": args.surface,
                        "l2": "per-step inputs+outputs (1.19 GB for c2) exceed the 126 MB L2; no flush",
                        "kernel_ms_avg": round(kern_max if world > 1 else kern_avg, 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": abytes, **({"issue": issue} if issue else {})},
+            "step_ms": {"mean": round(ms_per_step, 4), "median": round(step_med, 4), "min": round(step_min, 4),
+                        "kernel_mean": round(kern_max if world > 1 else kern_avg, 4),
+                        "kernel_median": round(kern_med, 4), "kernel_min": round(kern_min, 4),
+                        "note": "per-step CUDA events on the launching stream; max over ranks"},
+            "preprocess_ms_max_over_ranks": round(kern_max if world > 1 else kern_avg, 4),
             "plan_host_us": round(plan_us, 1),
             "gpu_launches": int(launches),  # fc_kernel_launches() delta over the timed region (this rank)
             "e2e": {"value": round(n_all / (e2e_ms * 1e-3), 2), "unit": "frames/s", "ms_per_step": round(e2e_ms, 3),
@@ -452,14 +515,20 @@ def run_ours(args):
         }
         if gather is not None:
             line["gather"] = gather
+        if full_rb is not None:  # the same e2e with the whole token tensor read back (host -> host)
+            full_rb["h2d_bytes_per_step"] = h2d
+            line["e2e_full_readback"] = full_rb
         if world == 1 and not args.no_cpu_baseline:
             cores = len(os.sched_getaffinity(0))
             pairs = min(plan0.grid_thw[0], 60)
             dt, f = oracle_sample(wl, pairs, cores, args.color)
+            dt1, f1 = oracle_sample(wl, 1, 1, args.color)  # one temporal pair on one core
             line["cpu_baseline"] = {"value": round(f / dt, 3), "unit": "frames/s", "cores": cores,
                                     "kind": "oracle",
                                     "sample": f"{f} sampled frames ({pairs} temporal pairs) of {args.config}, "
-                                              f"natural content, {dt:.1f} s wall on {cores} threads"}
+                                              f"natural content, {dt:.1f} s wall on {cores} threads",
+                                    "single_core": {"value": round(f1 / dt1, 3), "unit": "frames/s", "cores": 1,
+                                                    "sample": f"{f1} sampled frames (1 temporal pair), {dt1:.2f} s"}}
         print(json.dumps(line), flush=True)
     if comm is not None:
         comm.close()

@@ -40,7 +40,7 @@ extern "C" {
 
 #define FC_ABI_VERSION 4  /* 2: token_dtype + color in fc_model_cfg; tokens as void*
                              3: surface_format in fc_model_cfg, v plane in the surface
-                             4: fc_exchange_schedule, fc_last_kernel */
+                             4: fc_exchange_schedule, fc_last_kernel, fc_assign_requests */
 #define FC_TOKEN_COLS 1176 /* 3 channels * 2 (temporal patch) * 14 * 14 */
 
 typedef enum {
@@ -189,6 +189,19 @@ typedef struct {
 } fc_rank_plan;
 
 fc_status fc_plan_rank(const fc_plan_t* plan, int32_t rank, fc_rank_plan* out);
+
+/* fc_assign_requests -- throughput mode (many
+ * independent requests, "replicas only"): place whole requests on GPUs by LPT
+ * (longest processing time first) on their temporal-pair counts; no request
+ * is split, so no exchange is needed (the per-request GOP split of P:339-340
+ * is for latency mode).
+ *   pairs:   host array [n], each request's temporal pairs (its work), >= 0
+ *   rank_of: host array [n], written: the GPU of each request
+ * Requests are taken in decreasing pairs (ties: lower index first), each to
+ * the currently least-loaded rank (ties: lower rank); makespan <= 4/3 of the
+ * optimum (Graham).  Host only.  n < 0, world < 1 or NULL arrays with n > 0 ->
+ * FC_ERR_INVALID_ARG. */
+fc_status fc_assign_requests(const int64_t* pairs, int32_t n, int32_t world, int32_t* rank_of);
 
 /* One decoded frame in device memory (layout: the plan's cfg.surface_format).
  *   FC_SURFACE_NV12: luma plane y (height rows x pitch_y bytes) and the
@@ -359,9 +372,10 @@ int32_t fc_abi_version(void);
 uint64_t fc_kernel_launches(void);
 
 /* Which fused kernel the calling thread's last successful fc_preprocess*
- * launch used: FC_KERNEL_TC (the tcgen05 kernel: NV12 surfaces, fp32 tokens,
- * strip windows up to 255 source columns / 128 source rows per 16 output rows)
- * or FC_KERNEL_MMA (the mma.sync kernel: every other shape and variant);
+ * launch used: FC_KERNEL_MMA (the mma.sync kernel, the default for every
+ * request) or FC_KERNEL_TC (the tcgen05 kernel, selected with the environment
+ * variable FC_TC=1 for NV12 surfaces, fp32 tokens and strip windows up to 255
+ * source columns / 128 source rows per 16 output rows);
  * FC_KERNEL_NONE before any launch.  Thread-local, no CUDA call. */
 typedef enum { FC_KERNEL_NONE = 0, FC_KERNEL_TC = 1, FC_KERNEL_MMA = 2 } fc_kernel_id;
 int32_t fc_last_kernel(void);

@@ -22,7 +22,7 @@ from ._native import FcError, FC_TOKEN_COLS, check, lib
 
 __all__ = ["VideoMeta", "ModelCfg", "Plan", "SurfaceTable", "preprocess", "preprocess_debug", "preprocess_batch",
            "expand_tokens", "preprocess_paged",
-           "NcclComm", "gather", "exchange_schedule", "last_kernel", "FcError", "FC_TOKEN_COLS", "lib"]
+           "NcclComm", "gather", "exchange_schedule", "last_kernel", "assign_requests", "FcError", "FC_TOKEN_COLS", "lib"]
 
 
 @dataclass
@@ -341,6 +341,16 @@ def exchange_schedule(plan: Plan, rank: int, kind: str = "gather") -> list[dict]
           "fc_exchange_schedule")
     return [dict(peer=t.peer, dir=_native.XFER_DIRS[t.dir], src_offset=t.src_offset, dst_offset=t.dst_offset,
                  bytes=t.bytes) for t in arr[: n.value]]
+
+
+def assign_requests(pairs: Sequence[int], world: int) -> list[int]:
+    """fc_assign_requests: GPU of each whole request (LPT on temporal pairs;
+    throughput mode, no exchange)."""
+    n = len(pairs)
+    arr = (ctypes.c_int64 * max(n, 1))(*pairs)
+    out = (ctypes.c_int32 * max(n, 1))()
+    check(lib().fc_assign_requests(arr, n, world, out), "fc_assign_requests")
+    return list(out)[:n]
 
 
 def last_kernel() -> str | None:

@@ -93,7 +93,8 @@ EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_g
            "fc_plan_rank", "fc_preprocess", "fc_preprocess_debug", "fc_preprocess_batch", "fc_nccl_unique_id",
            "fc_nccl_comm_init", "fc_nccl_comm_destroy", "fc_gather", "fc_status_string", "fc_last_error",
            "fc_abi_version", "fc_kernel_launches", "fc_expand_tokens", "fc_preprocess_paged",
-           "fc_preprocess_colsplit", "fc_scatter_columns", "fc_exchange_schedule", "fc_last_kernel"]
+           "fc_preprocess_colsplit", "fc_scatter_columns", "fc_exchange_schedule", "fc_last_kernel",
+           "fc_assign_requests"]
 
 _lib = None
 
@@ -139,6 +140,7 @@ def lib() -> ctypes.CDLL:
     L.fc_kernel_launches.argtypes = []
     L.fc_kernel_launches.restype = ctypes.c_uint64
     L.fc_exchange_schedule.argtypes = [vp, i32, ctypes.c_int, ctypes.POINTER(TransferC), i32, ctypes.POINTER(i32)]
+    L.fc_assign_requests.argtypes = [ctypes.POINTER(ctypes.c_int64), i32, i32, ctypes.POINTER(ctypes.c_int32)]
     L.fc_last_kernel.argtypes = []
     L.fc_last_kernel.restype = ctypes.c_int32
     for name in EXPORTS:

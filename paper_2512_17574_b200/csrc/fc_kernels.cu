@@ -488,11 +488,12 @@ cudaMemPool_t descriptor_pool(int dev) {
 static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, uint8_t* dbg_src,
                              uint8_t* dbg_rs, const fc_paged_tokens* paged = nullptr, bool colsplit = false,
                              bool dry = false) {
-  // the tcgen05 kernel (fc_tc.cu) takes every NV12 / fp32 request whose
-  // windows fit its shared-memory plan; FC_TC=0 forces this kernel (A/B runs)
+  // FC_TC=1 routes NV12 / fp32 requests whose windows fit its shared-memory
+  // plan to the tcgen05 kernel (fc_tc.cu); by default this kernel runs them:
+  // it is faster on every BASELINE config
   if (!paged && !colsplit && P->cfg.token_dtype == FC_TOKENS_F32 && P->cfg.surface_format == FC_SURFACE_NV12) {
     const char* env = std::getenv("FC_TC");
-    if (!env || std::atoi(env) != 0) {
+    if (env && std::atoi(env) != 0) {
       bool handled = false;
       const fc_status st = launch_tc(P, jobs, stream, dbg_src, dbg_rs, &handled, dry);
       if (handled) return st;

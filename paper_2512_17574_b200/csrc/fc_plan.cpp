@@ -551,6 +551,25 @@ fc_status fc_plan_rank(const fc_plan_t* P, int32_t rank, fc_rank_plan* out) {
   return FC_OK;
 }
 
+fc_status fc_assign_requests(const int64_t* pairs, int32_t n, int32_t world, int32_t* rank_of) {
+  if (n < 0 || world < 1 || (n > 0 && (!pairs || !rank_of))) return fail(FC_ERR_INVALID_ARG, "assign_requests arguments");
+  std::vector<int32_t> order(static_cast<size_t>(n));
+  for (int32_t i = 0; i < n; ++i) {
+    if (pairs[i] < 0) return fail(FC_ERR_INVALID_ARG, "negative pair count");
+    order[static_cast<size_t>(i)] = i;
+  }
+  std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return pairs[a] > pairs[b]; });
+  std::vector<int64_t> load(static_cast<size_t>(world), 0);
+  for (int32_t i : order) {
+    int32_t best = 0;
+    for (int32_t r = 1; r < world; ++r)
+      if (load[static_cast<size_t>(r)] < load[static_cast<size_t>(best)]) best = r;
+    rank_of[i] = best;
+    load[static_cast<size_t>(best)] += pairs[i];
+  }
+  return FC_OK;
+}
+
 const char* fc_status_string(fc_status s) {
   switch (s) {
     case FC_OK: return "FC_OK";

@@ -56,6 +56,7 @@ struct TcTables {
   int32_t* vys = nullptr;
   int32_t* vcl = nullptr;
   uint32_t* lut2 = nullptr;
+  std::vector<int32_t> hvys, hvcl;  // host copies (the kernel parameters carry them too)
 };
 
 struct TcKey {
@@ -129,7 +130,7 @@ fc_status build(const fc_plan_s* P, TcTables* t) {
     t->why = "vertical window wider than 128 source rows per 16 output rows";
     return FC_OK;
   }
-  t->NCH = bspan + 2;  // >= span + 1: the ring-free wait never waits on a band that needs the chunk being written
+  t->NCH = std::max(3, bspan + 2);  // >= span + 1: the ring-free wait never waits on a band that needs the chunk being written
   // bands whose windows start within any NCH consecutive chunks: in flight between the
   // V MMAs and the H epilogue's ring-free wait (<= kNVD barrier slots, two runs' worth)
   int inflight = 0;
@@ -137,6 +138,10 @@ fc_status build(const fc_plan_s* P, TcTables* t) {
     int n = 0;
     for (int hb2 = hb; hb2 < gh2 && (vys[2 * hb2] >> 4) < (vys[2 * hb] >> 4) + t->NCH; ++hb2) ++n;
     inflight = std::max(inflight, n);
+  }
+  if (t->NCH + 2 > kNHR) {
+    t->why = "ring deeper than the ready-barrier slots";
+    return FC_OK;
   }
   if (2 * inflight + 2 > kNVD) {
     t->why = "too many bands per ring window";
@@ -192,6 +197,8 @@ fc_status build(const fc_plan_s* P, TcTables* t) {
       const int v = std::min(255, std::max(0, (i - (kLut2Lo - 1)) >> 1));  // floor((a + 1) / 2), a = i - 97
       lut2[c * kLut2N + i] = P->lut_dev[c * 256 + v];
     }
+  t->hvys = vys;
+  t->hvcl = vcl;
   cudaError_t e = upload(&t->sx0, sx0);
   if (e == cudaSuccess) e = upload(&t->hB, hB);
   if (e == cudaSuccess) e = upload(&t->vB, vB);
@@ -260,7 +267,7 @@ fc_status launch_tc(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, ui
     *handled = true;
     return st;
   }
-  if (!t->ok || nsm < t->nstrips) return FC_OK;
+  if (!t->ok || nsm < t->nstrips || P->h2 / 28 > kMaxBands) return FC_OK;
   const bool verbose = std::getenv("FC_VERBOSE") != nullptr;
 
   static thread_local TcParams prm;  // ~31 KB: keep it off the stack
@@ -300,6 +307,8 @@ fc_status launch_tc(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, ui
         off = up1024(off + nbv * prm.bvb);
         const int off_ring = off;
         off += 24 * prm.sbo_v;
+        const int off_tab = off;
+        off += (3 * prm.gh2 * 4 + 15) & ~15;
         const int total = off + 1024;  // the kernel aligns its base up to 1024
         if (total <= max_smem) {
           smem = total;
@@ -312,10 +321,13 @@ fc_status launch_tc(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, ui
           prm.off_bh = off_bh;
           prm.off_bv = off_bv;
           prm.off_ring = off_ring;
+          prm.off_tab = off_tab;
         }
       }
   if (!smem) return FC_OK;
   *handled = true;
+  for (int i = 0; i < 2 * prm.gh2; ++i) prm.cvys[i] = static_cast<uint16_t>(t->hvys[i]);
+  for (int i = 0; i < prm.gh2; ++i) prm.cvcl[i] = static_cast<uint16_t>(t->hvcl[i]);
   prm.sx0 = t->sx0;
   prm.hB = t->hB;
   prm.vB = t->vB;
@@ -400,8 +412,8 @@ fc_status launch_tc(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, ui
     cudaFree(prof);
     struct Role { const char* name; int w0, w1; const char* sites; };
     const Role roles[] = {{"V-epi", 0, 8, "vfull"}, {"H-epi", 8, 11, "vdone hfull"}, {"H-epi'", 12, 15, "vdone hfull"},
-                          {"MMA", 11, 12, "bh hdone afull bvfull vempty | [5] H issue [6] V issue"},
-                          {"TMA", 15, 16, "bvempty rawempty"}, {"colour", 16, 24, "rawfull aempty"}};
+                          {"H-MMA", 11, 12, "bh hempty afull | [5] H issue"}, {"V-MMA", 23, 24, "- hready bvfull vempty | [6] V issue"},
+                          {"TMA", 15, 16, "bvempty rawempty"}, {"colour", 16, 23, "rawfull aempty"}};
     for (const Role& r : roles) {
       double acc[9] = {0};
       int n = 0;

@@ -60,9 +60,10 @@ constexpr int kHEpiWarpB = 12;  //   output groups {0,1} (8..10) / {2,3} (12..14
 constexpr int kHEpiWarps = 6;
 constexpr int kMmaWarp = 11;    // quarter 3: MMA issuer + TMEM owner
 constexpr int kTmaWarp = 15;    // TMA producer
-constexpr int kColWarp0 = 16;   // warps 16..23: colour
-constexpr int kColWarps = 8;
-constexpr int kWarps = kColWarp0 + kColWarps;
+constexpr int kColWarp0 = 16;   // warps 16..22: colour
+constexpr int kColWarps = 7;
+constexpr int kVMmaWarp = kColWarp0 + kColWarps;  // warp 23: V-pass MMA issuer (warp 11 issues the H pass)
+constexpr int kWarps = kVMmaWarp + 1;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kColThreads = 32 * kColWarps;
 constexpr int kChunk = 16;        // source rows per chunk
@@ -75,7 +76,8 @@ constexpr int kNVD = 16;            // V-done barrier slots (bands in flight, ho
 constexpr int kMaxBV = 4;           // B_V slots (bands of V weights in flight)
 constexpr int kLut2Lo = 97;         // doubled table: index a + 97 for a = floor(S / 2^21) in [-97, 606]
 constexpr int kLut2N = 704;
-constexpr int kMaxInline = 120;     // frames whose tensor maps travel in the kernel parameters
+constexpr int kMaxInline = 112;     // frames whose tensor maps travel in the kernel parameters
+constexpr int kMaxBands = 128;      // bands whose V window table travels in the kernel parameters
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kHacc = 0;          // H accumulators: columns [0, 384) (2 buffers of 192)
 constexpr uint32_t kVacc = 2 * kNH;    // V accumulators: columns [384, 480) (2 buffers of 48)
@@ -89,8 +91,10 @@ enum Bar : int {
   kBvFull = 20, kBvEmpty = 24,   // NBV <= 4
   kBhFull = 28,
   kVDone = 32,                   // kNVD slots
-  kNumBars = kVDone + kNVD
+  kHReady = kVDone + kNVD,       // kNHR slots: chunk cs's ring rows written (H epilogue -> V MMA warp)
+  kNumBars = kHReady + 16
 };
+constexpr int kNHR = 16;  // > NCH + 1 (host-checked): the V warp never lags a full lap of these
 
 // ring position of a pipeline: slot index and the parity of its lap
 struct Pipe {
@@ -109,7 +113,7 @@ struct TcParams {
   int KH, KV, BW, NCH, NR, NA, NBV, nchunks;
   int rawb, ahb, bvb;  // bytes per raw stage / A_H stage / B_V slot
   int sbo_a, sbo_v;    // A_H 8-row group stride; ring 16-column group stride
-  int off_lut, off_raw, off_ah, off_bh, off_bv, off_ring;  // shared-memory offsets (from the 1024-aligned base)
+  int off_lut, off_raw, off_ah, off_bh, off_bv, off_ring, off_tab;  // shared-memory offsets (1024-aligned base)
   const int32_t* sx0;    // [nstrips] 16-aligned first source column of each strip
   const uint8_t* hB;     // [nstrips][192 x KH] H weight digits, K-major core matrices
   const uint8_t* vB;     // [gh2][2][48 x KV]  V weight digits per half band
@@ -126,6 +130,11 @@ struct TcParams {
   unsigned long long* prof;  // FC_TC_PROF experiments: per warp 8 wait-cycle counters + total, or null
   int ablate;                // FC_TC_ABLATE experiments (PROF instance only): bits skip parts of the work
   const CUtensorMap* tmg;  // device copy of the maps or null -> tm
+  // V window starts / last chunks again, in the parameter (constant) bank: the
+  // MMA warp indexes them with warp-uniform band numbers, so the descriptors it
+  // builds from them stay in uniform registers (no per-MMA R2UR)
+  uint16_t cvys[2 * kMaxBands];
+  uint16_t cvcl[kMaxBands];
   CUtensorMap tm[2 * kMaxInline];
 };
 
@@ -177,6 +186,9 @@ __device__ __forceinline__ void ldtm8(uint32_t taddr, uint32_t (&r)[8]) {
 __device__ __forceinline__ void sts128(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
 }
+__device__ __forceinline__ void sts64(uint32_t addr, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
+}
 __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
@@ -205,7 +217,14 @@ __device__ __forceinline__ Range cta_range(const TcParams& p) {
 }
 
 // Chunk (source-row block) bounds of a run: chunks kfirst .. klast.
-__device__ __forceinline__ int run_kfirst(const TcParams& p, int hbA) { return __ldg(p.vys + 2 * hbA) >> 4; }
+// vys / vcl live in shared memory (copied at kernel start): every role reads
+// them in its loop, and an L2 round trip per band sat on the MMA issue path
+__device__ __forceinline__ int ld_tab(const int* a) { return *a; }
+struct Tabs {
+  const int* vys;  // [gh2][2]
+  const int* vcl;  // [gh2]
+};
+__device__ __forceinline__ int run_kfirst(const Tabs& T, int hbA) { return T.vys[2 * hbA] >> 4; }
 
 
 // Token base of a pair (batch launches: per-job bases).
@@ -228,6 +247,24 @@ __device__ __forceinline__ void wait_bar(uint64_t* bar, uint32_t parity) {
       "@!p bra TC_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity), "r"(0x989680)
       : "memory");
+}
+
+// wait with back-off sleeps: for roles that run ahead of the pipeline (TMA
+// refills, colour), where a few hundred ns of wake-up latency is hidden by the
+// stage buffers and the issue slots a poll loop burns are not
+__device__ __forceinline__ void wait_bar_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t done = 0;
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) break;
+    __nanosleep(ns);
+  }
 }
 
 // V epilogue for one (unit half H_, row group VH) of 8 output rows: combine
@@ -260,6 +297,15 @@ __global__ void __launch_bounds__(kThreads, 1) fc_tc_kernel(const __grid_constan
   // PROF instance: cycles each warp spends in each of its barrier waits (slot k per call site)
   unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const long long pt0 = PROF ? clock64() : 0;
+  auto WB = [&](uint64_t* bar, uint32_t parity, int k, uint32_t ns) {
+    if constexpr (PROF) {
+      const long long t = clock64();
+      wait_bar_backoff(bar, parity, ns);
+      pacc[k] += clock64() - t;
+    } else {
+      wait_bar_backoff(bar, parity, ns);
+    }
+  };
   auto W = [&](uint64_t* bar, uint32_t parity, int k) {
     if constexpr (PROF) {
       const long long t = clock64();
@@ -301,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) fc_tc_kernel(const __grid_constan
     }
     mbar_init(&bars[kBhFull], 1);
     for (int i = 0; i < kNVD; ++i) mbar_init(&bars[kVDone + i], 1);
+    for (int i = 0; i < kNHR; ++i) mbar_init(&bars[kHReady + i], kHEpiWarps);
     fence_mbar_init();
   }
   if (warp == kMmaWarp) {  // TMEM: 512 columns (one CTA per SM)
@@ -310,6 +357,9 @@ __global__ void __launch_bounds__(kThreads, 1) fc_tc_kernel(const __grid_constan
   }
   for (int i = tid; i < 3 * kLut2N; i += kThreads)
     reinterpret_cast<uint32_t*>(smem + p.off_lut)[i] = __ldg(p.lut2 + i);
+  int* tab = reinterpret_cast<int*>(smem + p.off_tab);
+  for (int i = tid; i < 3 * p.gh2; i += kThreads) tab[i] = i < 2 * p.gh2 ? __ldg(p.vys + i) : __ldg(p.vcl + i - 2 * p.gh2);
+  const Tabs T{tab, tab + 2 * p.gh2};
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -324,18 +374,23 @@ __global__ void __launch_bounds__(kThreads, 1) fc_tc_kernel(const __grid_constan
       mbar_arrive_expect_tx(&bars[kBhFull], bhb);
       bulk_g2s(smem + p.off_bh, p.hB + static_cast<size_t>(R.strip) * bhb, bhb, &bars[kBhFull]);
       Pipe rw, bv;  // producer waits on "empty" with the inverted parity: a fresh barrier passes lap 0
+      uint32_t jb = 0;  // band sequence number
       for (int i = R.i0; i < R.i1;) {
         const int pair = i / p.gh2, hbA = i - pair * p.gh2, hbB = min(p.gh2, hbA + (R.i1 - i));
-        int knext = run_kfirst(p, hbA);
+        int knext = run_kfirst(T, hbA);
         const CUtensorMap* m0 = &tm[4 * pair];
-        for (int hb = hbA; hb < hbB; ++hb) {
-          W(&bars[kBvEmpty + bv.i], bv.ph ^ 1, 0);
+        for (int hb = hbA; hb < hbB; ++hb, ++jb) {
+          // B_V slot reuse: the V MMAs of band jb - NBV are done (its V-done phase)
+          if (jb >= static_cast<uint32_t>(p.NBV)) {
+            const uint32_t jo = jb - p.NBV;
+            W(&bars[kVDone + (jo % kNVD)], (jo / kNVD) & 1, 0);
+          }
           mbar_arrive_expect_tx(&bars[kBvFull + bv.i], static_cast<uint32_t>(p.bvb));
           bulk_g2s(smem + p.off_bv + bv.i * p.bvb, p.vB + static_cast<size_t>(hb) * p.bvb, p.bvb, &bars[kBvFull + bv.i]);
           bv.next(p.NBV);
-          const int kl = __ldg(p.vcl + hb);
+          const int kl = ld_tab(T.vcl + hb);
           for (; knext <= kl; ++knext) {
-            W(&bars[kRawEmpty + rw.i], rw.ph ^ 1, 1);
+            WB(&bars[kRawEmpty + rw.i], rw.ph ^ 1, 1, 256);
             uint64_t* fb = &bars[kRawFull + rw.i];
             mbar_arrive_expect_tx(fb, static_cast<uint32_t>(2 * 24 * p.BW));
             uint8_t* dst = smem + p.off_raw + rw.i * p.rawb;
@@ -349,17 +404,18 @@ __global__ void __launch_bounds__(kThreads, 1) fc_tc_kernel(const __grid_constan
         i += hbB - hbA;
       }
     }
-  } else if (warp >= kColWarp0) {
+  } else if (warp >= kColWarp0 && warp < kColWarp0 + kColWarps) {
     // ------------------------------------------------------------------ colour (a5)
     const int ct = tid - 32 * kColWarp0;
     const int NKC = p.KH >> 4;
     const int items = 2 * kChunk * NKC;  // (frame, row, 16-pixel column group), column group fastest
     const int SX0 = __ldg(p.sx0 + R.strip);
-    // this thread's items (<= 2: KH <= 256): raw Y / UV offsets, A_H offset
-    int oy[2], ouv[2], oa[2];
-    bool last[2];
+    // this thread's items (KH <= 256: <= 512 items, <= kMaxItems per thread): raw Y / UV offsets, A_H offset
+    constexpr int kMaxItems = (2 * kChunk * 16 + kColThreads - 1) / kColThreads;
+    int oy[kMaxItems], ouv[kMaxItems], oa[kMaxItems];
+    bool last[kMaxItems];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
+    for (int e = 0; e < kMaxItems; ++e) {
       const int it = ct + e * kColThreads;
       const int r = it / NKC, kc = it - r * NKC, f = r >> 4, y = r & 15;
       oy[e] = f * 24 * p.BW + y * p.BW + 16 * kc;
@@ -368,18 +424,20 @@ __global__ void __launch_bounds__(kThreads, 1) fc_tc_kernel(const __grid_constan
       oa[e] = (m0 >> 3) * p.sbo_a + kc * kLboA + (m0 & 7) * 16;
       last[e] = kc == NKC - 1;
     }
-    const int nmine = (ct < items) + (ct + kColThreads < items);
+    int nmine = 0;
+#pragma unroll
+    for (int e = 0; e < kMaxItems; ++e) nmine += ct + e * kColThreads < items;
     Pipe rw, ab;
     for (int i = R.i0; i < R.i1;) {
       const int pair = i / p.gh2, hbA = i - pair * p.gh2, hbB = min(p.gh2, hbA + (R.i1 - i));
-      const int kf = run_kfirst(p, hbA), kl = __ldg(p.vcl + hbB - 1);
+      const int kf = run_kfirst(T, hbA), kl = ld_tab(T.vcl + hbB - 1);
       for (int k = kf; k <= kl; ++k) {
-        W(&bars[kRawFull + rw.i], rw.ph, 0);
-        W(&bars[kAEmpty + ab.i], ab.ph ^ 1, 1);
+        WB(&bars[kRawFull + rw.i], rw.ph, 0, 64);
+        WB(&bars[kAEmpty + ab.i], ab.ph ^ 1, 1, 64);
         const uint32_t raw = s_raw + rw.i * p.rawb;
         const uint32_t ah = s_ah + ab.i * p.ahb;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
+        for (int e = 0; e < kMaxItems; ++e) {
           if (e >= nmine || (PROF && (p.ablate & 2))) break;
           const uint4 Yv = lds128(raw + oy[e]);
           const uint4 UVv = lds128(raw + ouv[e]);
@@ -422,173 +480,218 @@ __global__ void __launch_bounds__(kThreads, 1) fc_tc_kernel(const __grid_constan
       i += hbB - hbA;
     }
   } else if (warp == kMmaWarp) {
-    // ------------------------------------------------------------------ MMA issuer (a6, a7)
-    // The whole warp runs this loop (warp-uniform control flow and values, so
-    // the descriptors live in uniform registers; per-MMA R2UR moves cost ~200
-    // cycles each, tools/ubench/tc05e.cu) and one elected lane issues.
+    // ------------------------------------------------------------------ MMA issuers (a6: warp 11, a7: warp 24)
+    // Each issuer warp runs its loop with all lanes (warp-uniform control flow
+    // and values, so the descriptors live in uniform registers: per-MMA R2UR
+    // moves cost ~200 cycles each, tools/ubench/tc05e.cu) and one elected lane
+    // issues.  The H and V streams are independent (the V pass reads the ring
+    // the H epilogue writes), so two warps issue them and neither's fixed
+    // per-block cost (elect, commit, waits) stalls the other.
     if (R.i0 < R.i1) {
+      // the CTA owns all 512 TMEM columns, so the allocation starts at lane 0,
+      // column 0: a compile-time accumulator base keeps the MMA operands uniform
+      if (tmem != 0) __trap();
+      constexpr uint32_t tmem0 = 0;
       constexpr uint32_t idH = idesc_i8(128, kNH, 0);
-      constexpr uint32_t idV = idesc_i8(128, kNV, 1);
+      const uint32_t sbo_b = static_cast<uint32_t>(p.KH / 16) * 128;
+      const int ksh = p.KH >> 5;
       W(&bars[kBhFull], 0, 0);
       tc_fence_after();
-      const uint32_t sbo_b = static_cast<uint32_t>(p.KH / 16) * 128;
-      const uint32_t sbo_bv = static_cast<uint32_t>(p.KV / 16) * 128;
-      const int ksh = p.KH >> 5, ksv = p.KV >> 5;
-      uint32_t hiss = 0, hseen = 0, j = 0;
-      Pipe ab, vb, bv;
-      auto wait_hdone = [&](uint32_t c) {  // the H epilogue has finished chunk c (and all before)
-        while (hseen <= c) {
-          W(&bars[kHEmpty + (hseen & 1)], (hseen >> 1) & 1, 1);
-          ++hseen;
-        }
-      };
-      auto issue_h = [&]() {
-        const uint32_t cs = hiss++, b = cs & 1;
-        W(&bars[kAFull + ab.i], ab.ph, 2);
-        if (cs >= 2) wait_hdone(cs - 2);
-        tc_fence_after();
-        const long long t0 = PROF ? clock64() : 0;
-        const uint32_t ah = s_ah + ab.i * p.ahb;
-        const uint32_t d = tmem + kHacc + b * kNH;
-        const int nk = (PROF && (p.ablate & 16)) ? 0 : ksh;
-        if (elect_one()) {
-          for (int kk = 0; kk < nk; ++kk)
-            mma_i8(d, sdesc(ah + kk * 2 * kLboA, kLboA, p.sbo_a), sdesc(s_bh + kk * 256, 128, sbo_b), idH, kk > 0);
-          mma_commit(&bars[kHFull + b]);
-          mma_commit(&bars[kAEmpty + ab.i]);
-        }
-        __syncwarp();
-        if (PROF) pacc[5] += clock64() - t0;
-        ab.next(p.NA);
-      };
+      uint32_t cs = 0;
+      Pipe ab;
       for (int i = R.i0; i < R.i1;) {
         const int pair = i / p.gh2, hbA = i - pair * p.gh2, hbB = min(p.gh2, hbA + (R.i1 - i));
-        const int kf = bcast(run_kfirst(p, hbA)), klast = bcast(__ldg(p.vcl + hbB - 1));
-        const uint32_t cs0 = hiss;  // sequence number of chunk kf
-        // ring slot of chunk kf (the ring restarts nowhere: slots follow the chunk sequence)
-        const int slot0 = static_cast<int>(cs0 % static_cast<uint32_t>(p.NCH));
-        int knext = kf;
+        const int kf = p.cvys[2 * hbA] >> 4, klast = p.cvcl[hbB - 1];
+        for (int k = kf; k <= klast; ++k, ++cs) {
+          const uint32_t b = cs & 1;
+          W(&bars[kAFull + ab.i], ab.ph, 2);
+          if (cs >= 2) W(&bars[kHEmpty + b], ((cs >> 1) & 1) ^ 1, 1);  // the H epilogue drained chunk cs - 2
+          tc_fence_after();
+          const long long t0 = PROF ? clock64() : 0;
+          const uint32_t ah = s_ah + ab.i * p.ahb;
+          const uint32_t d = tmem0 + kHacc + b * kNH;
+          const int nk = (PROF && (p.ablate & 16)) ? 0 : ksh;
+          if (elect_one()) {
+            for (int kk = 0; kk < nk; ++kk)
+              mma_i8(d, sdesc(ah + kk * 2 * kLboA, kLboA, p.sbo_a), sdesc(s_bh + kk * 256, 128, sbo_b), idH, kk > 0);
+            mma_commit(&bars[kHFull + b]);
+            mma_commit(&bars[kAEmpty + ab.i]);
+          }
+          __syncwarp();
+          if (PROF) pacc[5] += clock64() - t0;
+          ab.next(p.NA);
+        }
+        i += hbB - hbA;
+      }
+    }
+  } else if (warp == kVMmaWarp) {
+    if (R.i0 < R.i1) {
+      if (tmem != 0) __trap();
+      constexpr uint32_t tmem0 = 0;
+      constexpr uint32_t idV = idesc_i8(128, kNV, 1);
+      const uint32_t sbo_bv = static_cast<uint32_t>(p.KV / 16) * 128;
+      const int ksv = p.KV >> 5;
+      uint32_t cs0 = 0, hseen = 0, j = 0;
+      int slot0 = 0;  // ring slot of the run's first chunk (cs0 mod NCH)
+      Pipe vb, bv;
+      for (int i = R.i0; i < R.i1;) {
+        const int pair = i / p.gh2, hbA = i - pair * p.gh2, hbB = min(p.gh2, hbA + (R.i1 - i));
+        const int kf = p.cvys[2 * hbA] >> 4, klast = p.cvcl[hbB - 1];
+        // band tables one band ahead (parameter-bank loads: their latency hides behind the band's MMAs)
+        int ys0 = p.cvys[2 * hbA], ys1 = p.cvys[2 * hbA + 1], cl = p.cvcl[hbA];
         for (int hb = hbA; hb < hbB; ++hb, ++j) {
-          const int kl = bcast(__ldg(p.vcl + hb));
-          const int target = min(kl + 1, klast);  // one chunk of H look-ahead beside the band's V MMAs
-          for (; knext <= target; ++knext) issue_h();
-          wait_hdone(cs0 + static_cast<uint32_t>(kl - kf));
+          const int hn = min(hb + 1, p.gh2 - 1);
+          const int nys0 = p.cvys[2 * hn], nys1 = p.cvys[2 * hn + 1], ncl = p.cvcl[hn];
+          // the band's rows are in the ring: the H epilogue finished its last chunk (and all before)
+          const uint32_t c = cs0 + static_cast<uint32_t>(cl - kf);
+          while (hseen <= c) {
+            W(&bars[kHReady + (hseen % kNHR)], (hseen / kNHR) & 1, 1);
+            ++hseen;
+          }
           W(&bars[kBvFull + bv.i], bv.ph, 3);
           tc_fence_after();
           const uint32_t bvs = s_bv + bv.i * p.bvb;
-          // per half band and k-step: the ring address of the window's rows
-          // (chunk slot of the row, wrapped; the mirror slots keep a k-step contiguous)
-          uint32_t ra[2][4];
           const int nkv = (PROF && (p.ablate & 8)) ? 0 : ksv;
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int ys = bcast(__ldg(p.vys + 2 * hb + h));
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const int row = ys + 32 * kk;
-              int slot = slot0 + ((row >> 4) - kf);
-              slot -= slot >= p.NCH ? p.NCH : 0;
-              slot -= slot >= p.NCH ? p.NCH : 0;
-              ra[h][kk] = s_ring + (slot * 16 + (row & 15)) * 16;
-            }
-          }
+          // ring slot of each half band's first window chunk, and its row offset
+          int sl0 = slot0 + ((ys0 >> 4) - kf), sl1 = slot0 + ((ys1 >> 4) - kf);
+          while (sl0 >= p.NCH) sl0 -= p.NCH;
+          while (sl1 >= p.NCH) sl1 -= p.NCH;
+          const uint32_t ab0 = s_ring + (ys0 & 15) * 16, ab1 = s_ring + (ys1 & 15) * 16;
           for (int t = 0; t < 3; ++t)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               W(&bars[kVEmpty + vb.i], vb.ph ^ 1, 4);
               tc_fence_after();
               const long long t0 = PROF ? clock64() : 0;
-              const uint32_t d = tmem + kVacc + vb.i * kNV;
+              const uint32_t abase = (h ? ab1 : ab0) + 8 * t * p.sbo_v;
+              const uint32_t d = tmem0 + kVacc + vb.i * kNV;
               const uint32_t bh = bvs + h * kNV * p.KV;
               if (elect_one()) {
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                  if (kk < nkv)
-                    mma_i8(d, sdesc(ra[h][kk] + 8 * t * p.sbo_v, 128, p.sbo_v), sdesc(bh + kk * 256, 128, sbo_bv), idV,
-                           kk > 0);
+                // k-step kk starts 32*kk rows on: two chunks (slots) per step, same offset within the chunk
+                int sk = h ? sl1 : sl0;
+                for (int kk = 0; kk < nkv; ++kk) {
+                  mma_i8(d, sdesc(abase + sk * 256, 128, p.sbo_v), sdesc(bh + kk * 256, 128, sbo_bv), idV, kk > 0);
+                  sk += 2;
+                  sk -= sk >= p.NCH ? p.NCH : 0;
+                }
                 mma_commit(&bars[kVFull + vb.i]);
               }
               __syncwarp();
               if (PROF) pacc[6] += clock64() - t0;
               vb.next(2);
             }
-          if (elect_one()) {
-            mma_commit(&bars[kVDone + (j % kNVD)]);
-            mma_commit(&bars[kBvEmpty + bv.i]);
-          }
+          if (elect_one()) mma_commit(&bars[kVDone + (j % kNVD)]);  // ring free (H epilogue) and B_V slot free (TMA)
           __syncwarp();
           bv.next(p.NBV);
+          ys0 = nys0;
+          ys1 = nys1;
+          cl = ncl;
         }
+        const int nrun = klast - kf + 1;  // chunks of the run
+        cs0 += static_cast<uint32_t>(nrun);
+        slot0 += nrun;
+        while (slot0 >= p.NCH) slot0 -= p.NCH;
         i += hbB - hbA;
       }
     }
   } else if (warp >= kHEpiWarpA) {
     // ------------------------------------------------------------------ H epilogue (a6 -> ring)
     const int q = warp & 3;                      // TMEM lane quarter 0..2
-    const int g0 = warp >= kHEpiWarpB ? 2 : 0;   // this warp's 16-output groups g0, g0+1
+    // this warp's 8-output steps: outputs 0..31 (warps 8..10) / 32..55 (warps 12..14; 56..63 carry no weights)
+    const int h0 = warp >= kHEpiWarpB ? 4 : 0, nh = warp >= kHEpiWarpB ? 3 : 4;
     const int m = 32 * q + lane;                 // A row: plane ip = m / 16, source row y = m % 16
     const int ip = m >> 4, y = m & 15;
     const uint32_t tl = static_cast<uint32_t>(32 * q) << 16;
-    const uint32_t ringc = s_ring + (ip * 4 + g0) * p.sbo_v + y * 16;  // + slot * 256
+    const uint32_t ringc = s_ring + (ip * 4 + h0 / 2) * p.sbo_v + y * 16;  // + slot * 256
     uint32_t cs = 0, vseen = 0;
     int slot = 0;
     // band iterator for the ring-free condition: band bi, item position within its run
     int bi = R.i0, brun_end = R.i0, bkf = 0, bhb = 0;
     uint32_t bcs0 = 0, bnext_cs0 = 0;
+    // sequence number of band bi's first window chunk (past the CTA's last band: never)
+    auto band_cfirst = [&]() -> long long {
+      if (bi >= R.i1) return 1ll << 40;
+      if (bi == brun_end) {  // the iterator enters a new run
+        const int bp = bi / p.gh2, bh = bi - bp * p.gh2, be = min(p.gh2, bh + (R.i1 - bi));
+        bcs0 = bnext_cs0;
+        bkf = run_kfirst(T, bh);
+        bhb = bh;
+        bnext_cs0 = bcs0 + static_cast<uint32_t>(ld_tab(T.vcl + be - 1) - bkf + 1);
+        brun_end = bi + (be - bh);
+      }
+      return static_cast<long long>(bcs0) + (run_kfirst(T, bhb) - bkf);
+    };
+    long long ncf = band_cfirst();
     for (int i = R.i0; i < R.i1;) {
       const int pair = i / p.gh2, hbA = i - pair * p.gh2, hbB = min(p.gh2, hbA + (R.i1 - i));
-      const int kf = run_kfirst(p, hbA), kl = __ldg(p.vcl + hbB - 1);
+      const int kf = run_kfirst(T, hbA), kl = ld_tab(T.vcl + hbB - 1);
       for (int k = kf; k <= kl; ++k, ++cs) {
         // ring free: chunk cs overwrites chunk cs - NCH, so every band whose
         // window starts at or before chunk cs - NCH must have finished its V MMAs
-        while (bi < R.i1) {
-          if (bi == brun_end) {  // the iterator enters a new run
-            const int bp = bi / p.gh2, bh = bi - bp * p.gh2, be = min(p.gh2, bh + (R.i1 - bi));
-            bcs0 = bnext_cs0;
-            bkf = run_kfirst(p, bh);
-            bhb = bh;
-            bnext_cs0 = bcs0 + static_cast<uint32_t>(__ldg(p.vcl + be - 1) - bkf + 1);
-            brun_end = bi + (be - bh);
-          }
-          const uint32_t cfirst = bcs0 + static_cast<uint32_t>(run_kfirst(p, bhb) - bkf);
-          if (cfirst + static_cast<uint32_t>(p.NCH) > cs) break;
+        while (ncf + p.NCH <= static_cast<long long>(cs)) {
           W(&bars[kVDone + (vseen % kNVD)], (vseen / kNVD) & 1, 0);
           ++vseen;
           ++bi;
           ++bhb;
+          ncf = band_cfirst();
         }
         const uint32_t b = cs & 1;
         W(&bars[kHFull + b], (cs >> 1) & 1, 1);
         tc_fence_after();
-        const uint32_t taddr = tmem + tl + kHacc + b * kNH + 16 * g0;
+        // 8-output steps (tcgen05.ld x8 per digit), software-pipelined: the loads
+        // of step s+1 are in flight while step s is combined and packed
+        const uint32_t taddr = tmem + tl + kHacc + b * kNH + 8 * h0;
         const uint32_t rrow = ringc + slot * 256;
+        if (!(PROF && (p.ablate & 4))) {
+          uint32_t x0[8], x1[8], x2[8], y0[8], y1[8], y2[8];
+          auto load = [&](int st, uint32_t (&e0)[8], uint32_t (&e1)[8], uint32_t (&e2)[8]) {
+            ldtm8(taddr + 8 * st, e0);
+            ldtm8(taddr + kStripPad + 8 * st, e1);
+            ldtm8(taddr + 2 * kStripPad + 8 * st, e2);
+          };
+          // clip8 (R4) = sat_u8(S >> 22), S = ((D2 << 8) + D1) << 8 + D0; 8 outputs -> 2 words
+          // (pack_sat_u8(a, b, c) = c<<16 | sat(a)<<8 | sat(b): bytes [v0 v1 v2 v3])
+          auto pack8 = [&](const uint32_t (&e0)[8], const uint32_t (&e1)[8], const uint32_t (&e2)[8], uint32_t& wa,
+                           uint32_t& wb) {
+            int v[8];
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          if (PROF && (p.ablate & 4)) break;
-          uint32_t d0[16], d1[16], d2[16];
-          ldtm16(taddr + 16 * g, d0);
-          ldtm16(taddr + kStripPad + 16 * g, d1);
-          ldtm16(taddr + 2 * kStripPad + 16 * g, d2);
+            for (int u = 0; u < 8; ++u)
+              v[u] = combine_planes(static_cast<int>(e2[u]), static_cast<int>(e1[u]), static_cast<int>(e0[u])) >> 22;
+            wa = pack_sat_u8(v[1], v[0], pack_sat_u8(v[3], v[2], 0u));
+            wb = pack_sat_u8(v[5], v[4], pack_sat_u8(v[7], v[6], 0u));
+          };
+          auto store = [&](uint32_t off, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3) {
+            sts128(off, w0, w1, w2, w3);
+            if (slot < 2) sts128(off + p.NCH * 256, w0, w1, w2, w3);  // mirror slot
+          };
+          uint32_t w0, w1, w2, w3;
+          load(0, x0, x1, x2);
+          load(1, y0, y1, y2);
           ld_wait();
-          uint32_t w[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            int v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-              v[u] = combine_planes(static_cast<int>(d2[4 * e + u]), static_cast<int>(d1[4 * e + u]),
-                                    static_cast<int>(d0[4 * e + u])) >> 22;
-            // clip8 (R4) = sat_u8(S >> 22); bytes [v0 v1 v2 v3] (pack_sat_u8(a, b, c) = c<<16 | sat(a)<<8 | sat(b))
-            w[e] = pack_sat_u8(v[1], v[0], pack_sat_u8(v[3], v[2], 0u));
+          pack8(x0, x1, x2, w0, w1);
+          pack8(y0, y1, y2, w2, w3);
+          if (nh > 2) load(2, x0, x1, x2);
+          if (nh > 3) load(3, y0, y1, y2);
+          store(rrow, w0, w1, w2, w3);  // outputs 16*(h0/2) .. +15
+          if (nh > 2) {
+            ld_wait();
+            pack8(x0, x1, x2, w0, w1);
+            if (nh > 3) {
+              pack8(y0, y1, y2, w2, w3);
+              store(rrow + p.sbo_v, w0, w1, w2, w3);
+            } else {  // outputs 48..55 (56..63 carry no weights: never stored)
+              sts64(rrow + p.sbo_v, w0, w1);
+              if (slot < 2) sts64(rrow + p.sbo_v + p.NCH * 256, w0, w1);
+            }
           }
-          const uint32_t a = rrow + g * p.sbo_v;
-          sts128(a, w[0], w[1], w[2], w[3]);
-          if (slot < 2) sts128(a + p.NCH * 256, w[0], w[1], w[2], w[3]);  // mirror slot
         }
         fence_proxy_async();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[kHEmpty + b]);
+        if (lane == 0) {
+          mbar_arrive(&bars[kHEmpty + b]);            // the H MMA warp may reuse the accumulator
+          mbar_arrive(&bars[kHReady + (cs % kNHR)]);  // the V MMA warp may read the ring rows
+        }
         if (++slot == p.NCH) slot = 0;
       }
       i += hbB - hbA;

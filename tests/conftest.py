@@ -39,8 +39,8 @@ def cuda():
 
 @pytest.fixture(params=["tc", "mma"])
 def kernel(request, monkeypatch):
-    """Which fused kernel serves NV12 / fp32 requests: "tc" (the tcgen05
-    kernel, the default wherever its shared-memory plan fits) or "mma" (the
-    mma.sync kernel, FC_TC=0).  libfc reads FC_TC at every launch."""
+    """Which fused kernel serves NV12 / fp32 requests: "mma" (the mma.sync
+    kernel, the default) or "tc" (the tcgen05 kernel, FC_TC=1, wherever its
+    shared-memory plan fits).  libfc reads FC_TC at every launch."""
     monkeypatch.setenv("FC_TC", "1" if request.param == "tc" else "0")
     return request.param

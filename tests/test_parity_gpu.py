@@ -5,10 +5,9 @@ Bar (BASELINE.json north star):
     RGB intermediate: bit-exact;
   * normalised fp32 tokens: |gpu - oracle| <= 1e-5 * max(|oracle|, 1) per
     element (reading R7; bit-exact expected, and the count is reported).
-Two fused kernels serve these requests: the tcgen05 kernel (default for NV12
-/ fp32 wherever its shared-memory plan fits) and the mma.sync kernel (every
-other shape and variant; FC_TC=0 forces it) -- the `kernel` fixture runs a
-test through each.  Small cases are compared element by element on the whole
+Two fused kernels serve these requests: the mma.sync kernel (the default) and
+the tcgen05 kernel (FC_TC=1: NV12 / fp32 wherever its shared-memory plan
+fits) -- the `kernel` fixture runs a test through each.  Small cases are compared element by element on the whole
 output, through both the production instance (fc_preprocess) and the debug
 instance that also dumps the integer intermediates; the full BASELINE configs
 run in the bench's launch configuration (one launch per rank, all frames) and
@@ -622,10 +621,12 @@ def test_gather_world1_copies_shard(fc, oracle, cuda):
                                                       bytes=shard.numel() * shard.element_size())]
 
 
-def test_tc_kernel_serves_the_baseline_configs(fc, cuda):
-    """The tcgen05 kernel's plan fits every BASELINE config (c1-c5); the
-    paper's 224x224 setting (37-tap windows) falls to the mma.sync kernel."""
+def test_tc_kernel_serves_the_baseline_configs(fc, cuda, monkeypatch):
+    """With FC_TC=1 the tcgen05 kernel's plan fits every BASELINE config
+    (c1-c5); the paper's 224x224 setting (37-tap windows) falls to the mma.sync
+    kernel; without it the mma.sync kernel serves everything."""
     import torch
+    monkeypatch.setenv("FC_TC", "1")
     for name in ("c1", "c2", "c3", "c4", "c5"):
         wl = synth.CONFIGS[name]
         plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
@@ -638,5 +639,13 @@ def test_tc_kernel_serves_the_baseline_configs(fc, cuda):
                      resized_width=224)
     host = {i: synth.frame_nv12(1920, 1080, i, "natural", 1) for i in (0, 1)}
     fc.preprocess(plan, 0, fc.SurfaceTable.from_tensors(synth.to_device(host), 8))
+    torch.cuda.synchronize()
+    assert fc.last_kernel() == "mma"
+    monkeypatch.delenv("FC_TC")
+    wl = synth.CONFIGS["c1"]
+    plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
+                   fc.ModelCfg(sampling="explicit", explicit_indices=[0, 1]))
+    host = {i: synth.frame_nv12(wl.width, wl.height, i, "natural", 1) for i in (0, 1)}
+    fc.preprocess(plan, 0, fc.SurfaceTable.from_tensors(synth.to_device(host), wl.num_frames))
     torch.cuda.synchronize()
     assert fc.last_kernel() == "mma"

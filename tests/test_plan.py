@@ -487,3 +487,30 @@ def test_exchange_schedule_errors(fc):
     with pytest.raises(fc.FcError) as e:  # 1176 % 5 != 0
         fc.exchange_schedule(p, 0, "colsplit")
     assert e.value.name == "FC_ERR_UNSUPPORTED"
+
+
+# ------------------------------------------------ throughput mode placement
+def test_assign_requests_lpt(fc):
+    """fc_assign_requests: every request placed once; equal requests (config 5:
+    64 clips of 10 pairs) split evenly; LPT within Graham's 4/3 bound of the
+    brute-force optimum on small random instances."""
+    import itertools
+    assert sorted(collections_count(fc.assign_requests([10] * 64, 8)).values()) == [8] * 8
+    assert fc.assign_requests([], 4) == []
+    rng = random.Random(3)
+    for _ in range(200):
+        n, w = rng.randint(1, 7), rng.randint(1, 4)
+        pairs = [rng.randint(0, 20) for _ in range(n)]
+        got = fc.assign_requests(pairs, w)
+        assert len(got) == n and all(0 <= r < w for r in got)
+        loads = [sum(p for p, r in zip(pairs, got) if r == k) for k in range(w)]
+        opt = min(max(sum(p for p, r in zip(pairs, a) if r == k) for k in range(w))
+                  for a in itertools.product(range(w), repeat=n))
+        assert max(loads) <= opt * 4 / 3 + 1e-9 or max(loads) == opt, (pairs, w, got, opt)
+    with pytest.raises(fc.FcError):
+        fc.assign_requests([1, -1], 2)
+
+
+def collections_count(xs):
+    import collections
+    return collections.Counter(xs)

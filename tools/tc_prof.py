@@ -6,6 +6,7 @@ import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("FC_TC", "1")  # the tcgen05 kernel
 import torch  # noqa: E402
 
 import paper_2512_17574_b200 as fc  # noqa: E402
