@@ -40,7 +40,7 @@ extern "C" {
 
 #define FC_ABI_VERSION 4  /* 2: token_dtype + color in fc_model_cfg; tokens as void*
                              3: surface_format in fc_model_cfg, v plane in the surface
-                             4: fc_exchange_schedule, fc_last_kernel, fc_assign_requests */
+                             4: fc_exchange_schedule, fc_last_kernel, fc_assign_requests, fc_submit */
 #define FC_TOKEN_COLS 1176 /* 3 channels * 2 (temporal patch) * 14 * 14 */
 
 typedef enum {
@@ -236,6 +236,18 @@ typedef fc_nv12_surface fc_yuv_surface;
  * launch.  A rank with no rows returns FC_OK without launching. */
 fc_status fc_preprocess(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
                         int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream);
+
+/* fc_submit -- plan one request and enqueue its preprocessing in ONE call
+ * (FlashCodec's add_decoding_request: analyse + submit): exactly
+ * fc_plan(meta, cfg) followed by fc_preprocess(plan, rank, ...), for the
+ * small-request path where per-call host overhead dominates (config 1: a
+ * ~12 us kernel).  *plan_out receives the plan (caller-owned: fc_plan_destroy
+ * after the stream work completes); on any error nothing is enqueued and
+ * *plan_out is NULL.  tokens: (row_end-row_begin) x 1176 of cfg.token_dtype,
+ * sized by the caller from the request's shape (fc_plan_rank of an equal
+ * request, or the closed form of fc_plan_info). */
+fc_status fc_submit(const fc_video_meta* meta, const fc_model_cfg* cfg, int32_t rank, const fc_nv12_surface* surfaces,
+                    int64_t num_surfaces, void* tokens, void* stream, fc_plan_t** plan_out);
 
 /* Same, additionally dumping the integer intermediates for parity tests:
  *   rgb_src:     device u8 [n_r, H, W, 3]  (BT.601 output) or NULL

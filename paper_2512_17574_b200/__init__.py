@@ -22,7 +22,7 @@ from ._native import FcError, FC_TOKEN_COLS, check, lib
 
 __all__ = ["VideoMeta", "ModelCfg", "Plan", "SurfaceTable", "preprocess", "preprocess_debug", "preprocess_batch",
            "expand_tokens", "preprocess_paged",
-           "NcclComm", "gather", "exchange_schedule", "last_kernel", "assign_requests", "FcError", "FC_TOKEN_COLS", "lib"]
+           "NcclComm", "gather", "exchange_schedule", "last_kernel", "assign_requests", "submit", "FcError", "FC_TOKEN_COLS", "lib"]
 
 
 @dataclass
@@ -36,6 +36,16 @@ class VideoMeta:
     gop_start: Sequence[int] = (0,)
 
     def to_c(self):
+        # requests of one shape reuse the marshalled struct (keyed by every field)
+        key = (self.width, self.height, self.num_frames, self.fps, tuple(self.gop_start))
+        cached = self.__dict__.get("_c")
+        if cached is not None and cached[0] == key:
+            return cached[1], cached[2]
+        m, arr = self._to_c()
+        self.__dict__["_c"] = (key, m, arr)
+        return m, arr
+
+    def _to_c(self):
         fr = Fraction(self.fps[0], self.fps[1]) if isinstance(self.fps, tuple) else Fraction(self.fps)
         gs = list(self.gop_start)
         arr = (ctypes.c_int64 * len(gs))(*gs)
@@ -68,6 +78,15 @@ class ModelCfg:
     surface_format: str = "nv12"    # "nv12" (interleaved chroma) | "i420" (planar U, V)
 
     def to_c(self):
+        key = tuple(tuple(v) if isinstance(v, (list, tuple)) else v for k, v in self.__dict__.items() if k != "_c")
+        cached = self.__dict__.get("_c")
+        if cached is not None and cached[0] == key:
+            return cached[1], cached[2]
+        c, keep = self._to_c()
+        self.__dict__["_c"] = (key, c, keep)
+        return c, keep
+
+    def _to_c(self):
         c = _native.ModelCfgC()
         lib().fc_model_cfg_default(ctypes.byref(c))
         c.world_size = self.world_size
@@ -102,13 +121,16 @@ class ModelCfg:
 class Plan:
     """fc_plan: sampling + smart_resize + GOP->rank partition + tables (host)."""
 
-    def __init__(self, meta: VideoMeta, cfg: ModelCfg | None = None):
+    def __init__(self, meta: VideoMeta, cfg: ModelCfg | None = None, _handle=None):
         self.meta = meta
         self.cfg = cfg or ModelCfg()
-        m, _keep_m = meta.to_c()
-        c, _keep_c = self.cfg.to_c()
-        h = ctypes.c_void_p()
-        check(lib().fc_plan(ctypes.byref(m), ctypes.byref(c), ctypes.byref(h)), "fc_plan")
+        if _handle is None:
+            m, _keep_m = meta.to_c()
+            c, _keep_c = self.cfg.to_c()
+            h = ctypes.c_void_p()
+            check(lib().fc_plan(ctypes.byref(m), ctypes.byref(c), ctypes.byref(h)), "fc_plan")
+        else:  # a plan created by fc_submit
+            h = _handle
         self._h = h
         info = _native.PlanInfoC()
         check(lib().fc_plan_info_get(h, ctypes.byref(info)), "fc_plan_info_get")
@@ -122,9 +144,25 @@ class Plan:
         self.ranks_used = info.ranks_used
         self.world_size = info.world_size
         self.max_taps = (info.max_taps_h, info.max_taps_v)
-        idx = (ctypes.c_int64 * max(self.num_sampled, 1))()
-        check(lib().fc_plan_sampled_indices(h, idx), "fc_plan_sampled_indices")
-        self.sampled_indices = list(idx)[: self.num_sampled]
+        self._sampled = None
+        self._rows: dict[int, int] = {}
+
+    @property
+    def sampled_indices(self) -> list[int]:
+        """fc_plan_sampled_indices (fetched on first use)."""
+        if self._sampled is None:
+            idx = (ctypes.c_int64 * max(self.num_sampled, 1))()
+            check(lib().fc_plan_sampled_indices(self._h, idx), "fc_plan_sampled_indices")
+            self._sampled = list(idx)[: self.num_sampled]
+        return self._sampled
+
+    def rank_rows(self, r: int) -> int:
+        """Token rows of rank r (row_end - row_begin; the plan is immutable, so cached)."""
+        n = self._rows.get(r)
+        if n is None:
+            rp = self.rank(r)
+            n = self._rows[r] = rp["row_end"] - rp["row_begin"]
+        return n
 
     @property
     def handle(self) -> ctypes.c_void_p:
@@ -182,8 +220,9 @@ class SurfaceTable:
 
 def _stream_ptr(stream) -> ctypes.c_void_p:
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return ctypes.c_void_p(s.cuda_stream)
+    if stream is None:  # the current stream's handle, without building a Stream object
+        return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(torch.cuda.current_device()))
+    return ctypes.c_void_p(stream.cuda_stream)
 
 
 def _tok_dtype(plan: Plan):
@@ -192,8 +231,7 @@ def _tok_dtype(plan: Plan):
 
 
 def _rank_rows(plan: Plan, rank: int) -> int:
-    rp = plan.rank(rank)
-    return rp["row_end"] - rp["row_begin"]
+    return plan.rank_rows(rank)
 
 
 def preprocess(plan: Plan, rank: int, surfaces: SurfaceTable, out=None, stream=None):
@@ -201,13 +239,23 @@ def preprocess(plan: Plan, rank: int, surfaces: SurfaceTable, out=None, stream=N
     the (row_end-row_begin) x 1176 fp32 token shard (allocated after planning
     if `out` is None, P:453)."""
     import torch
-    rows = _rank_rows(plan, rank)
     if out is None:
-        out = torch.empty((rows, FC_TOKEN_COLS), dtype=_tok_dtype(plan), device="cuda")
-    grid = (ctypes.c_int64 * 3)()
-    check(lib().fc_preprocess(plan.handle, rank, surfaces.arr, surfaces.n, ctypes.c_void_p(out.data_ptr()), grid,
+        out = torch.empty((_rank_rows(plan, rank), FC_TOKEN_COLS), dtype=_tok_dtype(plan), device="cuda")
+    check(lib().fc_preprocess(plan.handle, rank, surfaces.arr, surfaces.n, ctypes.c_void_p(out.data_ptr()), None,
                               _stream_ptr(stream)), "fc_preprocess")
     return out
+
+
+def submit(meta: VideoMeta, cfg: ModelCfg, rank: int, surfaces: SurfaceTable, out, stream=None) -> Plan:
+    """fc_submit: plan the request and enqueue its fused kernel in ONE C call
+    (small requests, where per-call overhead dominates); `out` is the
+    caller-allocated token shard of `rank`.  Returns the request's Plan."""
+    m, _km = meta.to_c()
+    c, _kc = cfg.to_c()
+    h = ctypes.c_void_p()
+    check(lib().fc_submit(ctypes.byref(m), ctypes.byref(c), rank, surfaces.arr, surfaces.n,
+                          ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream), ctypes.byref(h)), "fc_submit")
+    return Plan(meta, cfg, _handle=h)
 
 
 def preprocess_debug(plan: Plan, rank: int, surfaces: SurfaceTable, stream=None):

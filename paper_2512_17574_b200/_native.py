@@ -94,7 +94,7 @@ EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_g
            "fc_nccl_comm_init", "fc_nccl_comm_destroy", "fc_gather", "fc_status_string", "fc_last_error",
            "fc_abi_version", "fc_kernel_launches", "fc_expand_tokens", "fc_preprocess_paged",
            "fc_preprocess_colsplit", "fc_scatter_columns", "fc_exchange_schedule", "fc_last_kernel",
-           "fc_assign_requests"]
+           "fc_assign_requests", "fc_submit"]
 
 _lib = None
 
@@ -141,6 +141,8 @@ def lib() -> ctypes.CDLL:
     L.fc_kernel_launches.restype = ctypes.c_uint64
     L.fc_exchange_schedule.argtypes = [vp, i32, ctypes.c_int, ctypes.POINTER(TransferC), i32, ctypes.POINTER(i32)]
     L.fc_assign_requests.argtypes = [ctypes.POINTER(ctypes.c_int64), i32, i32, ctypes.POINTER(ctypes.c_int32)]
+    L.fc_submit.argtypes = [ctypes.POINTER(VideoMetaC), ctypes.POINTER(ModelCfgC), i32, ctypes.POINTER(Nv12SurfaceC),
+                            i64, vp, vp, ctypes.POINTER(vp)]
     L.fc_last_kernel.argtypes = []
     L.fc_last_kernel.restype = ctypes.c_int32
     for name in EXPORTS:

@@ -47,6 +47,7 @@ struct DeviceTables {
   DeviceTables(const DeviceTables&) = delete;
   DeviceTables& operator=(const DeviceTables&) = delete;
   ~DeviceTables();  // fc_kernels.cu
+  uint64_t serial = 0;         // unique per table set (keys the launch-configuration cache)
   int ksh = 1, ksv = 1;        // MMA k-steps of the H / V windows
   int32_t* hx = nullptr;       // H xmin per output column
   int32_t* hxs = nullptr;      // H window start per 8-column tile

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
@@ -219,6 +220,8 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, const DeviceTables
     return fail(FC_ERR_UNSUPPORTED, "resize window wider than 128 source pixels per 8 outputs");
   auto sp = std::make_shared<DeviceTables>();  // frees whatever was uploaded if this fails
   DeviceTables& t = *sp;
+  static std::atomic<uint64_t> serials{0};
+  t.serial = ++serials;
   t.ksh = m.ksh;
   t.ksv = m.ksv;
   cudaError_t e = cudaSuccess;
@@ -483,6 +486,62 @@ cudaMemPool_t descriptor_pool(int dev) {
   return pool;
 }
 
+// Launch configurations (geometry, TMA stages, occupancy) per (table set,
+// kernel instance, surface format): requests of a known shape skip the
+// geometry search and the occupancy queries (host cost of a small request).
+struct LaunchKey {
+  uint64_t serial;
+  const void* fn;
+  int i420;
+  bool operator==(const LaunchKey& o) const { return serial == o.serial && fn == o.fn && i420 == o.i420; }
+};
+struct LaunchKeyHash {
+  size_t operator()(const LaunchKey& k) const {
+    return std::hash<uint64_t>()(k.serial) ^ (std::hash<const void*>()(k.fn) << 1) ^ static_cast<size_t>(k.i420);
+  }
+};
+struct LaunchCfg {
+  Geometry g;
+  int occ;
+};
+static std::mutex g_launch_mu;
+static std::unordered_map<LaunchKey, LaunchCfg, LaunchKeyHash>* g_launch =
+    new std::unordered_map<LaunchKey, LaunchCfg, LaunchKeyHash>();
+
+}  // namespace fc
+namespace fc {
+// Device attributes the launch path needs, queried once per device.
+void device_attrs(int dev, int* major, int* max_smem, int* nsm) {
+  static std::mutex mu;
+  static std::map<int, std::array<int, 3>>* cache = new std::map<int, std::array<int, 3>>();
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache->find(dev);
+  if (it == cache->end()) {
+    std::array<int, 3> a{0, 0, 0};
+    cudaDeviceGetAttribute(&a[0], cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&a[1], cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&a[2], cudaDevAttrMultiProcessorCount, dev);
+    it = cache->emplace(dev, a).first;
+  }
+  *major = it->second[0];
+  *max_smem = it->second[1];
+  *nsm = it->second[2];
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize only ever grows per (device,
+// kernel), so a launch never sees a smaller limit set for another shape.
+fc_status ensure_smem_attr(int dev, const void* fn, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t>* cur = new std::map<std::pair<int, const void*>, size_t>();
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = (*cur)[{dev, fn}];
+  if (have >= smem) return FC_OK;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+  have = smem;
+  return FC_OK;
+}
+
 // dry: validate and prepare everything (tables, geometry, tensor maps) but
 // enqueue nothing -- fc_preprocess_batch checks every group before the first launch
 static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, uint8_t* dbg_src,
@@ -503,9 +562,7 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
   int major = 0, max_smem = 0, nsm = 0;
-  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  device_attrs(dev, &major, &max_smem, &nsm);
   if (major != 10) return fail(FC_ERR_CUDA, "fc kernels are built for sm_100a only (no CPU/other-arch fallback)");
   const int W = P->meta.width, H = P->meta.height;
   // strips of 2 merge blocks; 1 merge block when a very wide resize window
@@ -513,10 +570,28 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
   const DeviceTables* dt = nullptr;
   Geometry g;
   fc_status st = FC_OK;
+  const int i420k = P->cfg.surface_format == FC_SURFACE_I420 ? 1 : 0;
   for (int sw : {kStrip, 28}) {
     st = device_tables(P, dev, sw, &dt);
     if (st != FC_OK) return st;
+    // geometry per (table set, surface format), searched once (a failed
+    // search is remembered too: the caller then tries narrower strips)
+    const LaunchKey gkey{dt->serial, nullptr, i420k};
+    {
+      std::lock_guard<std::mutex> lk(g_launch_mu);
+      auto it = g_launch->find(gkey);
+      if (it != g_launch->end()) {
+        g = it->second.g;
+        st = it->second.occ ? FC_OK : FC_ERR_UNSUPPORTED;
+        if (st == FC_OK) break;
+        continue;
+      }
+    }
     st = choose_geometry(P, dt, sw, max_smem, &g);
+    {
+      std::lock_guard<std::mutex> lk(g_launch_mu);
+      (*g_launch)[gkey] = LaunchCfg{g, st == FC_OK ? 1 : 0};
+    }
     if (st == FC_OK) break;
   }
   if (st != FC_OK) return st;
@@ -537,22 +612,37 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
                 : td == FC_TOKENS_BF16 ? g.fn_bf16
                 : td == FC_TOKENS_U8   ? g.fn_u8
                                        : g.fn;
-  e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(g.smem));
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
   int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, g.smem);
-  if (e != cudaSuccess || occ < 1) return cuda_fail(e, "occupancy query");
-  if (g.nstages == kMaxStages) {
-    // a shallower TMA pipeline (2 stages) when it buys another CTA per SM:
-    // latency hiding across CTAs is worth more than 2 extra chunks in flight
-    const size_t smem2 = smem_bytes(2, g.SWP, g.BW * g.NX, g.TRW);
-    int occ2 = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, fn, kThreads, smem2) == cudaSuccess && occ2 > occ) {
-      g.nstages = 2;
-      g.smem = smem2;
-      occ = occ2;
+  const LaunchKey lkey{dt->serial, reinterpret_cast<const void*>(fn), i420 ? 1 : 0};
+  bool cached = false;
+  {
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    auto it = g_launch->find(lkey);
+    if (it != g_launch->end()) {
+      g = it->second.g;
+      occ = it->second.occ;
+      cached = true;
     }
+  }
+  if (!cached) {
+    st = ensure_smem_attr(dev, reinterpret_cast<const void*>(fn), g.smem);
+    if (st != FC_OK) return st;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kThreads, g.smem);
+    if (e != cudaSuccess || occ < 1) return cuda_fail(e, "occupancy query");
+    if (g.nstages == kMaxStages) {
+      // a shallower TMA pipeline (2 stages) when it buys another CTA per SM:
+      // latency hiding across CTAs is worth more than 2 extra chunks in flight
+      const size_t smem2 = smem_bytes(2, g.SWP, g.BW * g.NX, g.TRW);
+      int occ2 = 0;
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, fn, kThreads, smem2) == cudaSuccess && occ2 > occ) {
+        g.nstages = 2;
+        g.smem = smem2;
+        occ = occ2;
+      }
+    }
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    if (g_launch->size() > 4096) g_launch->clear();
+    (*g_launch)[lkey] = LaunchCfg{g, occ};
   }
 
   static thread_local Params prm;  // ~31 KB: keep it off the stack
@@ -766,6 +856,22 @@ extern "C" {
 fc_status fc_preprocess(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
                         int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream) {
   return preprocess_impl(plan, rank, surfaces, num_surfaces, tokens, grid_thw, stream, nullptr, nullptr);
+}
+
+fc_status fc_submit(const fc_video_meta* meta, const fc_model_cfg* cfg, int32_t rank, const fc_nv12_surface* surfaces,
+                    int64_t num_surfaces, void* tokens, void* stream, fc_plan_t** plan_out) {
+  if (!plan_out) return fail(FC_ERR_INVALID_ARG, "plan_out is NULL");
+  *plan_out = nullptr;
+  fc_plan_t* P = nullptr;
+  fc_status st = fc_plan(meta, cfg, &P);
+  if (st != FC_OK) return st;
+  st = preprocess_impl(P, rank, surfaces, num_surfaces, tokens, nullptr, stream, nullptr, nullptr);
+  if (st != FC_OK) {
+    fc_plan_destroy(P);
+    return st;
+  }
+  *plan_out = P;
+  return FC_OK;
 }
 
 fc_status fc_preprocess_colsplit(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,

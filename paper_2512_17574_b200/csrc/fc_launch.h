@@ -62,6 +62,10 @@ std::atomic<uint64_t>& launch_counter();
 int32_t& last_kernel();
 // 2-D u8 tensor map [rows][pitch] with a (bw x bh) box, cached per surface.
 fc_status tensor_map(const uint8_t* base, int64_t pitch, int64_t rows, int bw, int bh, CUtensorMap* out);
+// Compute capability major, opt-in shared memory per block, SM count (cached per device).
+void device_attrs(int dev, int* major, int* max_smem, int* nsm);
+// Raise a kernel's dynamic shared-memory limit to at least smem (monotone per device).
+fc_status ensure_smem_attr(int dev, const void* fn, size_t smem);
 // Library-owned stream-ordered pool for launch descriptors.
 cudaMemPool_t descriptor_pool(int dev);
 // Colour-matrix constants (R3, R15) as dp2a operand pairs and biases.

@@ -257,9 +257,7 @@ fc_status launch_tc(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, ui
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return FC_OK;
   int major = 0, max_smem = 0, nsm = 0;
-  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
-  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  device_attrs(dev, &major, &max_smem, &nsm);
   if (major != 10) return FC_OK;  // the caller reports the missing sm_100 device
   const TcTables* t = nullptr;
   fc_status st = tables(P, dev, &t);
@@ -382,10 +380,10 @@ fc_status launch_tc(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, ui
   // FC_TC_PROF=1 (experiments): the instance that counts each warp's barrier-wait cycles
   const bool profile = std::getenv("FC_TC_PROF") != nullptr && !(dbg_src || dbg_rs);
   TcKernelFn fn = (dbg_src || dbg_rs) ? fdbg : profile ? fprof : fprod;
-  e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) {
+  st = ensure_smem_attr(dev, reinterpret_cast<const void*>(fn), static_cast<size_t>(smem));
+  if (st != FC_OK) {
     if (desc) cudaFreeAsync(desc, s);
-    return cuda_fail(e, "cudaFuncSetAttribute (tcgen05 kernel)");
+    return st;
   }
   // one CTA per SM (512 TMEM columns each); every strip needs at least one CTA
   const long long work = static_cast<long long>(prm.npairs) * prm.gh2 * t->nstrips;

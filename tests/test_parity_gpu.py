@@ -649,3 +649,30 @@ def test_tc_kernel_serves_the_baseline_configs(fc, cuda, monkeypatch):
     fc.preprocess(plan, 0, fc.SurfaceTable.from_tensors(synth.to_device(host), wl.num_frames))
     torch.cuda.synchronize()
     assert fc.last_kernel() == "mma"
+
+
+def test_submit_equals_plan_then_preprocess(fc, oracle, cuda):
+    """fc_submit (plan + launch in one call) gives the oracle's tokens, and its
+    plan equals fc_plan's; a bad surface table leaves nothing enqueued."""
+    import torch
+    wl = synth.CONFIGS["c1"]
+    meta = fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start)
+    cfg = fc.ModelCfg(sample_fps=wl.sample_fps)
+    ref_plan = fc.Plan(meta, cfg)
+    idx = ref_plan.sampled_indices
+    host = synth.frames_nv12(wl, idx, "uniform")
+    surf = fc.SurfaceTable.from_tensors(synth.to_device(host), wl.num_frames)
+    out = torch.full((ref_plan.token_rows, 1176), -1.0, device="cuda")
+    plan = fc.submit(meta, cfg, 0, surf, out)
+    torch.cuda.synchronize()
+    assert plan.sampled_indices == idx and plan.grid_thw == ref_plan.grid_thw
+    h2, w2 = plan.resized
+    ref = oracle.preprocess([host[i] for i in idx], wl.width, wl.height, w2, h2)
+    assert tol_check(out.cpu().numpy(), ref, "fc_submit") == ref.size
+    bad = fc.SurfaceTable(wl.num_frames)  # every surface NULL
+    out.fill_(-1.0)
+    with pytest.raises(fc.FcError) as e:
+        fc.submit(meta, cfg, 0, bad, out)
+    assert e.value.name == "FC_ERR_MISSING_SURFACE"
+    torch.cuda.synchronize()
+    assert bool((out == -1.0).all())
