@@ -209,8 +209,15 @@ def run_ours(args):
     colx = world > 1 and args.exchange == "colsplit"
     if colx and (clips != 1 or args.tokens != "f32"):
         raise SystemExit("--exchange colsplit: single-request configs, f32 tokens")
+    # N>1 with the fused peer-store exchange (NEXT-1, --exchange p2p): every rank's
+    # kernel writes its u8 codes straight into the encoder's buffer through a CUDA
+    # IPC mapping (over NVLink), the exchange is one stream-ordered completion
+    # collective, and the encoder expands the codes
+    p2px = world > 1 and args.exchange == "p2p" and clips == 1
+    if p2px:
+        u8x = True
     if replicas:
-        u8x = colx = False
+        u8x = colx = p2px = False
     cfg = fc.ModelCfg(world_size=1 if replicas else world, sample_fps=wl.sample_fps,
                       token_dtype="u8" if u8x else args.tokens, color=args.color, surface_format=args.surface)
     tok_bytes = 2 if args.tokens == "bf16" else 4
@@ -252,10 +259,25 @@ def run_ours(args):
              if (world > 1 and rank == enc and not colx and not replicas) else None for _ in range(clips)]
     toks = [torch.empty((plan0.token_rows, 1176), dtype=tdt, device="cuda")
             if (u8x and rank == enc) else None for _ in range(clips)]
+    peer = None
+    if p2px:  # every rank's output = its rows of the encoder's code buffer (IPC-mapped off the encoder)
+        hdl = [fc.ipc_export(fulls[0]) if rank == enc else None]
+        dist.broadcast_object_list(hdl, src=enc)
+        if rank == enc:
+            outs[0] = fulls[0][rp["row_begin"]:rp["row_end"]]
+        elif rows:
+            peer = fc.PeerBuffer(hdl[0][0])
+            outs[0] = peer.tensor((rows, 1176), torch.uint8, hdl[0][1] + rp["row_begin"] * 1176)
+        done = torch.zeros(1, device="cuda")
     stream = torch.cuda.current_stream()
 
     def exchange(plans):
         """a10 (+ the encoder-side expand of the u8 exchange)."""
+        if p2px:  # the codes are already in place: order the encoder after every rank's kernel
+            dist.all_reduce(done)
+            if rank == enc:
+                fc.expand_tokens(plans[0], fulls[0], toks[0], args.tokens)
+            return
         for pl, o, fl, tk, mn in zip(plans, outs, fulls, toks, mines):
             if colx:
                 fc.scatter_columns(pl, rank, comm, o if rows else None, mn)
@@ -368,7 +390,10 @@ def run_ours(args):
         if colx:  # bytes into the busiest rank: every other rank's rows x its C columns
             gbytes = max((plan0.token_rows - (r["row_end"] - r["row_begin"])) * (1176 // world) * 4
                          for r in plan0.ranks())
-        gather = {"exchange": "column split all-to-all (P:527-530)" if colx else
+        if p2px:  # the bytes crossed NVLink inside the ranks' kernels; this times completion + expand
+            gbytes = sum((r["row_end"] - r["row_begin"]) * 1176 for i, r in enumerate(plan0.ranks()) if i != enc)
+        gather = {"exchange": "fused peer stores of u8 codes (IPC) + completion all-reduce + encoder expand" if p2px
+                  else "column split all-to-all (P:527-530)" if colx else
                   "u8 codes + encoder expand" if u8x else args.tokens,
                   "ms": round(gms.item(), 4), "bytes_into_encoder": gbytes,
                   "GB/s": round(gbytes / (gms.item() * 1e-3) / 1e9, 1), "nvlink_nominal_GB/s": 900,
@@ -557,6 +582,8 @@ def run_ours(args):
                                     "single_core": {"value": round(f1 / dt1, 3), "unit": "frames/s", "cores": 1,
                                                     "sample": f"{f1} sampled frames (1 temporal pair), {dt1:.2f} s"}}
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        peer.close()
     if comm is not None:
         comm.close()
     if world > 1:
@@ -574,9 +601,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tokens", default="f32", choices=["f32", "bf16"],
                     help="token dtype (NEXT-4 variant; the BASELINE metric is f32)")
-    ap.add_argument("--exchange", default="u8", choices=["u8", "f32", "colsplit"],
-                    help="N>1 exchange: u8 codes + encoder-side expand (default), the tokens themselves, or the "
-                         "paper's column split (every rank keeps 1176/N columns of all rows)")
+    ap.add_argument("--exchange", default="u8", choices=["u8", "f32", "colsplit", "p2p"],
+                    help="N>1 exchange: u8 codes + encoder-side expand (default), the tokens themselves, the "
+                         "paper's column split (every rank keeps 1176/N columns of all rows), or fused peer stores "
+                         "(each rank's kernel writes its codes into the encoder's buffer over NVLink)")
     ap.add_argument("--color", default="bt601", choices=["bt601", "bt709", "bt601_full", "bt709_full"],
                     help="YUV->RGB matrix (NEXT-4 variant; the BASELINE metric is bt601)")
     ap.add_argument("--surface", default="nv12", choices=["nv12", "i420"],

@@ -40,7 +40,7 @@ extern "C" {
 
 #define FC_ABI_VERSION 4  /* 2: token_dtype + color in fc_model_cfg; tokens as void*
                              3: surface_format in fc_model_cfg, v plane in the surface
-                             4: fc_exchange_schedule, fc_last_kernel, fc_assign_requests, fc_submit */
+                             4: fc_exchange_schedule, fc_last_kernel, fc_assign_requests, fc_submit, fc_ipc_* */
 #define FC_TOKEN_COLS 1176 /* 3 channels * 2 (temporal patch) * 14 * 14 */
 
 typedef enum {
@@ -362,6 +362,28 @@ typedef struct {
 } fc_transfer;
 fc_status fc_exchange_schedule(const fc_plan_t* plan, int32_t rank, fc_exchange_kind kind, fc_transfer* out,
                                int32_t capacity, int32_t* count);
+
+/* CUDA IPC handles for the fused peer-store exchange (NEXT-1, P:527-530:
+ * shards written straight into the encoder's IPC patch buffer).  The
+ * encoder exports its token buffer once; every other rank imports it and
+ * passes  peer_base + row_begin * row_bytes  as the `tokens` of fc_preprocess,
+ * so its kernel's epilogue stores land in the encoder's HBM over NVLink while
+ * the rank computes -- no separate gather pass.  The caller orders the
+ * encoder's reads after every rank's kernel (e.g. a stream-ordered
+ * collective or an interprocess event).
+ *   fc_ipc_export: dev_ptr = the base of a cudaMalloc'd allocation (torch
+ *                  tensors from the caching allocator: data_ptr() may be
+ *                  inside a larger block -- export with its offset, see
+ *                  fc_ipc_export_range); handle = 64 opaque bytes.
+ *   fc_ipc_import: *dev_ptr = the allocation's base in this process (another
+ *                  process; cudaIpcMemLazyEnablePeerAccess).
+ *   fc_ipc_close:  releases an imported mapping.
+ * Errors: FC_ERR_INVALID_ARG (NULL), FC_ERR_CUDA (the runtime's reason). */
+fc_status fc_ipc_export(void* dev_ptr, uint8_t handle[64]);
+/* the allocation containing ptr: its handle and ptr's byte offset in it */
+fc_status fc_ipc_export_range(void* ptr, uint8_t handle[64], int64_t* offset);
+fc_status fc_ipc_import(const uint8_t handle[64], void** dev_ptr);
+fc_status fc_ipc_close(void* dev_ptr);
 
 /* fc_gather -- gatherv of every rank's contiguous row shard into the encoder
  * rank's full token buffer (grouped ncclSend/ncclRecv, R9):

@@ -22,7 +22,7 @@ from ._native import FcError, FC_TOKEN_COLS, check, lib
 
 __all__ = ["VideoMeta", "ModelCfg", "Plan", "SurfaceTable", "preprocess", "preprocess_debug", "preprocess_batch",
            "expand_tokens", "preprocess_paged",
-           "NcclComm", "gather", "exchange_schedule", "last_kernel", "assign_requests", "submit", "FcError", "FC_TOKEN_COLS", "lib"]
+           "NcclComm", "gather", "exchange_schedule", "last_kernel", "assign_requests", "submit", "ipc_export", "PeerBuffer", "FcError", "FC_TOKEN_COLS", "lib"]
 
 
 @dataclass
@@ -399,6 +399,45 @@ def assign_requests(pairs: Sequence[int], world: int) -> list[int]:
     out = (ctypes.c_int32 * max(n, 1))()
     check(lib().fc_assign_requests(arr, n, world, out), "fc_assign_requests")
     return list(out)[:n]
+
+
+def ipc_export(tensor) -> tuple[bytes, int]:
+    """fc_ipc_export_range: (64-byte IPC handle of the allocation holding
+    `tensor`, byte offset of tensor.data_ptr() in it) -- for another process
+    to map (ipc_import) and write into (the fused peer-store exchange)."""
+    h = (ctypes.c_uint8 * 64)()
+    off = ctypes.c_int64()
+    check(lib().fc_ipc_export_range(ctypes.c_void_p(tensor.data_ptr()), h, ctypes.byref(off)), "fc_ipc_export_range")
+    return bytes(h), off.value
+
+
+class PeerBuffer:
+    """A peer process's device buffer mapped into this process
+    (fc_ipc_import); `tensor(shape, dtype, offset)` views it as a torch
+    tensor (no copy; writes land in the peer's memory).  close() unmaps."""
+
+    def __init__(self, handle: bytes):
+        p = ctypes.c_void_p()
+        check(lib().fc_ipc_import((ctypes.c_uint8 * 64)(*handle), ctypes.byref(p)), "fc_ipc_import")
+        self.ptr = p.value
+
+    def tensor(self, shape, dtype, offset: int = 0):
+        import torch
+
+        class _View:  # __cuda_array_interface__ (v3) for torch.as_tensor
+            def __init__(self, ptr, shape, typestr):
+                self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (ptr, False),
+                                                 "version": 3, "strides": None}
+        typestr = {torch.float32: "<f4", torch.bfloat16: "<V2", torch.uint8: "|u1"}[dtype]
+        if dtype == torch.bfloat16:  # no bf16 typestr: view the bytes as int16 and reinterpret
+            t = torch.as_tensor(_View(self.ptr + offset, shape, "<i2"), device="cuda")
+            return t.view(torch.bfloat16)
+        return torch.as_tensor(_View(self.ptr + offset, shape, typestr), device="cuda")
+
+    def close(self):
+        if self.ptr:
+            check(lib().fc_ipc_close(ctypes.c_void_p(self.ptr)), "fc_ipc_close")
+            self.ptr = None
 
 
 def last_kernel() -> str | None:

@@ -94,7 +94,8 @@ EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_g
            "fc_nccl_comm_init", "fc_nccl_comm_destroy", "fc_gather", "fc_status_string", "fc_last_error",
            "fc_abi_version", "fc_kernel_launches", "fc_expand_tokens", "fc_preprocess_paged",
            "fc_preprocess_colsplit", "fc_scatter_columns", "fc_exchange_schedule", "fc_last_kernel",
-           "fc_assign_requests", "fc_submit"]
+           "fc_assign_requests", "fc_submit", "fc_ipc_export", "fc_ipc_export_range", "fc_ipc_import",
+           "fc_ipc_close"]
 
 _lib = None
 
@@ -143,6 +144,10 @@ def lib() -> ctypes.CDLL:
     L.fc_assign_requests.argtypes = [ctypes.POINTER(ctypes.c_int64), i32, i32, ctypes.POINTER(ctypes.c_int32)]
     L.fc_submit.argtypes = [ctypes.POINTER(VideoMetaC), ctypes.POINTER(ModelCfgC), i32, ctypes.POINTER(Nv12SurfaceC),
                             i64, vp, vp, ctypes.POINTER(vp)]
+    L.fc_ipc_export.argtypes = [vp, ctypes.POINTER(ctypes.c_uint8)]
+    L.fc_ipc_export_range.argtypes = [vp, ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(ctypes.c_int64)]
+    L.fc_ipc_import.argtypes = [ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(vp)]
+    L.fc_ipc_close.argtypes = [vp]
     L.fc_last_kernel.argtypes = []
     L.fc_last_kernel.restype = ctypes.c_int32
     for name in EXPORTS:

@@ -52,22 +52,8 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, 
       "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void prefetch_tmap(const void* tmap) {
-  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
-}
 
 // ---------------------------------------------------------------- integer math
-__device__ __forceinline__ uint32_t dp4a_uu(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("dp4a.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-// a: four unsigned pixel bytes; b: four signed weight bytes
-__device__ __forceinline__ uint32_t dp4a_us(uint32_t a, uint32_t b, uint32_t c) {
-  uint32_t d;
-  asm("dp4a.u32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
 // a: two signed 16-bit coefficients; b: pixel bytes 0,1 (lo) or 2,3 (hi)
 __device__ __forceinline__ int dp2a_lo(uint32_t a, uint32_t b, int c) {
   int d;
@@ -96,26 +82,6 @@ __device__ __forceinline__ int add_min_relu(int a, int b, int c) {
   int d;
   asm("min.relu.s32 %0, %1, %2;" : "=r"(d) : "r"(a + b), "r"(c));
   return d;
-}
-
-// Exact 22-bit fixed-point FIR over NW words of 4 taps (R4):
-//   S = 2^21 + sum px*iw = ((s2*256 + s1)*256 + s0), with the byte planes
-// accumulated as one DP4A chain (plane 2 first, seeded with 32 = 2^21/2^16,
-// shifted left 8 between planes).  int32 arithmetic is modular, so the
-// result equals the exact sum whenever the exact sum fits (R4 headroom).
-template <int NW>
-__device__ __forceinline__ int fir_sum(const uint32_t (&d)[NW], const uint32_t (&w0)[NW], const uint32_t (&w1)[NW],
-                                       const uint32_t (&w2)[NW]) {
-  uint32_t s = 32u;
-#pragma unroll
-  for (int i = 0; i < NW; ++i) s = dp4a_us(d[i], w2[i], s);
-  s <<= 8;
-#pragma unroll
-  for (int i = 0; i < NW; ++i) s = dp4a_uu(d[i], w1[i], s);
-  s <<= 8;
-#pragma unroll
-  for (int i = 0; i < NW; ++i) s = dp4a_uu(d[i], w0[i], s);
-  return static_cast<int>(s);
 }
 
 // Integer YUV -> RGB (R3 BT.601 limited by default; R15 variants) on 4 pixels.  yw = Y0..Y3 bytes, uvw =
@@ -221,9 +187,6 @@ __device__ __forceinline__ void bar_sync(int id, int n) { asm volatile("bar.sync
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void sts8(uint32_t addr, uint32_t v) {
-  asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
 
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(static_cast<unsigned short>(v)) : "memory");
@@ -237,11 +200,6 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ float ldsf(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
 
@@ -274,9 +232,6 @@ __device__ __forceinline__ void st_cs_pred2(uint16_t* p, uint32_t a, uint32_t b,
 }
 __device__ __forceinline__ void st_cs_pred2(uint8_t* p, uint32_t a, uint32_t b, bool pred) {
   st_cs_pred(reinterpret_cast<uint16_t*>(p), __byte_perm(a, b, 0x0040), pred);  // u8 codes in the low bytes
-}
-__device__ __forceinline__ void st_cs_f2(float* p, float a, float b) {
-  asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
 
 }  // namespace fc

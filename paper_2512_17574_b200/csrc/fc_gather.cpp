@@ -5,6 +5,7 @@
 // contiguous row range and the exchange is a gatherv: NCCL has no gatherv,
 // so it is a grouped ncclSend/ncclRecv with the encoder receiving each peer's
 // shard directly at full + row_begin*1176 (no staging copy).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -49,6 +50,58 @@ fc_status fc_nccl_comm_destroy(void* comm) {
   if (!comm) return FC_OK;
   ncclResult_t r = ncclCommDestroy(static_cast<ncclComm_t>(comm));
   if (r != ncclSuccess) return nccl_fail(r, "ncclCommDestroy");
+  return FC_OK;
+}
+
+// ---------------------------------------------------------------- CUDA IPC
+static fc_status cuda_err(cudaError_t e, const char* what) {
+  return fail(FC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+fc_status fc_ipc_export(void* dev_ptr, uint8_t handle[64]) {
+  if (!dev_ptr || !handle) return fail(FC_ERR_INVALID_ARG, "dev_ptr/handle is NULL");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "cudaIpcMemHandle_t size");
+  cudaIpcMemHandle_t h;
+  const cudaError_t e = cudaIpcGetMemHandle(&h, dev_ptr);
+  if (e != cudaSuccess) return cuda_err(e, "cudaIpcGetMemHandle");
+  std::memcpy(handle, &h, 64);
+  return FC_OK;
+}
+
+fc_status fc_ipc_export_range(void* ptr, uint8_t handle[64], int64_t* offset) {
+  if (!ptr || !handle || !offset) return fail(FC_ERR_INVALID_ARG, "ptr/handle/offset is NULL");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  // the runtime has no base-address query; the driver's cuMemGetAddressRange does
+  using GetRange = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static GetRange fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return static_cast<GetRange>(nullptr);
+    return reinterpret_cast<GetRange>(f);
+  }();
+  if (!fn) return fail(FC_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+    return fail(FC_ERR_INVALID_ARG, "ptr is not device memory of this process");
+  *offset = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  return fc_ipc_export(reinterpret_cast<void*>(base), handle);
+}
+
+fc_status fc_ipc_import(const uint8_t handle[64], void** dev_ptr) {
+  if (!handle || !dev_ptr) return fail(FC_ERR_INVALID_ARG, "handle/dev_ptr is NULL");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, 64);
+  const cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return cuda_err(e, "cudaIpcOpenMemHandle");
+  return FC_OK;
+}
+
+fc_status fc_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return fail(FC_ERR_INVALID_ARG, "dev_ptr is NULL");
+  const cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  if (e != cudaSuccess) return cuda_err(e, "cudaIpcCloseMemHandle");
   return FC_OK;
 }
 

@@ -18,21 +18,17 @@ constexpr int kMerge = 2;
 constexpr int kBlock = kPatch * kMerge;  // 28: merge-block side in pixels
 constexpr int kCols = FC_TOKEN_COLS;     // 1176
 constexpr int kPrecisionBits = 22;       // Pillow 8bpc fixed point (R4)
-constexpr int kMaxWords = 16;            // <= 64 taps per output on either axis
 
-// One resize axis in the form the kernel consumes (R4):
-// per output index o: first source index xmin[o], tap count cnt[o], and the
-// 22-bit integer weights split into three byte planes packed 4 taps per word
-// (plane 0/1 unsigned bytes, plane 2 signed byte), so that
-//   sum_k px[k]*iw[k] = dp4a(px,P0) + 256*dp4a(px,P1) + 65536*dp4a(px,P2).
+// One resize axis (R4): per output index o the first
+// source index xmin[o], the tap count cnt[o] and Pillow's 22-bit integer
+// weights iw[o][0..cnt) (ksize slots per output).  The kernels' tables (MMA
+// fragments / weight digits) are derived from these per device.
 struct AxisTable {
   int in = 0, out = 0;
   int ksize = 0;   // Pillow ksize
   int max_cnt = 0; // widest window actually used
-  int words = 0;   // ceil(max_cnt/4)
   std::vector<int32_t> xmin, cnt;
   std::vector<int32_t> iw;       // out x ksize integer weights
-  std::vector<uint32_t> planes;  // out x 3 x words
 };
 
 struct RankPlan {

@@ -81,27 +81,12 @@ fc_status build_axis(int in, int out, AxisTable* t) {
     max_cnt = std::max(max_cnt, xmax);
   }
   t->max_cnt = max_cnt;
-  t->words = (max_cnt + 3) / 4;
-  if (t->words < 1) t->words = 1;
-  if (t->words > kMaxWords)
-    return fail(FC_ERR_UNSUPPORTED, "resize window of " + std::to_string(max_cnt) + " taps exceeds " +
-                                        std::to_string(4 * kMaxWords) + " (downscale factor too large)");
-  // byte planes: iw = P2*65536 + P1*256 + P0, P0/P1 in [0,255], P2 signed
-  const int W = t->words;
-  t->planes.assign(static_cast<size_t>(out) * 3 * W, 0u);
+  // the kernels split each weight into three bytes (the mma.sync kernel: two
+  // unsigned low bytes and a signed high byte), so |iw| < 2^23 is required
   for (int o = 0; o < out; ++o)
     for (int kk = 0; kk < t->cnt[o]; ++kk) {
-      const int32_t v = t->iw[static_cast<size_t>(o) * ksize + kk];
-      const uint32_t b0 = static_cast<uint32_t>(v) & 0xFFu;
-      const uint32_t b1 = (static_cast<uint32_t>(v) >> 8) & 0xFFu;
-      const int32_t hi = v >> 16;  // arithmetic: in [-128, 127] for |v| < 2^23
+      const int32_t hi = t->iw[static_cast<size_t>(o) * ksize + kk] >> 16;
       if (hi < -128 || hi > 127) return fail(FC_ERR_UNSUPPORTED, "resize weight out of byte-plane range");
-      const uint32_t b2 = static_cast<uint32_t>(hi) & 0xFFu;
-      const int word = kk >> 2, sh = (kk & 3) * 8;
-      uint32_t* p = &t->planes[(static_cast<size_t>(o) * 3) * W];
-      p[0 * W + word] |= b0 << sh;
-      p[1 * W + word] |= b1 << sh;
-      p[2 * W + word] |= b2 << sh;
     }
   return FC_OK;
 }
