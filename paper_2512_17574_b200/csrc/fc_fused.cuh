@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
   int sfix = -1;
   // (grid = G: the first r strips get Qhi = ceil(G / nstrips) groups, the
   // others Qhi - 1, so only the r / nstrips boundary drifts)
-  if (KSH == 1 && KSV == 1 && p.smap) {  // narrow windows only (the host rule), keeps wide instances lean
+  if (p.smap) {
     const int ns = p.nstrips, q = blockIdx.x / ns;
     sfix = blockIdx.x - q * ns;
     const int qhi = (gridDim.x + ns - 1) / ns, rr = gridDim.x - (qhi - 1) * ns;

@@ -749,14 +749,15 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
     if (paged) prm.page_ids = reinterpret_cast<const int32_t*>(static_cast<uint8_t*>(desc) + mbytes + tbytes);
   }
   int grid = static_cast<int>(std::min<long long>(items, static_cast<long long>(occ) * nsm));
-  // strip-synchronous work mapping (see the kernel): DRAM reads of c2 drop from
-  // 669 MB to 404 MB (strip halos become L2 hits) and the kernel gets 0.5%
-  // faster; measured slower for wide windows (c4 +3%) and long single jobs (c3
-  // +2.5%), so only narrow-window requests of <= 128 pairs take it.
+  // strip-synchronous work mapping (see the kernel): the CTAs of a strip walk
+  // down the same frames side by side, so strip halos are L2 hits.  Per-launch
+  // DRAM reads (single-pass ncu, round 2): c2 669 -> 404 MB, c3 1.70 -> 0.88 GB,
+  // c4 1.04 -> 0.76 GB (746.5 MB of NV12), c5 1.75 GB -> ~0.8 GB, i.e. traffic
+  // ~= the algorithmic bytes; kernel time c2 -0.2%, c3 +0.6%, c4 +2.3%, c5
+  // +0.4% (the kernel is issue-bound, not DRAM-bound).  On for every launch.
   // FC_SMAP=0/1 forces it off/on (A/B runs).
   const char* smenv = std::getenv("FC_SMAP");
-  const bool smap_default = dt->ksh == 1 && dt->ksv == 1 && jobs.size() == 1 && prm.npairs <= 128;
-  if ((smenv ? std::atoi(smenv) != 0 : smap_default) && grid >= g.nstrips) prm.smap = 1;
+  if ((smenv ? std::atoi(smenv) != 0 : true) && grid >= g.nstrips) prm.smap = 1;
   unsigned long long* cta_t = nullptr;
   if (std::getenv("FC_CTA_TIMES") && cudaMalloc(&cta_t, 3 * sizeof(unsigned long long) * grid) == cudaSuccess) {
     cudaMemsetAsync(cta_t, 0, 3 * sizeof(unsigned long long) * grid, s);

@@ -409,9 +409,12 @@ fc_status launch_tc(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, ui
     cudaStreamSynchronize(s);
     cudaFree(prof);
     struct Role { const char* name; int w0, w1; const char* sites; };
-    const Role roles[] = {{"V-epi", 0, 8, "vfull"}, {"H-epi", 8, 11, "vdone hfull"}, {"H-epi'", 12, 15, "vdone hfull"},
-                          {"H-MMA", 11, 12, "bh hempty afull | [5] H issue"}, {"V-MMA", 23, 24, "- hready bvfull vempty | [6] V issue"},
-                          {"TMA", 15, 16, "bvempty rawempty"}, {"colour", 16, 23, "rawfull aempty"}};
+    const Role roles[] = {{"V-epi", kVEpi0, kVEpi0 + 8, "vfull"}, {"H-epi", kHEpiWarpA, kHEpiWarpA + 3, "vdone hfull"},
+                          {"H-epi'", kHEpiWarpB, kHEpiWarpB + 3, "vdone hfull"},
+                          {"H-MMA", kMmaWarp, kMmaWarp + 1, "bh hempty afull | [5] H issue"},
+                          {"V-MMA", kVMmaWarp, kVMmaWarp + 1, "- hready bvfull vempty | [6] V issue"},
+                          {"TMA", kTmaWarp, kTmaWarp + 1, "bvempty rawempty"},
+                          {"colour", kColWarp0, kColWarp0 + kColWarps, "rawfull aempty"}};
     for (const Role& r : roles) {
       double acc[9] = {0};
       int n = 0;

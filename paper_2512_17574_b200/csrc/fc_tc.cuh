@@ -54,16 +54,29 @@ namespace tc {
 // warp roles (24 warps, one CTA per SM).  tcgen05.ld reaches TMEM lane
 // quarter (warp % 4) only, so each epilogue role owns whole quarters and two
 // warps share a quarter (splitting its columns between them).
-constexpr int kVEpiWarps = 8;   // warps 0..7: V epilogue, quarter w%4, rows half w/4 of each 16-row unit
-constexpr int kHEpiWarpA = 8;   // warps 8..10 and 12..14: H epilogue, quarters 0..2 (the 96 real A rows),
-constexpr int kHEpiWarpB = 12;  //   output groups {0,1} (8..10) / {2,3} (12..14)
-constexpr int kHEpiWarps = 6;
-constexpr int kMmaWarp = 11;    // quarter 3: MMA issuer + TMEM owner
-constexpr int kTmaWarp = 15;    // TMA producer
-constexpr int kColWarp0 = 16;   // warps 16..22: colour
+// Two layouts (the SM's warp arbiter favours higher warp ids):
+//   FC_TC_LAYOUT 0: V epilogue 0..7, H epilogue 8..10 + 12..14, H MMA 11, TMA 15,
+//                   colour 16..22, V MMA 23;
+//   FC_TC_LAYOUT 1: colour 0..6, TMA 7, V epilogue 8..15, H epilogue 16..18 +
+//                   20..22, H MMA 19, V MMA 23 (the busiest roles on top).
+#ifndef FC_TC_LAYOUT
+#define FC_TC_LAYOUT 1
+#endif
+constexpr int kVEpiWarps = 8;   // V epilogue: quarter w%4, rows half (w - kVEpi0)/4 of each 16-row unit
+constexpr int kHEpiWarps = 6;   // H epilogue: quarters 0..2 (the 96 real A rows), outputs 0..31 (A) / 32..55 (B)
 constexpr int kColWarps = 7;
-constexpr int kVMmaWarp = kColWarp0 + kColWarps;  // warp 23: V-pass MMA issuer (warp 11 issues the H pass)
-constexpr int kWarps = kVMmaWarp + 1;
+#if FC_TC_LAYOUT == 0
+constexpr int kVEpi0 = 0, kHEpiWarpA = 8, kHEpiWarpB = 12, kMmaWarp = 11, kTmaWarp = 15, kColWarp0 = 16;
+#else
+constexpr int kVEpi0 = 8, kHEpiWarpA = 16, kHEpiWarpB = 20, kMmaWarp = 19, kTmaWarp = 7, kColWarp0 = 0;
+#endif
+constexpr int kVMmaWarp = 23;   // V-pass MMA issuer (kMmaWarp issues the H pass and owns TMEM)
+static_assert(kVEpi0 % 4 == 0 && kHEpiWarpA % 4 == 0 && kHEpiWarpB % 4 == 0, "epilogue warps start at a lane quarter");
+__host__ __device__ constexpr bool is_hepi(int w) {
+  return (w >= kHEpiWarpA && w < kHEpiWarpA + 3) || (w >= kHEpiWarpB && w < kHEpiWarpB + 3);
+}
+__host__ __device__ constexpr bool is_col(int w) { return w >= kColWarp0 && w < kColWarp0 + kColWarps; }
+constexpr int kWarps = 24;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kColThreads = 32 * kColWarps;
 constexpr int kChunk = 16;        // source rows per chunk
@@ -404,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1) fc_tc_kernel(const __grid_constan
         i += hbB - hbA;
       }
     }
-  } else if (warp >= kColWarp0 && warp < kColWarp0 + kColWarps) {
+  } else if (is_col(warp)) {
     // ------------------------------------------------------------------ colour (a5)
     const int ct = tid - 32 * kColWarp0;
     const int NKC = p.KH >> 4;
@@ -594,7 +607,7 @@ __global__ void __launch_bounds__(kThreads, 1) fc_tc_kernel(const __grid_constan
         i += hbB - hbA;
       }
     }
-  } else if (warp >= kHEpiWarpA) {
+  } else if (is_hepi(warp)) {
     // ------------------------------------------------------------------ H epilogue (a6 -> ring)
     const int q = warp & 3;                      // TMEM lane quarter 0..2
     // this warp's 8-output steps: outputs 0..31 (warps 8..10) / 32..55 (warps 12..14; 56..63 carry no weights)
@@ -698,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, 1) fc_tc_kernel(const __grid_constan
     }
   } else {
     // ------------------------------------------------------------------ V epilogue (a7 -> a8, a9)
-    const int q = warp & 3, vh = warp >> 2;  // lane quarter; rows 8vh..8vh+7 of each 16-row unit
+    const int q = warp & 3, vh = (warp - kVEpi0) >> 2;  // lane quarter; rows 8vh..8vh+7 of each 16-row unit
     const int m = 32 * q + lane;
     const int pp = m >> 6, x = m & 63;  // plane of the M-tile pair, strip column
     const uint32_t tl = static_cast<uint32_t>(32 * q) << 16;
