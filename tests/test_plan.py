@@ -195,6 +195,44 @@ def test_no_cpu_fallback(fc):
     assert b"sm_100" in fc.lib().fc_last_error() or b"cuda" in fc.lib().fc_last_error().lower()
 
 
+def test_no_cpu_fallback_submit_and_tc(fc, monkeypatch):
+    """fc_submit and the tcgen05 route (FC_TC=1) fail loudly too without an
+    sm_100 device: no plan is returned, nothing computes on the CPU."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    buf = (ctypes.c_uint8 * (48 * 64 * 2 + 64))()
+    base = (ctypes.addressof(buf) + 15) & ~15
+    surf = fc.SurfaceTable(100)
+    for i in (0, 10):
+        surf.arr[i] = fc._native.Nv12SurfaceC(base, base + 48 * 64, 64, 64)
+    meta = fc.VideoMeta(64, 48, 100, (30, 1), [0, 50])
+    cfg = fc.ModelCfg(sampling="explicit", explicit_indices=[0, 10])
+    m, _km = meta.to_c()
+    c, _kc = cfg.to_c()
+    out = (ctypes.c_float * (28 * 1176 * 4))()
+    h = ctypes.c_void_p()
+    for tc in ("0", "1"):
+        monkeypatch.setenv("FC_TC", tc)
+        st = fc.lib().fc_submit(ctypes.byref(m), ctypes.byref(c), 0, surf.arr, 100, ctypes.cast(out, ctypes.c_void_p),
+                                None, ctypes.byref(h))
+        assert fc._native.STATUS[st] == "FC_ERR_CUDA" and not h.value
+        assert fc.lib().fc_last_kernel() == 0  # no launch happened on this thread
+
+
+def test_ipc_and_submit_argument_errors(fc):
+    """Host-side validation of the round-2 entry points (no CUDA call needed)."""
+    h = (ctypes.c_uint8 * 64)()
+    assert fc._native.STATUS[fc.lib().fc_ipc_export(None, h)] == "FC_ERR_INVALID_ARG"
+    assert fc._native.STATUS[fc.lib().fc_ipc_import(None, None)] == "FC_ERR_INVALID_ARG"
+    assert fc._native.STATUS[fc.lib().fc_ipc_close(None)] == "FC_ERR_INVALID_ARG"
+    off = ctypes.c_int64()
+    assert fc._native.STATUS[fc.lib().fc_ipc_export_range(None, h, ctypes.byref(off))] == "FC_ERR_INVALID_ARG"
+    assert fc._native.STATUS[fc.lib().fc_submit(None, None, 0, None, 0, None, None, None)] == "FC_ERR_INVALID_ARG"
+    n = ctypes.c_int32()
+    assert fc._native.STATUS[fc.lib().fc_exchange_schedule(None, 0, 0, None, 0, ctypes.byref(n))] == "FC_ERR_INVALID_ARG"
+
+
 def test_missing_surface_reported(fc):
     p = plan_of(fc, 64, 48, 100, [0, 50], sampling="explicit", explicit_indices=[0, 10])
     surf = fc.SurfaceTable(100)  # all NULL
