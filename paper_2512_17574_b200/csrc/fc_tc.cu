@@ -49,7 +49,7 @@ struct TcTables {
   }
   bool ok = false;
   std::string why;  // why the request is outside the kernel's plan (then the mma.sync kernel runs)
-  int KH = 0, KV = 0, NCH = 0, nchunks = 0, nstrips = 0;
+  int KH = 0, KV = 0, NCH = 0, NCHmax = 0, nchunks = 0, nstrips = 0;
   int32_t* sx0 = nullptr;
   uint8_t* hB = nullptr;
   uint8_t* vB = nullptr;
@@ -146,6 +146,19 @@ fc_status build(const fc_plan_s* P, TcTables* t) {
   if (2 * inflight + 2 > kNVD) {
     t->why = "too many bands per ring window";
     return FC_OK;
+  }
+  // the deepest ring the barrier slots allow (the launch uses what shared memory
+  // leaves: a deeper ring lets the H epilogue run further ahead of the V pass)
+  t->NCHmax = t->NCH;
+  for (int nch = t->NCH + 1; nch + 2 <= kNHR; ++nch) {
+    int n_in = 0;
+    for (int hb = 0; hb < gh2; ++hb) {
+      int n = 0;
+      for (int hb2 = hb; hb2 < gh2 && (vys[2 * hb2] >> 4) < (vys[2 * hb] >> 4) + nch; ++hb2) ++n;
+      n_in = std::max(n_in, n);
+    }
+    if (2 * n_in + 2 > kNVD) break;
+    t->NCHmax = nch;
   }
   // every V output lands inside the doubled table: floor((S + 2^21) / 2^22) in [-48, 303]
   for (int o = 0; o < tv.out; ++o) {
@@ -280,48 +293,55 @@ fc_status launch_tc(fc_plan_s* P, const std::vector<Job>& jobs, void* stream, ui
   prm.KH = t->KH;
   prm.KV = t->KV;
   prm.BW = t->KH;
-  prm.NCH = t->NCH;
   prm.nchunks = t->nchunks;
   prm.rawb = 48 * prm.BW;
   prm.sbo_a = (prm.KH / 16) * kLboA;
   prm.ahb = 16 * prm.sbo_a;
   prm.bvb = 2 * kNV * prm.KV;
-  prm.sbo_v = (prm.NCH + 2) * 256;
-  // shared-memory plan: deepest A_H / raw / B_V pipelines that fit
+  // shared-memory plan: deepest A_H / raw / B_V pipelines that fit, then the
+  // deepest ring that still fits
   int smem = 0;
-  for (int na = 2; na >= 1 && !smem; --na)
+  auto plan = [&](int na, int nr, int nbv, int nch, bool commit) -> int {
+    int off = 1024;  // barriers + TMEM slot
+    const int off_lut = off;
+    off = up1024(off + 3 * kLut2N * 4);
+    const int off_raw = off;
+    off = up1024(off + nr * prm.rawb);
+    const int off_ah = off;
+    off = up1024(off + na * prm.ahb);
+    const int off_bh = off;
+    off = up1024(off + kNH * prm.KH);
+    const int off_bv = off;
+    off = up1024(off + nbv * prm.bvb);
+    const int off_ring = off;
+    off += 24 * (nch + 2) * 256;
+    const int off_tab = off;
+    off += (3 * prm.gh2 * 4 + 15) & ~15;
+    const int total = off + 1024;  // the kernel aligns its base up to 1024
+    if (commit) {
+      prm.NR = nr;
+      prm.NA = na;
+      prm.NBV = nbv;
+      prm.NCH = nch;
+      prm.sbo_v = (nch + 2) * 256;
+      prm.off_lut = off_lut;
+      prm.off_raw = off_raw;
+      prm.off_ah = off_ah;
+      prm.off_bh = off_bh;
+      prm.off_bv = off_bv;
+      prm.off_ring = off_ring;
+      prm.off_tab = off_tab;
+    }
+    return total;
+  };
+  for (int na = 3; na >= 1 && !smem; --na)
     for (int nr = 4; nr >= 2 && !smem; --nr)
-      for (int nbv = kMaxBV; nbv >= 2 && !smem; --nbv) {
-        int off = 1024;  // barriers + TMEM slot
-        const int off_lut = off;
-        off = up1024(off + 3 * kLut2N * 4);
-        const int off_raw = off;
-        off = up1024(off + nr * prm.rawb);
-        const int off_ah = off;
-        off = up1024(off + na * prm.ahb);
-        const int off_bh = off;
-        off = up1024(off + kNH * prm.KH);
-        const int off_bv = off;
-        off = up1024(off + nbv * prm.bvb);
-        const int off_ring = off;
-        off += 24 * prm.sbo_v;
-        const int off_tab = off;
-        off += (3 * prm.gh2 * 4 + 15) & ~15;
-        const int total = off + 1024;  // the kernel aligns its base up to 1024
-        if (total <= max_smem) {
-          smem = total;
-          prm.NR = nr;
-          prm.NA = na;
-          prm.NBV = nbv;
-          prm.off_lut = off_lut;
-          prm.off_raw = off_raw;
-          prm.off_ah = off_ah;
-          prm.off_bh = off_bh;
-          prm.off_bv = off_bv;
-          prm.off_ring = off_ring;
-          prm.off_tab = off_tab;
+      for (int nbv = kMaxBV; nbv >= 2 && !smem; --nbv)
+        if (plan(na, nr, nbv, t->NCH, false) <= max_smem) {
+          int nch = t->NCH;
+          while (nch < t->NCHmax && plan(na, nr, nbv, nch + 1, false) <= max_smem) ++nch;
+          smem = plan(na, nr, nbv, nch, true);
         }
-      }
   if (!smem) return FC_OK;
   *handled = true;
   for (int i = 0; i < 2 * prm.gh2; ++i) prm.cvys[i] = static_cast<uint16_t>(t->hvys[i]);

@@ -98,11 +98,11 @@ constexpr uint32_t kVacc = 2 * kNH;    // V accumulators: columns [384, 480) (2 
 // mbarrier indices in the barrier block
 enum Bar : int {
   kRawFull = 0, kRawEmpty = 4,   // NR <= 4
-  kAFull = 8, kAEmpty = 10,      // NA <= 2
-  kHFull = 12, kHEmpty = 14,
-  kVFull = 16, kVEmpty = 18,
-  kBvFull = 20, kBvEmpty = 24,   // NBV <= 4
-  kBhFull = 28,
+  kAFull = 8, kAEmpty = 11,      // NA <= 3
+  kHFull = 14, kHEmpty = 16,
+  kVFull = 18, kVEmpty = 20,
+  kBvFull = 22, kBvEmpty = 26,   // NBV <= 4
+  kBhFull = 30,
   kVDone = 32,                   // kNVD slots
   kHReady = kVDone + kNVD,       // kNHR slots: chunk cs's ring rows written (H epilogue -> V MMA warp)
   kNumBars = kHReady + 16
@@ -346,9 +346,11 @@ __global__ void __launch_bounds__(kThreads, 1) fc_tc_kernel(const __grid_constan
       mbar_init(&bars[kRawFull + i], 1);
       mbar_init(&bars[kRawEmpty + i], kColWarps);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < p.NA; ++i) {
       mbar_init(&bars[kAFull + i], kColWarps);
       mbar_init(&bars[kAEmpty + i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&bars[kHFull + i], 1);
       mbar_init(&bars[kHEmpty + i], kHEpiWarps);
       mbar_init(&bars[kVFull + i], 1);
