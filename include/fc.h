@@ -38,9 +38,10 @@
 extern "C" {
 #endif
 
-#define FC_ABI_VERSION 4  /* 2: token_dtype + color in fc_model_cfg; tokens as void*
+#define FC_ABI_VERSION 5  /* 2: token_dtype + color in fc_model_cfg; tokens as void*
                              3: surface_format in fc_model_cfg, v plane in the surface
-                             4: fc_exchange_schedule, fc_last_kernel, fc_assign_requests, fc_submit, fc_ipc_* */
+                             4: fc_exchange_schedule, fc_last_kernel, fc_assign_requests, fc_submit, fc_ipc_*
+                             5: the paged buffer's page table (fc_pages_*), fc_paged_copy, FC_ERR_OUT_OF_PAGES */
 #define FC_TOKEN_COLS 1176 /* 3 channels * 2 (temporal patch) * 14 * 14 */
 
 typedef enum {
@@ -53,7 +54,8 @@ typedef enum {
   FC_ERR_RANK = 6,            /* rank outside [0, world_size) */
   FC_ERR_OOM = 7,             /* host or device allocation failed */
   FC_ERR_CUDA = 8,            /* CUDA launch/config error, or no sm_100 device */
-  FC_ERR_NCCL = 9             /* NCCL call failed */
+  FC_ERR_NCCL = 9,            /* NCCL call failed */
+  FC_ERR_OUT_OF_PAGES = 10    /* paged buffer: free list too short (back-pressure) */
 } fc_status;
 
 /* Exact rational frame rate (e.g. 30000/1001). */
@@ -297,6 +299,107 @@ typedef struct {
 
 fc_status fc_preprocess_paged(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
                               int64_t num_surfaces, const fc_paged_tokens* out, int64_t grid_thw[3], void* stream);
+
+/* ---- NEXT-2: the paged embedding buffer (Fig. 10; SPEC
+ * embed_buffer S:218-290) ----
+ *
+ * The buffer's page table is host bookkeeping (fc_pages_*); the data moves in
+ * device kernels: fc_preprocess_paged (vision tokens straight from the pixel
+ * kernel) and fc_paged_copy (read_chunk: pages -> a contiguous chunk, "materialise
+ * into contiguous memory only at use time"; write_chunk: a contiguous
+ * chunk -> pages).  Each iteration's reads or writes are described by the
+ * paper's four indices (reading R21 in DESIGN.md):
+ *   pv_indptr[i] .. pv_indptr[i+1]   request i's tokens in the iteration's
+ *                                    contiguous chunk (CSR; count = difference)
+ *   pv_page_indices[pv_page_indptr[i] .. pv_page_indptr[i+1]]
+ *                                    the pages request i touches this iteration,
+ *                                    in token order
+ *   pv_cu_page_len[i]                tokens request i wrote (or read) in all
+ *                                    previous iterations; its first token this
+ *                                    iteration is token n = pv_cu_page_len[i] mod
+ *                                    page_rows of the first listed page, and the
+ *                                    next ones fill the listed pages in order. */
+typedef struct {
+  int32_t num_requests;
+  const int64_t* pv_indptr;       /* [num_requests + 1], pv_indptr[0] == 0, non-decreasing */
+  const int32_t* pv_page_indptr;  /* [num_requests + 1], pv_page_indptr[0] == 0, non-decreasing */
+  const int32_t* pv_page_indices; /* [pv_page_indptr[num_requests]] page ids */
+  const int64_t* pv_cu_page_len;  /* [num_requests], >= 0 */
+} fc_ragged_index;
+
+typedef enum { FC_PAGE_WRITE = 0, FC_PAGE_READ = 1 } fc_page_op;
+
+/* The page table (SPEC PageTable): total_pages pages of page_rows
+ * tokens (page_rows a power of two <= 2^20); a page is free or owned by
+ * exactly one request; requests are caller-chosen int64 ids.  Not thread-safe
+ * (one owner thread: the scheduler that builds the iteration).  Host only, no
+ * CUDA call.  Errors: FC_ERR_INVALID_ARG, FC_ERR_OOM. */
+typedef struct fc_pages_s fc_pages_t;
+fc_status fc_pages_create(int64_t total_pages, int32_t page_rows, fc_pages_t** out);
+void fc_pages_destroy(fc_pages_t* t);
+
+/* alloc_pages: reserve room for `tokens` more tokens after what
+ * request `req` has written (or had reserved) so far, appending the minimal
+ * number of pages from the free list (lowest ids first); new_ids (may be NULL,
+ * else capacity >= the pages appended) receives them, *n_new their count.
+ * All or nothing: FC_ERR_OUT_OF_PAGES when the free list is too short (the
+ * caller's back-pressure signal, nothing is allocated). */
+fc_status fc_pages_alloc(fc_pages_t* t, int64_t req, int64_t tokens, int32_t* new_ids, int32_t capacity,
+                         int32_t* n_new);
+
+/* Build one iteration's ragged index for n requests: reqs[i] moves counts[i]
+ * tokens (counts[i] >= 0; a request may appear once per call).
+ *   FC_PAGE_WRITE: tokens go after the request's written ones; the pages must
+ *     be allocated (FC_ERR_INVALID_ARG otherwise: SPEC CapacityError).
+ *   FC_PAGE_READ: tokens follow the request's read ones, a prefix-ordered read
+ *     of written tokens (FC_ERR_INVALID_ARG past the written count: SPEC
+ *     UnwrittenRange).  Pages whose last token this read consumes become
+ *     "consumed"; fc_pages_free_consumed releases them.
+ * The cursors advance at this call (the caller orders the device work on a
+ * stream).  Outputs are caller arrays: pv_indptr [n + 1], pv_page_indptr
+ * [n + 1], pv_cu_page_len [n], pv_page_indices [capacity]; *num_indices = the
+ * page ids written -- capacity too small -> FC_ERR_INVALID_ARG, *num_indices =
+ * the size needed, nothing changes.  All or nothing on every error. */
+fc_status fc_pages_index(fc_pages_t* t, fc_page_op op, const int64_t* reqs, const int64_t* counts, int32_t n,
+                         int64_t* pv_indptr, int32_t* pv_page_indptr, int32_t* pv_page_indices, int32_t capacity,
+                         int64_t* pv_cu_page_len, int32_t* num_indices);
+
+/* Eager page free (Fig. 10: "processed blocks (e.g., 8 and 11) are
+ * promptly freed"): return every consumed page to the free list; call it once
+ * the iteration's read kernels have completed.  A page is consumed when a read
+ * passes its last token, or when its request was released.  freed (may be
+ * NULL) receives up to `capacity` ids in the order they were consumed;
+ * *n_freed = how many were freed (all of them are, whatever the capacity). */
+fc_status fc_pages_free_consumed(fc_pages_t* t, int32_t* freed, int32_t capacity, int32_t* n_freed);
+
+/* A finished (or cancelled) request: all its pages become consumed (freed at
+ * the next fc_pages_free_consumed) and its id is forgotten.  Unknown id ->
+ * FC_ERR_INVALID_ARG. */
+fc_status fc_pages_release(fc_pages_t* t, int64_t req);
+
+/* Counters: free pages, pages owned by live requests, consumed pages awaiting
+ * fc_pages_free_consumed, live requests (any pointer may be NULL).  free +
+ * owned + consumed == total_pages always. */
+fc_status fc_pages_stats(const fc_pages_t* t, int64_t* free_pages, int64_t* owned_pages, int64_t* consumed_pages,
+                         int64_t* live_requests);
+
+/* read_chunk / write_chunk on the device: moves the iteration's tokens between
+ * the pool and a contiguous chunk, as `idx` says.
+ *   op = FC_PAGE_READ:  chunk row pv_indptr[i] + k  <-  request i's k-th token
+ *   op = FC_PAGE_WRITE: the same rows in the other direction
+ * where request i's k-th token is pool row page * page_rows + s % page_rows,
+ * page = pv_page_indices[pv_page_indptr[i] + s / page_rows], s = n + k,
+ * n = pv_cu_page_len[i] mod page_rows.
+ *   pool:      device pointer, pool_pages * page_rows rows of row_bytes
+ *   chunk:     device pointer, pv_indptr[num_requests] rows of row_bytes
+ *   row_bytes: a multiple of 8 (fp32 tokens 4704, bf16 2352, u8 codes 1176);
+ *              pool and chunk 16-byte aligned.
+ *   idx:       HOST arrays, validated (monotone pointers, enough pages for
+ *              each request, ids inside the pool) and uploaded with the launch.
+ * One HBM-bound kernel launch on `stream` (none for an empty chunk).  Errors:
+ * FC_ERR_INVALID_ARG (nothing launched), FC_ERR_CUDA. */
+fc_status fc_paged_copy(fc_page_op op, const fc_ragged_index* idx, void* pool, int64_t pool_pages, int32_t page_rows,
+                        int64_t row_bytes, void* chunk, void* stream);
 
 /* fc_expand_tokens -- R5 on u8 codes (FC_TOKENS_U8 output of fc_preprocess,
  * usually gathered from all ranks): tokens[r][i] = table[channel(i)][codes[r][i]]

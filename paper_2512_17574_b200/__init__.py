@@ -21,7 +21,7 @@ from . import _native
 from ._native import FcError, FC_TOKEN_COLS, check, lib
 
 __all__ = ["VideoMeta", "ModelCfg", "Plan", "SurfaceTable", "preprocess", "preprocess_debug", "preprocess_batch",
-           "expand_tokens", "preprocess_paged",
+           "expand_tokens", "preprocess_paged", "PageTable", "RaggedIndex", "paged_copy",
            "NcclComm", "gather", "exchange_schedule", "last_kernel", "assign_requests", "submit", "ipc_export", "PeerBuffer", "FcError", "FC_TOKEN_COLS", "lib"]
 
 
@@ -307,6 +307,88 @@ def preprocess_paged(plan: Plan, rank: int, surfaces: SurfaceTable, pool, page_i
     grid = (ctypes.c_int64 * 3)()
     check(lib().fc_preprocess_paged(plan.handle, rank, surfaces.arr, surfaces.n, ctypes.byref(d), grid,
                                     _stream_ptr(stream)), "fc_preprocess_paged")
+
+
+@dataclass
+class RaggedIndex:
+    """One iteration's four indices: pv_indptr [n+1],
+    pv_page_indptr [n+1], pv_page_indices, pv_cu_page_len [n] (host lists)."""
+    pv_indptr: list
+    pv_page_indptr: list
+    pv_page_indices: list
+    pv_cu_page_len: list
+
+    def to_c(self):
+        n = len(self.pv_cu_page_len)
+        arrs = ((ctypes.c_int64 * (n + 1))(*self.pv_indptr), (ctypes.c_int32 * (n + 1))(*self.pv_page_indptr),
+                (ctypes.c_int32 * max(len(self.pv_page_indices), 1))(*self.pv_page_indices),
+                (ctypes.c_int64 * max(n, 1))(*self.pv_cu_page_len))
+        c = _native.RaggedIndexC(n, *(ctypes.cast(a, ctypes.POINTER(t)) for a, t in
+                                      zip(arrs, (ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64))))
+        return c, arrs  # keep arrs alive with the struct
+
+
+class PageTable:
+    """fc_pages_* (NEXT-2): the paged embedding buffer's page table
+    (host bookkeeping in libfc; the data moves in fc_preprocess_paged and
+    fc_paged_copy)."""
+
+    def __init__(self, total_pages: int, page_rows: int):
+        self._h = ctypes.c_void_p()
+        check(lib().fc_pages_create(total_pages, page_rows, ctypes.byref(self._h)), "fc_pages_create")
+        self.total_pages, self.page_rows = total_pages, page_rows
+
+    def alloc(self, req: int, tokens: int) -> list[int]:
+        cap = tokens // self.page_rows + 2
+        ids, n = (ctypes.c_int32 * cap)(), ctypes.c_int32()
+        check(lib().fc_pages_alloc(self._h, req, tokens, ids, cap, ctypes.byref(n)), "fc_pages_alloc")
+        return list(ids[:n.value])
+
+    def index(self, op: str, reqs: Sequence[int], counts: Sequence[int]) -> RaggedIndex:
+        n = len(reqs)
+        r, c = (ctypes.c_int64 * max(n, 1))(*reqs), (ctypes.c_int64 * max(n, 1))(*counts)
+        indptr, pindptr, cu = (ctypes.c_int64 * (n + 1))(), (ctypes.c_int32 * (n + 1))(), (ctypes.c_int64 * max(n, 1))()
+        m = ctypes.c_int32()
+        cap = sum(int(x) // self.page_rows + 2 for x in counts)
+        pages = (ctypes.c_int32 * max(cap, 1))()
+        check(lib().fc_pages_index(self._h, _native.PAGE_OPS[op], r, c, n, indptr, pindptr, pages, cap, cu,
+                                   ctypes.byref(m)), "fc_pages_index")
+        return RaggedIndex(list(indptr), list(pindptr), list(pages[:m.value]), list(cu[:n]))
+
+    def free_consumed(self) -> list[int]:
+        _, _, consumed, _ = self.stats()
+        ids, n = (ctypes.c_int32 * max(consumed, 1))(), ctypes.c_int32()
+        check(lib().fc_pages_free_consumed(self._h, ids, max(consumed, 1), ctypes.byref(n)), "fc_pages_free_consumed")
+        return list(ids[:n.value])
+
+    def release(self, req: int) -> None:
+        check(lib().fc_pages_release(self._h, req), "fc_pages_release")
+
+    def stats(self) -> tuple[int, int, int, int]:
+        """(free pages, owned pages, consumed pages, live requests)"""
+        v = [ctypes.c_int64() for _ in range(4)]
+        check(lib().fc_pages_stats(self._h, *(ctypes.byref(x) for x in v)), "fc_pages_stats")
+        return tuple(x.value for x in v)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().fc_pages_destroy(h)
+            except (TypeError, AttributeError):  # interpreter teardown: module globals already cleared
+                pass
+            self._h = None
+
+
+def paged_copy(op: str, index: RaggedIndex, pool, chunk, stream=None) -> None:
+    """fc_paged_copy (NEXT-2 read_chunk / write_chunk): op "read" gathers the
+    iteration's tokens from pool [pool_pages, page_rows, cols] into chunk
+    [pv_indptr[-1], cols]; "write" scatters them back.  One HBM-bound launch."""
+    c, _keep = index.to_c()
+    row_bytes = pool.shape[2] * pool.element_size()
+    check(lib().fc_paged_copy(_native.PAGE_OPS[op], ctypes.byref(c), ctypes.c_void_p(pool.data_ptr()), pool.shape[0],
+                              pool.shape[1], row_bytes, ctypes.c_void_p(chunk.data_ptr()), _stream_ptr(stream)),
+          "fc_paged_copy")
 
 
 def expand_tokens(plan: Plan, codes, out=None, out_dtype: str = "f32", stream=None):

@@ -15,10 +15,10 @@ LIB_PATH = os.path.join(HERE, f"libfc_{os.environ['FC_LIB_VARIANT']}.so" if os.e
                         else "libfc.so")
 
 FC_TOKEN_COLS = 1176
-ABI_VERSION = 4  # include/fc.h FC_ABI_VERSION this binding marshals for
+ABI_VERSION = 5  # include/fc.h FC_ABI_VERSION this binding marshals for
 STATUS = {0: "FC_OK", 1: "FC_ERR_INVALID_ARG", 2: "FC_ERR_EMPTY_SELECTION", 3: "FC_ERR_ASPECT_RATIO",
           4: "FC_ERR_UNSUPPORTED", 5: "FC_ERR_MISSING_SURFACE", 6: "FC_ERR_RANK", 7: "FC_ERR_OOM",
-          8: "FC_ERR_CUDA", 9: "FC_ERR_NCCL"}
+          8: "FC_ERR_CUDA", 9: "FC_ERR_NCCL", 10: "FC_ERR_OUT_OF_PAGES"}
 SAMPLING = {"fps_stride": 0, "linspace": 1, "explicit": 2}
 TOKEN_DTYPES = {"f32": 0, "bf16": 1, "u8": 2}
 COLORS = {"bt601": 0, "bt709": 1, "bt601_full": 2, "bt709_full": 3}
@@ -60,6 +60,16 @@ class PagedTokensC(ctypes.Structure):
                 ("first_offset", ctypes.c_int64)]
 
 
+class RaggedIndexC(ctypes.Structure):
+    _fields_ = [("num_requests", ctypes.c_int32), ("pv_indptr", ctypes.POINTER(ctypes.c_int64)),
+                ("pv_page_indptr", ctypes.POINTER(ctypes.c_int32)),
+                ("pv_page_indices", ctypes.POINTER(ctypes.c_int32)),
+                ("pv_cu_page_len", ctypes.POINTER(ctypes.c_int64))]
+
+
+PAGE_OPS = {"write": 0, "read": 1}
+
+
 class PlanInfoC(ctypes.Structure):
     _fields_ = [("grid_thw", ctypes.c_int64 * 3), ("resized_h", ctypes.c_int32), ("resized_w", ctypes.c_int32),
                 ("num_sampled", ctypes.c_int64), ("pad_frames", ctypes.c_int64), ("token_rows", ctypes.c_int64),
@@ -95,7 +105,8 @@ EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_g
            "fc_abi_version", "fc_kernel_launches", "fc_expand_tokens", "fc_preprocess_paged",
            "fc_preprocess_colsplit", "fc_scatter_columns", "fc_exchange_schedule", "fc_last_kernel",
            "fc_assign_requests", "fc_submit", "fc_ipc_export", "fc_ipc_export_range", "fc_ipc_import",
-           "fc_ipc_close"]
+           "fc_ipc_close", "fc_pages_create", "fc_pages_destroy", "fc_pages_alloc", "fc_pages_index",
+           "fc_pages_free_consumed", "fc_pages_release", "fc_pages_stats", "fc_paged_copy"]
 
 _lib = None
 
@@ -148,11 +159,21 @@ def lib() -> ctypes.CDLL:
     L.fc_ipc_export_range.argtypes = [vp, ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(ctypes.c_int64)]
     L.fc_ipc_import.argtypes = [ctypes.POINTER(ctypes.c_uint8), ctypes.POINTER(vp)]
     L.fc_ipc_close.argtypes = [vp]
+    pi32, pi64 = ctypes.POINTER(i32), ctypes.POINTER(i64)
+    L.fc_pages_create.argtypes = [i64, i32, ctypes.POINTER(vp)]
+    L.fc_pages_destroy.argtypes = [vp]
+    L.fc_pages_destroy.restype = None
+    L.fc_pages_alloc.argtypes = [vp, i64, i64, pi32, i32, pi32]
+    L.fc_pages_index.argtypes = [vp, ctypes.c_int, pi64, pi64, i32, pi64, pi32, pi32, i32, pi64, pi32]
+    L.fc_pages_free_consumed.argtypes = [vp, pi32, i32, pi32]
+    L.fc_pages_release.argtypes = [vp, i64]
+    L.fc_pages_stats.argtypes = [vp, pi64, pi64, pi64, pi64]
+    L.fc_paged_copy.argtypes = [ctypes.c_int, ctypes.POINTER(RaggedIndexC), vp, i64, i32, i64, vp, vp]
     L.fc_last_kernel.argtypes = []
     L.fc_last_kernel.restype = ctypes.c_int32
     for name in EXPORTS:
         fn = getattr(L, name)
-        if name not in ("fc_model_cfg_default", "fc_plan_destroy", "fc_status_string", "fc_last_error",
+        if name not in ("fc_model_cfg_default", "fc_plan_destroy", "fc_pages_destroy", "fc_status_string", "fc_last_error",
                         "fc_abi_version", "fc_kernel_launches", "fc_last_kernel"):
             fn.restype = ctypes.c_int
     _lib = L

@@ -567,6 +567,7 @@ const char* fc_status_string(fc_status s) {
     case FC_ERR_OOM: return "FC_ERR_OOM";
     case FC_ERR_CUDA: return "FC_ERR_CUDA";
     case FC_ERR_NCCL: return "FC_ERR_NCCL";
+    case FC_ERR_OUT_OF_PAGES: return "FC_ERR_OUT_OF_PAGES";
   }
   return "FC_ERR_UNKNOWN";
 }
