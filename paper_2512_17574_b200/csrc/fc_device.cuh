@@ -115,6 +115,33 @@ __device__ __forceinline__ void yuv2rgb_4(uint32_t yw, uint32_t uvw, uint32_t& R
   B = __byte_perm(b01, b23, 0x7531);
 }
 
+// yuv2rgb_4 on two vertically adjacent rows of 4 pixels that share their
+// chroma (4:2:0): ye / yo = the even / odd row's Y0..Y3.  The chroma-only
+// term of G (cGV*V + bias) is computed once for both rows.
+__device__ __forceinline__ void yuv2rgb_4x2(uint32_t ye, uint32_t yo, uint32_t uvw, uint32_t& Re, uint32_t& Ge,
+                                            uint32_t& Be, uint32_t& Ro, uint32_t& Go, uint32_t& Bo, uint32_t kR,
+                                            uint32_t kG, uint32_t kGv, uint32_t kB, int bR, int bG, int bB) {
+  const int g0 = dp2a_lo(kGv, uvw, bG);  // cGV*V0 + bias (kGv's low half is 0: U0 drops out)
+  const int g1 = dp2a_hi(kGv, uvw, bG);  // cGV*V1 + bias
+  auto row = [&](uint32_t yw, uint32_t& R, uint32_t& G, uint32_t& B) {
+    const uint32_t yv01 = __byte_perm(yw, uvw, 0x5150);
+    const uint32_t yv23 = __byte_perm(yw, uvw, 0x7372);
+    const uint32_t yu01 = __byte_perm(yw, uvw, 0x4140);
+    const uint32_t yu23 = __byte_perm(yw, uvw, 0x6362);
+    const uint32_t r01 = pack_sat_u16(dp2a_hi(kR, yv01, bR), dp2a_lo(kR, yv01, bR));
+    const uint32_t r23 = pack_sat_u16(dp2a_hi(kR, yv23, bR), dp2a_lo(kR, yv23, bR));
+    const uint32_t b01 = pack_sat_u16(dp2a_hi(kB, yu01, bB), dp2a_lo(kB, yu01, bB));
+    const uint32_t b23 = pack_sat_u16(dp2a_hi(kB, yu23, bB), dp2a_lo(kB, yu23, bB));
+    const uint32_t g01 = pack_sat_u16(dp2a_hi(kG, yu01, g0), dp2a_lo(kG, yu01, g0));
+    const uint32_t g23 = pack_sat_u16(dp2a_hi(kG, yu23, g1), dp2a_lo(kG, yu23, g1));
+    R = __byte_perm(r01, r23, 0x7531);
+    G = __byte_perm(g01, g23, 0x7531);
+    B = __byte_perm(b01, b23, 0x7531);
+  };
+  row(ye, Re, Ge, Be);
+  row(yo, Ro, Go, Bo);
+}
+
 // ---------------------------------------------------------------- int8 MMA
 // D = A(16x32 u8, row) * B(32x8, col) + C, s32.  Fragment layout (g = lane/4,
 // t = lane%4; verified on B200 by tools/ubench/mma_layout.cu):
@@ -196,6 +223,10 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   uint2 v;
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
   return v;
+}
+// the four words of one MMA A fragment (a0..a3 land in consecutive registers)
+__device__ __forceinline__ void lds128(uint32_t (&a)[4], uint32_t addr) {
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]) : "r"(addr));
 }
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;

@@ -30,6 +30,9 @@
 
 namespace fc {
 
+#ifndef FC_HG1
+#define FC_HG1 3  // H-pass planes interleaved per MMA group, narrow windows (A/B knob)
+#endif
 constexpr int kChunkRows = 16;             // source rows per chunk
 constexpr int kTileN = 8;                  // outputs per H-pass MMA tile (N of m16n8k32)
 constexpr int kStrip = 56;                 // output columns per strip: 2 merge blocks = 4 patches
@@ -189,7 +192,10 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
   const int NS = p.nstages;
   const uint32_t smask = static_cast<uint32_t>(NS - 1);
   const int SWP = p.SWP;
-  uint8_t* rgb = raw + NS * 2 * RAWF;                             // [2 f][3 c][16 rows][SWP]
+  // RGB planes [2 f][3 c][8 row pairs][2 SWP]: a row pair interleaves its two
+  // rows in 4-byte column groups, (row r, column x) at (r/2)*2SWP + (x/4)*8 +
+  // (r&1)*4 + x%4, so one LDS.128 is a whole H-pass A fragment
+  uint8_t* rgb = raw + NS * 2 * RAWF;
   uint32_t* ring = reinterpret_cast<uint32_t*>(rgb + 6 * CH * SWP);  // [TRW][RS] words: [w][f][c][x]
 
   const int tid = threadIdx.x;
@@ -229,19 +235,20 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
   }
 
   // ------------------------------------------------------------ compute warps
-  // colour items (frame, row, 16-pixel group): at most 2 per thread; their
-  // offsets are launch constants (raw stage: Y / UV byte, RGB plane byte)
-  const int NQ16 = p.SWPN >> 4;
-  const int citems = 2 * CH * NQ16;
+  // colour items (frame, row pair, 8-pixel group): 16 pixels sharing 4 chroma
+  // pairs, at most 2 items per thread; their offsets are launch constants
+  // (raw stage: even-row Y / UV byte, RGB plane byte)
+  const int NQ8 = p.SWPN >> 3;
+  const int citems = 2 * (CH / 2) * NQ8;
   int cy[2], cuv[2], crgb[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const int it = tid + e * kComputeThreads;
-    const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
-    const int xb = 16 * q, sub = xb >> p.bwshift, xo = xb & p.bwmask;
-    cy[e] = f * RAWF + (sub * 16 + rr) * p.BW + xo;
-    cuv[e] = chroma_offset<I420>(p, f * RAWF + 16 * p.BW * p.NX, sub, rr, xo);
-    crgb[e] = ((f * 3) * CH + rr) * SWP + xb;
+    const int q = it % NQ8, rowi = it / NQ8, f = rowi >= CH / 2, rp = rowi - f * (CH / 2);
+    const int xb = 8 * q, sub = xb >> p.bwshift, xo = xb & p.bwmask;
+    cy[e] = f * RAWF + (sub * 16 + 2 * rp) * p.BW + xo;
+    cuv[e] = chroma_offset<I420>(p, f * RAWF + 16 * p.BW * p.NX, sub, 2 * rp, xo);
+    crgb[e] = (f * 3) * CH * SWP + rp * 2 * SWP + 2 * xb;
   }
   const uint32_t rgb_s = smem_u32(rgb);
   const uint32_t ring_s = smem_u32(ring);
@@ -282,19 +289,22 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
           hb[k][pl][1] = __ldg(f + (k * 3 + pl) * 64 + 1);
         }
     }
-    // A-fragment byte addresses in an RGB plane: rows 2g, 2g+1; columns xs + 4t (+16)
-    // H-pass MMA rows g / g+8 are source rows 2g / 2g+1 of the chunk, so each
-    // thread's two rows of one output column are adjacent bytes of one ring word
-    // (SWP = 8 mod 16: rows 2g of the 8 lane groups fall in distinct bank quads)
-    const uint32_t hA0 = rgb_s + 2 * g * SWP + (hact ? __ldg(p.hxs + htile) - SX0 : 0) + 4 * tq;
-    const uint32_t hA1 = hA0 + SWP;
+    // A-fragment address in an RGB plane.  H-pass MMA rows g / g+8 are the two
+    // source rows of row pair hp = (g>>1) | (g&1)<<2: a thread's two rows of one
+    // output column are the two bytes of one ring half-word, and the two row
+    // pairs of a quarter-warp's LDS.128 lie 64 B apart mod 128 (row-pair stride
+    // 2SWP = 16 mod 32): no bank conflicts.  The MMA's K order is permuted (the
+    // host orders the B fragments so): thread t's k = 4t..4t+3 and 16+4t.. are
+    // source columns xs + 8t + [0, 8), i.e. a0 a1 a2 a3 = 16 contiguous bytes.
+    const int hp = (g >> 1) | ((g & 1) << 2);
+    const uint32_t hA = rgb_s + hp * 2 * SWP + 2 * (hact ? __ldg(p.hxs + htile) - SX0 : 0) + 16 * tq;
     // ring columns of this thread's outputs (2t, 2t+1 of the tile); masked past the strip / frame
     const int ho = warp * kTileN + 2 * tq;
     const bool hst0 = hact && ho < p.sw && X0 + ho < p.W2;
     const bool hst1 = hact && ho + 1 < p.sw && X0 + ho + 1 < p.W2;
     int next_k = r.kfirst;
-    // ring words of source rows kfirst*16 + g and + g + 8 (advanced per chunk)
-    int hwA = ((r.kfirst * CH) / 4 + (g >> 1)) % p.TRW;
+    // ring word of source rows kfirst*16 + 2hp, 2hp + 1 (advanced per chunk)
+    int hwA = ((r.kfirst * CH) / 4 + (hp >> 1)) % p.TRW;
     // prefill: the run's first nstages chunks (every stage is free: the previous
     // run consumed all it issued, before the barrier that ended its last band)
     if (issuer)
@@ -308,40 +318,40 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
         const int buf = seq & smask;
         const uint8_t* rawb = raw + buf * 2 * RAWF;
         mbar_wait(&full[buf], (seq >> p.stage_shift) & 1);
-        // ---- a5: NV12 -> RGB planes, 16 pixels per item
+        // ---- a5: NV12 -> RGB planes, 8 pixels x 2 rows per item
         auto convert = [&](int oy, int ouv, int orgb, int e) {
-            const uint4 Yv = *reinterpret_cast<const uint4*>(rawb + oy);
-            uint4 UVv;
-            if constexpr (I420) {  // interleave 8 U and 8 V bytes into NV12 order [U0 V0 U1 V1 ...]
-              const uint2 u = *reinterpret_cast<const uint2*>(rawb + ouv);
-              const uint2 v = *reinterpret_cast<const uint2*>(rawb + ouv + 4 * p.BW);
-              UVv = make_uint4(__byte_perm(u.x, v.x, 0x5140), __byte_perm(u.x, v.x, 0x7362),
-                               __byte_perm(u.y, v.y, 0x5140), __byte_perm(u.y, v.y, 0x7362));
+            const uint2 Ye = *reinterpret_cast<const uint2*>(rawb + oy);          // even row, 8 pixels
+            const uint2 Yo = *reinterpret_cast<const uint2*>(rawb + oy + p.BW);   // odd row
+            uint2 UVv;
+            if constexpr (I420) {  // interleave 4 U and 4 V bytes into NV12 order [U0 V0 U1 V1 ...]
+              const uint32_t u = *reinterpret_cast<const uint32_t*>(rawb + ouv);
+              const uint32_t v = *reinterpret_cast<const uint32_t*>(rawb + ouv + 4 * p.BW);
+              UVv = make_uint2(__byte_perm(u, v, 0x5140), __byte_perm(u, v, 0x7362));
             } else {
-              UVv = *reinterpret_cast<const uint4*>(rawb + ouv);
+              UVv = *reinterpret_cast<const uint2*>(rawb + ouv);
             }
+            // per channel: even row px 0-3, odd row px 0-3, even px 4-7, odd px 4-7
             uint4 Rv, Gv, Bv;
-            yuv2rgb_4(Yv.x, UVv.x, Rv.x, Gv.x, Bv.x, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
-            yuv2rgb_4(Yv.y, UVv.y, Rv.y, Gv.y, Bv.y, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
-            yuv2rgb_4(Yv.z, UVv.z, Rv.z, Gv.z, Bv.z, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
-            yuv2rgb_4(Yv.w, UVv.w, Rv.w, Gv.w, Bv.w, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR, p.cbG, p.cbB);
-            uint8_t* dst = rgb + orgb;  // 8-byte aligned rows (SWP = 8 mod 16)
-            reinterpret_cast<uint2*>(dst)[0] = make_uint2(Rv.x, Rv.y);
-            reinterpret_cast<uint2*>(dst)[1] = make_uint2(Rv.z, Rv.w);
-            reinterpret_cast<uint2*>(dst + CH * SWP)[0] = make_uint2(Gv.x, Gv.y);
-            reinterpret_cast<uint2*>(dst + CH * SWP)[1] = make_uint2(Gv.z, Gv.w);
-            reinterpret_cast<uint2*>(dst + 2 * CH * SWP)[0] = make_uint2(Bv.x, Bv.y);
-            reinterpret_cast<uint2*>(dst + 2 * CH * SWP)[1] = make_uint2(Bv.z, Bv.w);
+            yuv2rgb_4x2(Ye.x, Yo.x, UVv.x, Rv.x, Gv.x, Bv.x, Rv.y, Gv.y, Bv.y, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR,
+                        p.cbG, p.cbB);
+            yuv2rgb_4x2(Ye.y, Yo.y, UVv.y, Rv.z, Gv.z, Bv.z, Rv.w, Gv.w, Bv.w, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR,
+                        p.cbG, p.cbB);
+            uint8_t* dst = rgb + orgb;  // 16-byte aligned (row-pair stride 2SWP = 0 mod 16)
+            *reinterpret_cast<uint4*>(dst) = Rv;
+            *reinterpret_cast<uint4*>(dst + CH * SWP) = Gv;
+            *reinterpret_cast<uint4*>(dst + 2 * CH * SWP) = Bv;
             if (DBG && p.dbg_src != nullptr) {
               const int it = tid + e * kComputeThreads;
-              const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
-              const int y = k * CH + rr, x = SX0 + 16 * q;
-              if (y < p.H) {
-                const uint32_t cw[3][4] = {{Rv.x, Rv.y, Rv.z, Rv.w}, {Gv.x, Gv.y, Gv.z, Gv.w}, {Bv.x, Bv.y, Bv.z, Bv.w}};
-                const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
-                for (int i = 0; i < 16 && x + i < p.W; ++i)
-                  for (int c = 0; c < 3; ++c)
-                    p.dbg_src[((fi * p.H + y) * p.W + x + i) * 3 + c] = (cw[c][i >> 2] >> (8 * (i & 3))) & 0xFF;
+              const int q = it % NQ8, rowi = it / NQ8, f = rowi >= CH / 2, rp = rowi - f * (CH / 2);
+              const uint32_t cw[3][4] = {{Rv.x, Rv.y, Rv.z, Rv.w}, {Gv.x, Gv.y, Gv.z, Gv.w}, {Bv.x, Bv.y, Bv.z, Bv.w}};
+              const size_t fi = static_cast<size_t>(p.frame_base + 2 * r.pair + f);
+              for (int h = 0; h < 2; ++h) {
+                const int y = k * CH + 2 * rp + h, x = SX0 + 8 * q;
+                if (y < p.H)
+                  for (int i = 0; i < 8 && x + i < p.W; ++i)
+                    for (int c = 0; c < 3; ++c)
+                      p.dbg_src[((fi * p.H + y) * p.W + x + i) * 3 + c] =
+                          (cw[c][2 * (i >> 2) + h] >> (8 * (i & 3))) & 0xFF;
               }
             }
         };
@@ -354,10 +364,11 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
             }
           } else {  // very wide resize windows: any number of items
             for (int it = tid; it < citems; it += kComputeThreads) {
-              const int q = it % NQ16, rowi = it / NQ16, f = rowi >= CH, rr = rowi - f * CH;
-              const int xb = 16 * q, sub = xb >> p.bwshift, xo = xb & p.bwmask;
-              convert(f * RAWF + (sub * 16 + rr) * p.BW + xo, chroma_offset<I420>(p, f * RAWF + 16 * p.BW * p.NX, sub, rr, xo),
-                      ((f * 3) * CH + rr) * SWP + xb, (it - tid) / kComputeThreads);
+              const int q = it % NQ8, rowi = it / NQ8, f = rowi >= CH / 2, rp = rowi - f * (CH / 2);
+              const int xb = 8 * q, sub = xb >> p.bwshift, xo = xb & p.bwmask;
+              convert(f * RAWF + (sub * 16 + 2 * rp) * p.BW + xo,
+                      chroma_offset<I420>(p, f * RAWF + 16 * p.BW * p.NX, sub, 2 * rp, xo),
+                      (f * 3) * CH * SWP + rp * 2 * SWP + 2 * xb, (it - tid) / kComputeThreads);
             }
           }
         }
@@ -367,8 +378,8 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
         if (issuer && k + NS < r.klast) issue_chunk<I420>(p, r.pair, SX0, k + NS, raw + buf * 2 * RAWF, &full[buf]);
         // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of 3 for ILP
         if (hact) {
-          const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + 2 * (g & 1);  // bytes of rows 2g, 2g+1
-          constexpr int HG = KSH == 1 ? 3 : 2;  // planes interleaved per group (ILP vs registers)
+          const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + 2 * (hp & 1);  // bytes of rows 2hp, 2hp+1
+          constexpr int HG = KSH == 1 ? FC_HG1 : 2;  // planes interleaved per group (ILP vs registers)
 #pragma unroll
           for (int fg = 0; fg < 6; fg += HG) {
             uint32_t a[HG][KSH][4];
@@ -376,11 +387,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
             for (int e = 0; e < HG; ++e)
 #pragma unroll
               for (int kk = 0; kk < KSH; ++kk) {
-                const uint32_t po = (fg + e) * CH * SWP + 32 * kk;
-                a[e][kk][0] = lds32(hA0 + po);
-                a[e][kk][1] = lds32(hA1 + po);
-                a[e][kk][2] = lds32(hA0 + po + 16);
-                a[e][kk][3] = lds32(hA1 + po + 16);
+                lds128(a[e][kk], hA + (fg + e) * CH * SWP + 64 * kk);  // k-step kk: 32 columns x 2 rows
               }
             int d2[HG][4], d1[HG][4], d0[HG][4];
 #pragma unroll
@@ -388,12 +395,12 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
 #pragma unroll
             for (int e = 0; e < HG; ++e) {
               // clip8 (R4) = sat_u8(S >> 22) (arithmetic shift; S < 2^31 by Pillow's
-              // headroom): d0,d1 = row 2g, columns ho, ho+1; d2,d3 = row 2g+1
+              // headroom): d0,d1 = row 2hp, columns ho, ho+1; d2,d3 = row 2hp+1
               const uint32_t off = (fg + e) * SW * 4;
               int v[4];
 #pragma unroll
               for (int i = 0; i < 4; ++i) v[i] = combine_planes(d2[e][i], d1[e][i], d0[e][i]) >> 22;
-              if (hst0) sts16(dA + off, pack_sat_u8(v[2], v[0], 0u));      // column ho: rows 2g, 2g+1
+              if (hst0) sts16(dA + off, pack_sat_u8(v[2], v[0], 0u));      // column ho: rows 2hp, 2hp+1
               if (hst1) sts16(dA + off + 4, pack_sat_u8(v[3], v[1], 0u));  // column ho + 1
             }
           }

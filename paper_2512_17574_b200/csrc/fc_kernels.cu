@@ -67,8 +67,11 @@ static uint32_t weight_byte(int32_t w, int plane) {
 
 // B fragments of m16n8k32 for a group of 8 outputs (H: 8 columns; V: 8 rows of
 // a band) whose windows start at source index xs: b_r (r = 0,1) of lane
-// (g = lane/4, t = lane%4) holds k = ks*32 + 16 r + 4 t + [0..3] of output g.
-static void frag_group(const AxisTable& t, const int (&outs)[8], int xs, int KS, uint32_t* dst) {
+// (g = lane/4, t = lane%4) holds MMA k = ks*32 + 16 r + 4 t + [0..3] of output
+// g.  V: MMA k is source index xs + k.  H (kperm): the kernel loads A with one
+// LDS.64 per row, so MMA k = ks*32 + 16 r + 4 t + b is source index
+// xs + ks*32 + 8 t + 4 r + b.
+static void frag_group(const AxisTable& t, const int (&outs)[8], int xs, int KS, uint32_t* dst, bool kperm) {
   for (int ks = 0; ks < KS; ++ks)
     for (int pl = 0; pl < 3; ++pl)
       for (int lane = 0; lane < 32; ++lane)
@@ -76,7 +79,7 @@ static void frag_group(const AxisTable& t, const int (&outs)[8], int xs, int KS,
           const int g = lane >> 2, tq = lane & 3;
           uint32_t word = 0;
           for (int bb = 0; bb < 4; ++bb) {
-            const int k = ks * 32 + 16 * rr + 4 * tq + bb;
+            const int k = ks * 32 + (kperm ? 8 * tq + 4 * rr : 16 * rr + 4 * tq) + bb;
             word |= weight_byte(weight_at(t, outs[g], xs + k), pl) << (8 * bb);
           }
           dst[((ks * 3 + pl) * 32 + lane) * 2 + rr] = word;
@@ -131,7 +134,7 @@ static void build_mma_tables(const fc_plan_s* P, int sw, MmaTables* m) {
     int outs[8];
     h_outs(tt, outs);
     const int first = std::min(tt / htiles * sw + 8 * (tt % htiles), th.out - 1);
-    m->hxs[tt] = th.xmin[first] & ~3;
+    m->hxs[tt] = th.xmin[first] & ~7;  // 8-byte aligned LDS.64 A loads
     ksh = std::max(ksh, group_ks(th, outs, m->hxs[tt]));
   }
   for (int grp = 0; grp < gh2 * 4; ++grp) {
@@ -147,12 +150,12 @@ static void build_mma_tables(const fc_plan_s* P, int sw, MmaTables* m) {
   for (int tt = 0; tt < nth; ++tt) {
     int outs[8];
     h_outs(tt, outs);
-    frag_group(th, outs, m->hxs[tt], ksh, &m->hfr[static_cast<size_t>(tt) * ksh * 3 * 64]);
+    frag_group(th, outs, m->hxs[tt], ksh, &m->hfr[static_cast<size_t>(tt) * ksh * 3 * 64], true);
   }
   for (int grp = 0; grp < gh2 * 4; ++grp) {
     int outs[8];
     v_outs(grp, outs);
-    frag_group(tv, outs, m->vys[grp], ksv, &m->vfr[static_cast<size_t>(grp) * ksv * 3 * 64]);
+    frag_group(tv, outs, m->vys[grp], ksv, &m->vfr[static_cast<size_t>(grp) * ksv * 3 * 64], false);
   }
 }
 
@@ -274,15 +277,16 @@ static fc_status choose_geometry(const fc_plan_s* P, const DeviceTables* dt, int
     const int X0 = s * SW, X1 = std::min(X0 + SW, P->w2);
     const int SX0 = th.xmin[X0] & (P->cfg.surface_format == FC_SURFACE_I420 ? ~31 : ~15);  // == the kernel's sxmask
     for (int i = 0; i < g->htiles && X0 + 8 * i < X1; ++i)
-      need = std::max(need, (th.xmin[X0 + 8 * i] & ~3) - SX0 + 32 * dt->ksh);
+      need = std::max(need, (th.xmin[X0 + 8 * i] & ~7) - SX0 + 32 * dt->ksh);
     for (int o = X0; o < X1; ++o) taps = std::max(taps, th.xmin[o] + th.cnt[o] - SX0);
   }
   // converted width; I420 loads U and V boxes of SWPN/2 bytes, which TMA wants
   // in multiples of 16
   const int cq = P->cfg.surface_format == FC_SURFACE_I420 ? 32 : 16;
   need = std::max(need, (taps + cq - 1) / cq * cq);  // the converted width (SWPN) fits every row
-  // round up to 8 mod 16: H-pass lanes g read rows 2g, 2g+1, and with a row
-  // stride of 4m+2 words the rows 2g of the 8 lane groups hit distinct bank quads
+  // round up to 8 mod 16: the H pass's LDS.64 A loads of a half-warp read rows
+  // 0, 4, 8, 12 (or 2, 6, 10, 14) of a chunk, 32 B each; with a row stride of
+  // 8 mod 16 bytes those land in distinct quarters of the 128-B bank space
   const int swp8 = (need + 7) / 8 * 8;
   const int swpb = swp8 % 16 == 8 ? swp8 : swp8 + 8;
   g->SWPN = ((taps + cq - 1) / cq) * cq;

@@ -1,0 +1,5 @@
+# A/B run: parity of the variant (fast subset) + interleaved bench of base and variants
+export PYTHONUNBUFFERED=1
+v=${1:-var}; shift
+FC_LIB_VARIANT=$v timeout 900 python -m pytest tests/test_parity_gpu.py -x -q -m gpu -k "c1_shape or shapes or full_c2 or full_c4 or virtual or i420 or color" 2>&1 | tail -3
+bash tools/ab_simple.sh "c2 c4 c3" base "$v" "$@"
