@@ -30,6 +30,9 @@
 
 namespace fc {
 
+#ifndef FC_PREF
+#define FC_PREF 1  // per-band table reads issued a band ahead (A/B knob)
+#endif
 #ifndef FC_HG1
 #define FC_HG1 3  // H-pass planes interleaved per MMA group, narrow windows (A/B knob)
 #endif
@@ -310,9 +313,20 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
     if (issuer)
       for (int j = 0; j < NS && r.kfirst + j < r.klast; ++j)
         issue_chunk<I420>(p, r.pair, SX0, r.kfirst + j, raw + ((seq + j) & smask) * 2 * RAWF, &full[(seq + j) & smask]);
+#if FC_PREF
+    // per-band table reads are issued one band ahead (their L2 latency was
+    // exposed at every band start): the end row of the band's last V window
+    int vend_nx = __ldg(p.vx + 28 * r.hb0 + 27) + __ldg(p.vcnt + 28 * r.hb0 + 27);
+#endif
     for (int hb_ = r.hb0; hb_ < r.hb1; ++hb_) {
       const int yo0 = hb_ * 28;
+#if FC_PREF
+      const int kneed = min(p.nchunks, (vend_nx + CH - 1) / CH);
+      if (hb_ + 1 < r.hb1) vend_nx = __ldg(p.vx + yo0 + 55) + __ldg(p.vcnt + yo0 + 55);
+      const int ys_pf = __ldg(p.vys + hb_ * 4 + vjg);  // consumed by this band's V pass, after the chunks
+#else
       const int kneed = min(p.nchunks, (__ldg(p.vx + yo0 + 27) + __ldg(p.vcnt + yo0 + 27) + CH - 1) / CH);
+#endif
       for (; next_k < kneed; ++next_k, ++seq) {
         const int k = next_k;
         const int buf = seq & smask;
@@ -422,7 +436,11 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
             vb[kk][pl][0] = __ldg(f + (kk * 3 + pl) * 64);
             vb[kk][pl][1] = __ldg(f + (kk * 3 + pl) * 64 + 1);
           }
+#if FC_PREF
+        const int ys = ys_pf;
+#else
         const int ys = __ldg(p.vys + grp);
+#endif
         // A rows: columns (g, g+8) of a patch; k = source rows ys + 32kk + 4t (+16)
         uint32_t rb[KSV][2];
         {
