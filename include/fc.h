@@ -38,10 +38,11 @@
 extern "C" {
 #endif
 
-#define FC_ABI_VERSION 5  /* 2: token_dtype + color in fc_model_cfg; tokens as void*
+#define FC_ABI_VERSION 6  /* 2: token_dtype + color in fc_model_cfg; tokens as void*
                              3: surface_format in fc_model_cfg, v plane in the surface
                              4: fc_exchange_schedule, fc_last_kernel, fc_assign_requests, fc_submit, fc_ipc_*
-                             5: the paged buffer's page table (fc_pages_*), fc_paged_copy, FC_ERR_OUT_OF_PAGES */
+                             5: the paged buffer's page table (fc_pages_*), fc_paged_copy, FC_ERR_OUT_OF_PAGES
+                             6: fc_model_cfg.backend: HF PIL or torchvision processor arithmetic */
 #define FC_TOKEN_COLS 1176 /* 3 channels * 2 (temporal patch) * 14 * 14 */
 
 typedef enum {
@@ -114,6 +115,21 @@ typedef enum {
   FC_SURFACE_I420 = 1  /* Y plane + separate U and V planes (planar YUV420, "I420") */
 } fc_surface_format;
 
+/* Which HF processor backend's arithmetic the resize (a6, a7) and normalise
+ * (a8) steps reproduce (reading R21; "selectable interpolation
+ * algorithms").  Sampling, smart_resize, colour and patch layout are shared.
+ *   FC_BACKEND_PIL: HF's PIL-backend processor -- Pillow Image.resize(BICUBIC)
+ *     (22-bit fixed point, R4), then f32(f64(v)/255) and (x - mean)/std (R5).
+ *   FC_BACKEND_TORCHVISION: HF's torchvision-backend processor on CPU --
+ *     torch's uint8 antialiased bicubic (the same Pillow windows and double
+ *     weights, rounded at the precision p < 22 that keeps the largest weight of
+ *     the axis an int16: the largest p with (int)(0.5 + wmax*2^(p+1)) < 2^15;
+ *     each pass clamp((2^(p-1) + sum px*iw) >> p) with a u8 intermediate), then
+ *     HF's fused normalisation (f32(v) - mean*f32(1/rescale)) / (std*f32(1/rescale))
+ *     in float32.  (On CUDA tensors torchvision resizes in float, whose bits
+ *     depend on the device; this mode is the CPU uint8 path, bit for bit.) */
+typedef enum { FC_BACKEND_PIL = 0, FC_BACKEND_TORCHVISION = 1 } fc_backend;
+
 /* Model / preprocessing configuration (Qwen2-VL video processor defaults,
  * filled by fc_model_cfg_default). */
 typedef struct {
@@ -140,6 +156,7 @@ typedef struct {
   fc_token_dtype token_dtype;  /* FC_TOKENS_F32 (default) or FC_TOKENS_BF16 */
   fc_color color;              /* FC_COLOR_BT601_LIMITED (default) */
   fc_surface_format surface_format; /* FC_SURFACE_NV12 (default) or FC_SURFACE_I420 (ABI 3) */
+  fc_backend backend;          /* FC_BACKEND_PIL (default) or FC_BACKEND_TORCHVISION (ABI 6) */
 } fc_model_cfg;
 
 void fc_model_cfg_default(fc_model_cfg* cfg);

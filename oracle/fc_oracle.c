@@ -135,24 +135,34 @@ static double cubic(double x) {
 
 #define PRECISION_BITS 22
 
+/* Backends (reading R21): 0 = HF's PIL-backend processor (Pillow,
+ * PRECISION_BITS = 22); 1 = HF's torchvision-backend processor on CPU, whose
+ * uint8 antialiased bicubic (torch.nn.functional.interpolate(antialias=True)
+ * on uint8, ATen's Pillow port) uses the same windows and double weights but
+ * rounds them at a precision p chosen per axis: the largest p < 22 with
+ * (int)(0.5 + wmax * 2^(p+1)) < 2^15, wmax the largest normalised weight of
+ * the axis (int16 weights); each pass is clamp((2^(p-1) + sum px*iw) >> p).
+ * Pinned bit-exact against torch (tests/test_oracle_pins.py). */
 typedef struct {
   int ksize;
+  int prec;   /* fixed-point bits of iw */
   int* xmin;  /* [out] */
   int* cnt;   /* [out] */
   int* iw;    /* [out*ksize] */
 } coeffs_t;
 
-static int make_coeffs(int in, int out, coeffs_t* c) {
+static int make_coeffs(int in, int out, int backend, coeffs_t* c) {
   double scale = (double)in / (double)out;
   double filterscale = scale < 1.0 ? 1.0 : scale;
   double support = 2.0 * filterscale;
   int ksize = (int)ceil(support) * 2 + 1;
-  double* k = (double*)malloc(sizeof(double) * ksize);
+  double* k = (double*)calloc((size_t)out * ksize, sizeof(double)); /* normalised weights, all outputs */
   c->ksize = ksize;
   c->xmin = (int*)malloc(sizeof(int) * out);
   c->cnt = (int*)malloc(sizeof(int) * out);
   c->iw = (int*)calloc((size_t)out * ksize, sizeof(int));
   if (!k || !c->xmin || !c->cnt || !c->iw) return -1;
+  double wmax = 0.0;
   for (int o = 0; o < out; ++o) {
     double center = (o + 0.5) * scale;
     double ww = 0.0;
@@ -162,21 +172,29 @@ static int make_coeffs(int in, int out, coeffs_t* c) {
     int xmax = (int)(center + support + 0.5);
     if (xmax > in) xmax = in;
     xmax -= xmin;
+    double* kk = k + (size_t)o * ksize;
     for (int x = 0; x < xmax; ++x) {
       double w = cubic((x + xmin - center + 0.5) * ss);
-      k[x] = w;
+      kk[x] = w;
       ww += w;
     }
     for (int x = 0; x < xmax; ++x)
-      if (ww != 0.0) k[x] /= ww;
-    for (int x = 0; x < xmax; ++x) {
-      double w = k[x];
-      c->iw[(size_t)o * ksize + x] =
-          (int)(w < 0 ? -0.5 + w * (1 << PRECISION_BITS) : 0.5 + w * (1 << PRECISION_BITS));
-    }
+      if (ww != 0.0) kk[x] /= ww;
+    for (int x = 0; x < xmax; ++x)
+      if (kk[x] > wmax) wmax = kk[x];
     c->xmin[o] = xmin;
     c->cnt[o] = xmax;
   }
+  int prec = PRECISION_BITS;
+  if (backend == 1)
+    for (prec = 0; prec < 22; ++prec)
+      if ((int)(0.5 + wmax * (1 << (prec + 1))) >= (1 << 15)) break;
+  c->prec = prec;
+  for (int o = 0; o < out; ++o)
+    for (int x = 0; x < c->cnt[o]; ++x) {
+      double w = k[(size_t)o * ksize + x];
+      c->iw[(size_t)o * ksize + x] = (int)(w < 0 ? -0.5 + w * (1 << prec) : 0.5 + w * (1 << prec));
+    }
   free(k);
   return 0;
 }
@@ -187,16 +205,18 @@ static void free_coeffs(coeffs_t* c) {
   free(c->iw);
 }
 
-static uint8_t clip8(int64_t v) {
-  if (v >= ((int64_t)1 << PRECISION_BITS << 8)) return 255;
+static uint8_t clip8(int64_t v, int prec) {
+  if (v >= ((int64_t)1 << prec << 8)) return 255;
   if (v <= 0) return 0;
-  return (uint8_t)(v >> PRECISION_BITS);
+  return (uint8_t)(v >> prec);
 }
 
-/* Exposed for tests: the integer coefficient table of one axis. */
-int oracle_resize_coeffs(int in, int out, int* xmin, int* cnt, int* iw, int ksize_cap) {
+/* Exposed for tests: the integer coefficient table of one axis (its
+ * precision in *prec when prec != NULL). */
+int oracle_resize_coeffs(int in, int out, int backend, int* xmin, int* cnt, int* iw, int ksize_cap, int* prec) {
   coeffs_t c;
-  if (make_coeffs(in, out, &c) != 0) return -1;
+  if (make_coeffs(in, out, backend, &c) != 0) return -1;
+  if (prec) *prec = c.prec;
   int ks = c.ksize;
   if (ks <= ksize_cap) {
     memcpy(xmin, c.xmin, sizeof(int) * out);
@@ -207,23 +227,24 @@ int oracle_resize_coeffs(int in, int out, int* xmin, int* cnt, int* iw, int ksiz
   return ks;
 }
 
-/* Pillow order: horizontal pass (all rows, u8 result) then vertical pass. */
-int oracle_resize_bicubic(const uint8_t* in, int w, int h, int w2, int h2, uint8_t* out) {
+/* Pillow order (both backends): horizontal pass (all rows, u8 result) then
+ * vertical pass. */
+int oracle_resize_bicubic(const uint8_t* in, int w, int h, int w2, int h2, int backend, uint8_t* out) {
   const uint8_t* src = in;
   uint8_t* tmp = NULL;
   int cw = w;
   if (w2 != w) {
     coeffs_t c;
-    if (make_coeffs(w, w2, &c) != 0) return -1;
+    if (make_coeffs(w, w2, backend, &c) != 0) return -1;
     tmp = (uint8_t*)malloc((size_t)h * w2 * 3);
     if (!tmp) return -1;
     for (int y = 0; y < h; ++y)
       for (int o = 0; o < w2; ++o)
         for (int ch = 0; ch < 3; ++ch) {
-          int64_t ss = (int64_t)1 << (PRECISION_BITS - 1);
+          int64_t ss = (int64_t)1 << (c.prec - 1);
           for (int k = 0; k < c.cnt[o]; ++k)
             ss += (int64_t)src[((size_t)y * w + c.xmin[o] + k) * 3 + ch] * c.iw[(size_t)o * c.ksize + k];
-          tmp[((size_t)y * w2 + o) * 3 + ch] = clip8(ss);
+          tmp[((size_t)y * w2 + o) * 3 + ch] = clip8(ss, c.prec);
         }
     free_coeffs(&c);
     src = tmp;
@@ -231,14 +252,14 @@ int oracle_resize_bicubic(const uint8_t* in, int w, int h, int w2, int h2, uint8
   }
   if (h2 != h) {
     coeffs_t c;
-    if (make_coeffs(h, h2, &c) != 0) return -1;
+    if (make_coeffs(h, h2, backend, &c) != 0) return -1;
     for (int o = 0; o < h2; ++o)
       for (int x = 0; x < cw; ++x)
         for (int ch = 0; ch < 3; ++ch) {
-          int64_t ss = (int64_t)1 << (PRECISION_BITS - 1);
+          int64_t ss = (int64_t)1 << (c.prec - 1);
           for (int k = 0; k < c.cnt[o]; ++k)
             ss += (int64_t)src[((size_t)(c.xmin[o] + k) * cw + x) * 3 + ch] * c.iw[(size_t)o * c.ksize + k];
-          out[((size_t)o * cw + x) * 3 + ch] = clip8(ss);
+          out[((size_t)o * cw + x) * 3 + ch] = clip8(ss, c.prec);
         }
     free_coeffs(&c);
   } else {
@@ -249,9 +270,20 @@ int oracle_resize_bicubic(const uint8_t* in, int w, int h, int w2, int h2, uint8
 }
 
 /* ------------------------------------------------------------------ O9 -- */
-/* HF rescale: (float)((double)v * rescale_factor); normalize: (x - mean)/std in
- * float32 (transformers image_transforms.rescale / normalize). */
-float oracle_normalize(int v, int ch, const float* mean, const float* std, double rescale) {
+/* Backend 0 (PIL): HF rescale (float)((double)v * rescale_factor), then
+ * normalize (x - mean)/std in float32 (transformers image_transforms.rescale
+ * / normalize).  Backend 1 (torchvision, R21): HF fuses the two
+ * (image_processing_backends.py _fuse_mean_std_and_rescale_factor): mean' =
+ * f32(mean) * f32(1/rescale_factor), std' likewise, in float32; then
+ * tvF.normalize: (f32(v) - mean') / std' in float32. */
+float oracle_normalize(int v, int ch, const float* mean, const float* std, double rescale, int backend) {
+  if (backend == 1) {
+    float inv = (float)(1.0 / rescale);
+    float m2 = mean[ch] * inv;
+    float s2 = std[ch] * inv;
+    float d = (float)v - m2;
+    return d / s2;
+  }
   float x = (float)((double)v * rescale);
   float d = x - mean[ch];
   return d / std[ch];
@@ -261,7 +293,7 @@ float oracle_normalize(int v, int ch, const float* mean, const float* std, doubl
 /* rows (t, hb, wb, hm, wm) x cols (c, tp, ph, pw); frame index 2t+tp, padded
  * with the last frame.  `rs` holds n resized frames h2 x w2 x 3. */
 void oracle_tokens(const uint8_t* rs, int64_t n, int w2, int h2, const float* mean, const float* std,
-                   double rescale, float* tokens) {
+                   double rescale, int backend, float* tokens) {
   const int P = 14, M = 2, TP = 2;
   int64_t gt = (n + TP - 1) / TP;
   int gh = h2 / P, gw = w2 / P;
@@ -281,7 +313,7 @@ void oracle_tokens(const uint8_t* rs, int64_t n, int w2, int h2, const float* me
                     int y = (hb * M + hm) * P + ph;
                     int x = (wb * M + wm) * P + pw;
                     int v = rs[(((size_t)f * h2 + y) * w2 + x) * 3 + c];
-                    tokens[row * 1176 + col] = oracle_normalize(v, c, mean, std, rescale);
+                    tokens[row * 1176 + col] = oracle_normalize(v, c, mean, std, rescale, backend);
                     ++col;
                   }
             ++row;
@@ -329,6 +361,7 @@ typedef struct {
   uint8_t* rgb_rs;  /* n*h2*w2*3 */
   int nthreads, tid;
   int matrix;
+  int backend;
   int status;
 } job_t;
 
@@ -339,7 +372,7 @@ static void* frame_worker(void* arg) {
   for (int64_t f = j->tid; f < j->n; f += j->nthreads) {
     oracle_nv12_to_rgb_m(j->y[f], j->pitch_y[f], j->uv[f], j->pitch_uv[f], j->w, j->h, j->matrix, src);
     if (j->rgb_src) memcpy(j->rgb_src + (size_t)f * j->h * j->w * 3, src, (size_t)j->h * j->w * 3);
-    if (oracle_resize_bicubic(src, j->w, j->h, j->w2, j->h2, j->rgb_rs + (size_t)f * j->h2 * j->w2 * 3) != 0)
+    if (oracle_resize_bicubic(src, j->w, j->h, j->w2, j->h2, j->backend, j->rgb_rs + (size_t)f * j->h2 * j->w2 * 3) != 0)
       j->status = -1;
   }
   free(src);
@@ -350,7 +383,7 @@ static void* frame_worker(void* arg) {
 int oracle_preprocess(const uint8_t* const* y, const uint8_t* const* uv, const int64_t* pitch_y,
                       const int64_t* pitch_uv, int64_t n, int w, int h, int w2, int h2,
                       const float* mean, const float* std, double rescale, float* tokens,
-                      uint8_t* rgb_src, uint8_t* rgb_rs, int nthreads, int matrix) {
+                      uint8_t* rgb_src, uint8_t* rgb_rs, int nthreads, int matrix, int backend) {
   if (n <= 0 || w2 % 28 || h2 % 28) return -1;
   if (nthreads < 1) nthreads = 1;
   uint8_t* rs = rgb_rs ? rgb_rs : (uint8_t*)malloc((size_t)n * h2 * w2 * 3);
@@ -359,7 +392,7 @@ int oracle_preprocess(const uint8_t* const* y, const uint8_t* const* uv, const i
   pthread_t* th = (pthread_t*)calloc(nthreads, sizeof(pthread_t));
   int status = 0;
   for (int i = 0; i < nthreads; ++i) {
-    job_t j = {y, uv, pitch_y, pitch_uv, n, w, h, w2, h2, rgb_src, rs, nthreads, i, matrix, 0};
+    job_t j = {y, uv, pitch_y, pitch_uv, n, w, h, w2, h2, rgb_src, rs, nthreads, i, matrix, backend, 0};
     jobs[i] = j;
     if (nthreads == 1) frame_worker(&jobs[i]);
     else pthread_create(&th[i], NULL, frame_worker, &jobs[i]);
@@ -368,7 +401,7 @@ int oracle_preprocess(const uint8_t* const* y, const uint8_t* const* uv, const i
     if (nthreads > 1) pthread_join(th[i], NULL);
     if (jobs[i].status) status = -1;
   }
-  if (status == 0 && tokens) oracle_tokens(rs, n, w2, h2, mean, std, rescale, tokens);
+  if (status == 0 && tokens) oracle_tokens(rs, n, w2, h2, mean, std, rescale, backend, tokens);
   free(jobs);
   free(th);
   if (!rgb_rs) free(rs);

@@ -62,21 +62,21 @@ def lib():
         L.oracle_bt601_pixel.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p]
         L.oracle_nv12_to_rgb.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_int64,
                                          ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
-        L.oracle_resize_coeffs.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
-                                           ctypes.c_void_p, ctypes.c_int]
+        L.oracle_resize_coeffs.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
         L.oracle_resize_coeffs.restype = ctypes.c_int
         L.oracle_resize_bicubic.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                            ctypes.c_int, ctypes.c_void_p]
+                                            ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         L.oracle_resize_bicubic.restype = ctypes.c_int
         L.oracle_normalize.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
-                                       ctypes.c_double]
+                                       ctypes.c_double, ctypes.c_int]
         L.oracle_normalize.restype = ctypes.c_float
         L.oracle_tokens.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
-                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p]
+                                    ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_int, ctypes.c_void_p]
         L.oracle_preprocess.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                         ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_void_p,
-                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int]
         L.oracle_yuv_coeffs.argtypes = [ctypes.c_int, ctypes.c_void_p]
         L.oracle_codes.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
         L.oracle_yuv_pixel.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, u8p]
@@ -309,32 +309,42 @@ def to_bf16(x: np.ndarray) -> np.ndarray:
     return ((b + 0x7FFF + ((b >> 16) & 1)) >> 16).astype(np.uint16)
 
 
-def resize_bicubic(rgb: np.ndarray, w2: int, h2: int) -> np.ndarray:
-    """O8 Pillow-exact bicubic on an [H, W, 3] u8 image."""
+BACKENDS = {"pil": 0, "torchvision": 1}  # reading R21 (fc_oracle.c make_coeffs / oracle_normalize)
+
+
+def resize_bicubic(rgb: np.ndarray, w2: int, h2: int, backend: str = "pil") -> np.ndarray:
+    """O8 bicubic on an [H, W, 3] u8 image: Pillow-exact ("pil") or torch's
+    uint8 antialiased bicubic ("torchvision", R21)."""
     rgb = np.ascontiguousarray(rgb, dtype=np.uint8)
     h, w = rgb.shape[:2]
     out = np.empty((h2, w2, 3), np.uint8)
-    if lib().oracle_resize_bicubic(_ptr(rgb), w, h, w2, h2, _ptr(out)) != 0:
+    if lib().oracle_resize_bicubic(_ptr(rgb), w, h, w2, h2, BACKENDS[backend], _ptr(out)) != 0:
         raise MemoryError
     return out
 
 
-def resize_coeffs(n_in: int, n_out: int):
-    ks = lib().oracle_resize_coeffs(n_in, n_out, None, None, None, 0)
+def resize_coeffs(n_in: int, n_out: int, backend: str = "pil", with_precision: bool = False):
+    b = BACKENDS[backend]
+    ks = lib().oracle_resize_coeffs(n_in, n_out, b, None, None, None, 0, None)
     xmin = np.empty(n_out, np.int32)
     cnt = np.empty(n_out, np.int32)
     iw = np.empty(n_out * ks, np.int32)
-    lib().oracle_resize_coeffs(n_in, n_out, _ptr(xmin), _ptr(cnt), _ptr(iw), ks)
+    prec = ctypes.c_int(0)
+    lib().oracle_resize_coeffs(n_in, n_out, b, _ptr(xmin), _ptr(cnt), _ptr(iw), ks, ctypes.byref(prec))
+    if with_precision:
+        return xmin, cnt, iw.reshape(n_out, ks), prec.value
     return xmin, cnt, iw.reshape(n_out, ks)
 
 
-def normalize_value(v: int, ch: int, mean=CLIP_MEAN, std=CLIP_STD, rescale: float = 1 / 255) -> np.float32:
+def normalize_value(v: int, ch: int, mean=CLIP_MEAN, std=CLIP_STD, rescale: float = 1 / 255,
+                    backend: str = "pil") -> np.float32:
     m = np.array(mean, np.float32)
     s = np.array(std, np.float32)
-    return np.float32(lib().oracle_normalize(v, ch, _ptr(m), _ptr(s), rescale))
+    return np.float32(lib().oracle_normalize(v, ch, _ptr(m), _ptr(s), rescale, BACKENDS[backend]))
 
 
-def tokens_from_resized(rs: np.ndarray, mean=CLIP_MEAN, std=CLIP_STD, rescale: float = 1 / 255) -> np.ndarray:
+def tokens_from_resized(rs: np.ndarray, mean=CLIP_MEAN, std=CLIP_STD, rescale: float = 1 / 255,
+                        backend: str = "pil") -> np.ndarray:
     """O10-O11 on [n, H', W', 3] u8 resized frames."""
     rs = np.ascontiguousarray(rs, dtype=np.uint8)
     n, h2, w2 = rs.shape[:3]
@@ -342,7 +352,7 @@ def tokens_from_resized(rs: np.ndarray, mean=CLIP_MEAN, std=CLIP_STD, rescale: f
     out = np.empty((gt * gh * gw, COLS), np.float32)
     m = np.array(mean, np.float32)
     s = np.array(std, np.float32)
-    lib().oracle_tokens(_ptr(rs), n, w2, h2, _ptr(m), _ptr(s), rescale, _ptr(out))
+    lib().oracle_tokens(_ptr(rs), n, w2, h2, _ptr(m), _ptr(s), rescale, BACKENDS[backend], _ptr(out))
     return out
 
 
@@ -374,7 +384,7 @@ def preprocess_i420(frames, width: int, height: int, w2: int, h2: int, **kw):
 
 def preprocess(frames: list[tuple[np.ndarray, np.ndarray]], width: int, height: int, w2: int, h2: int,
                mean=CLIP_MEAN, std=CLIP_STD, rescale: float = 1 / 255, want_rgb: bool = False,
-               nthreads: int = 1, matrix: str = "bt601"):
+               nthreads: int = 1, matrix: str = "bt601", backend: str = "pil"):
     """O7..O11 end to end on the *sampled* frames (in order), each a pair
     (y [H, pitch_y] u8, uv [H/2, pitch_uv] u8).  Returns tokens
     [ceil(n/2)*gh*gw, 1176] f32 (and the RGB dumps if ``want_rgb``)."""
@@ -393,7 +403,7 @@ def preprocess(frames: list[tuple[np.ndarray, np.ndarray]], width: int, height: 
     s = np.array(std, np.float32)
     st = lib().oracle_preprocess(yp, uvp, _ptr(py), _ptr(puv), n, width, height, w2, h2, _ptr(m), _ptr(s),
                                  rescale, _ptr(tokens), _ptr(rgb_src) if want_rgb else None, _ptr(rgb_rs),
-                                 nthreads, MATRICES[matrix])
+                                 nthreads, MATRICES[matrix], BACKENDS[backend])
     if st != 0:
         raise RuntimeError("oracle_preprocess failed")
     if want_rgb:

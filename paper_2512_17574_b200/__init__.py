@@ -76,6 +76,7 @@ class ModelCfg:
     token_dtype: str = "f32"        # "f32" (HF output) | "bf16" (R16) | "u8" (codes; NEXT-1 exchange format)
     color: str = "bt601"            # "bt601" (R3) | "bt709" | "bt601_full" | "bt709_full" (R15)
     surface_format: str = "nv12"    # "nv12" (interleaved chroma) | "i420" (planar U, V)
+    backend: str = "pil"            # HF processor arithmetic (R21): "pil" | "torchvision" (CPU uint8 AA bicubic)
 
     def to_c(self):
         key = tuple(tuple(v) if isinstance(v, (list, tuple)) else v for k, v in self.__dict__.items() if k != "_c")
@@ -95,6 +96,7 @@ class ModelCfg:
         c.token_dtype = _native.TOKEN_DTYPES[self.token_dtype]
         c.color = _native.COLORS[self.color]
         c.surface_format = _native.SURFACES[self.surface_format]
+        c.backend = _native.BACKENDS[self.backend]
         c.sample_fps = self.sample_fps
         c.num_frames = self.num_frames
         c.min_frames = self.min_frames

@@ -15,7 +15,7 @@ LIB_PATH = os.path.join(HERE, f"libfc_{os.environ['FC_LIB_VARIANT']}.so" if os.e
                         else "libfc.so")
 
 FC_TOKEN_COLS = 1176
-ABI_VERSION = 5  # include/fc.h FC_ABI_VERSION this binding marshals for
+ABI_VERSION = 6  # include/fc.h FC_ABI_VERSION this binding marshals for
 STATUS = {0: "FC_OK", 1: "FC_ERR_INVALID_ARG", 2: "FC_ERR_EMPTY_SELECTION", 3: "FC_ERR_ASPECT_RATIO",
           4: "FC_ERR_UNSUPPORTED", 5: "FC_ERR_MISSING_SURFACE", 6: "FC_ERR_RANK", 7: "FC_ERR_OOM",
           8: "FC_ERR_CUDA", 9: "FC_ERR_NCCL", 10: "FC_ERR_OUT_OF_PAGES"}
@@ -23,6 +23,7 @@ SAMPLING = {"fps_stride": 0, "linspace": 1, "explicit": 2}
 TOKEN_DTYPES = {"f32": 0, "bf16": 1, "u8": 2}
 COLORS = {"bt601": 0, "bt709": 1, "bt601_full": 2, "bt709_full": 3}
 SURFACES = {"nv12": 0, "i420": 1}
+BACKENDS = {"pil": 0, "torchvision": 1}
 
 
 class FcError(RuntimeError):
@@ -51,7 +52,7 @@ class ModelCfgC(ctypes.Structure):
                 ("image_mean", ctypes.c_float * 3), ("image_std", ctypes.c_float * 3),
                 ("rescale_factor", ctypes.c_double), ("world_size", ctypes.c_int32),
                 ("encoder_rank", ctypes.c_int32), ("token_dtype", ctypes.c_int), ("color", ctypes.c_int),
-                ("surface_format", ctypes.c_int)]
+                ("surface_format", ctypes.c_int), ("backend", ctypes.c_int)]
 
 
 class PagedTokensC(ctypes.Structure):

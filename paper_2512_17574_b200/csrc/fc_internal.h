@@ -28,7 +28,8 @@ struct AxisTable {
   int ksize = 0;   // Pillow ksize
   int max_cnt = 0; // widest window actually used
   std::vector<int32_t> xmin, cnt;
-  std::vector<int32_t> iw;       // out x ksize integer weights
+  std::vector<int32_t> iw;       // out x ksize integer weights, 22-bit fixed point
+  int prec = kPrecisionBits;     // the backend's rounding precision (iw = round(w*2^prec) << (22-prec))
 };
 
 struct RankPlan {
@@ -80,6 +81,6 @@ struct fc_plan_s {
 namespace fc {
 void set_error(const std::string& msg);
 fc_status fail(fc_status s, const std::string& msg);
-fc_status build_axis(int in, int out, AxisTable* t);
-fc_status axis_cached(int in, int out, std::shared_ptr<const AxisTable>* t);
+fc_status build_axis(int in, int out, int backend, AxisTable* t);
+fc_status axis_cached(int in, int out, int backend, std::shared_ptr<const AxisTable>* t);
 }  // namespace fc

@@ -164,7 +164,7 @@ static void build_mma_tables(const fc_plan_s* P, int sw, MmaTables* m) {
 // requests share one upload, so fc_plan + fc_preprocess never touch the device
 // synchronously after the first request of a shape.
 struct TableKey {
-  int dev, sw, w, w2, h, h2;
+  int dev, sw, w, w2, h, h2, backend;
   uint32_t lut_bits[768];
   bool operator<(const TableKey& o) const { return std::memcmp(this, &o, sizeof(TableKey)) < 0; }
 };
@@ -192,6 +192,7 @@ static fc_status device_tables(fc_plan_s* P, int dev, int sw, const DeviceTables
   key.w2 = P->th->out;
   key.h = P->tv->in;
   key.h2 = P->tv->out;
+  key.backend = P->cfg.backend;
   std::memcpy(key.lut_bits, P->lut_dev.data(), sizeof(key.lut_bits));
   std::lock_guard<std::mutex> gk(g_tables_mu);
   if (std::shared_ptr<DeviceTables> hit = g_tables->get(key)) {

@@ -8,11 +8,14 @@
 //   R2 resize target = HF smart_resize, Python round-half-even
 //   R4 resize        = Pillow ImagingResample BICUBIC, 22-bit ints, H then V
 //   R5 normalise     = f32((f64(v)*rescale)) then f32 (x-mean)/std
+//   R21 backends     = PIL (R4, R5) or torchvision on CPU (torch's uint8 AA
+//                      bicubic precision rule, HF's fused normalisation)
 //   R8 partition     = contiguous GOP ranges, method b, exact DP
 #include <algorithm>
 #include <climits>
 #include <cmath>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <cstring>
 #include <limits>
@@ -40,9 +43,13 @@ static double bicubic(double x) {
   return 0.0;
 }
 
-// Pillow precompute_coeffs + normalize_coeffs_8bpc for in -> out, then the
-// byte-plane packing of DESIGN.md "Tables".
-fc_status build_axis(int in, int out, AxisTable* t) {
+// Pillow precompute_coeffs + normalize_coeffs_8bpc for in -> out (R4).  The
+// torchvision backend (R21) keeps the windows and double weights and rounds
+// them at torch's int16 precision p instead of 22 bits; the table holds
+// round(w*2^p) << (22 - p), so the kernels' 22-bit arithmetic,
+// clamp((2^21 + sum px*iw) >> 22), is exactly torch's clamp((2^(p-1) + sum
+// px*round(w*2^p)) >> p).
+fc_status build_axis(int in, int out, int backend, AxisTable* t) {
   t->in = in;
   t->out = out;
   const double scale = static_cast<double>(in) / static_cast<double>(out);
@@ -53,9 +60,11 @@ fc_status build_axis(int in, int out, AxisTable* t) {
   t->xmin.assign(out, 0);
   t->cnt.assign(out, 0);
   t->iw.assign(static_cast<size_t>(out) * ksize, 0);
-  std::vector<double> k(ksize);
+  std::vector<double> kall(static_cast<size_t>(out) * ksize, 0.0);  // normalised weights of every output
+  double wmax = 0.0;
   int max_cnt = 0;
   for (int o = 0; o < out; ++o) {
+    double* k = &kall[static_cast<size_t>(o) * ksize];
     const double center = (o + 0.5) * scale;
     double ww = 0.0;
     const double ss = 1.0 / filterscale;
@@ -71,16 +80,23 @@ fc_status build_axis(int in, int out, AxisTable* t) {
     }
     for (int x = 0; x < xmax; ++x)
       if (ww != 0.0) k[x] /= ww;
-    for (int x = 0; x < xmax; ++x) {
-      const double w = k[x];
-      t->iw[static_cast<size_t>(o) * ksize + x] =
-          static_cast<int32_t>(w < 0 ? -0.5 + w * (1 << kPrecisionBits) : 0.5 + w * (1 << kPrecisionBits));
-    }
+    for (int x = 0; x < xmax; ++x) wmax = std::max(wmax, k[x]);
     t->xmin[o] = xmin;
     t->cnt[o] = xmax;
     max_cnt = std::max(max_cnt, xmax);
   }
   t->max_cnt = max_cnt;
+  int prec = kPrecisionBits;
+  if (backend == FC_BACKEND_TORCHVISION)  // torch: the largest p < 22 keeping every weight an int16
+    for (prec = 0; prec < 22; ++prec)
+      if (static_cast<int>(0.5 + wmax * (1 << (prec + 1))) >= (1 << 15)) break;
+  t->prec = prec;
+  for (int o = 0; o < out; ++o)
+    for (int x = 0; x < t->cnt[o]; ++x) {
+      const double w = kall[static_cast<size_t>(o) * ksize + x];
+      const int32_t q = static_cast<int32_t>(w < 0 ? -0.5 + w * (1 << prec) : 0.5 + w * (1 << prec));
+      t->iw[static_cast<size_t>(o) * ksize + x] = static_cast<int32_t>(static_cast<uint32_t>(q) << (kPrecisionBits - prec));
+    }
   // the kernels split each weight into three bytes (the mma.sync kernel: two
   // unsigned low bytes and a signed high byte), so |iw| < 2^23 is required
   for (int o = 0; o < out; ++o)
@@ -94,23 +110,23 @@ fc_status build_axis(int in, int out, AxisTable* t) {
 // Axis tables depend only on (in, out): requests of one resolution share them
 // (a serving process sees few distinct shapes).  Bounded; evicted tables stay
 // alive while a plan holds them.
-fc_status axis_cached(int in, int out, std::shared_ptr<const AxisTable>* t) {
+fc_status axis_cached(int in, int out, int backend, std::shared_ptr<const AxisTable>* t) {
   static std::mutex mu;
-  static auto* cache = new std::map<std::pair<int, int>, std::shared_ptr<const AxisTable>>();  // never freed
+  static auto* cache = new std::map<std::tuple<int, int, int>, std::shared_ptr<const AxisTable>>();  // never freed
   {
     std::lock_guard<std::mutex> lk(mu);
-    auto it = cache->find({in, out});
+    auto it = cache->find({in, out, backend});
     if (it != cache->end()) {
       *t = it->second;
       return FC_OK;
     }
   }
   auto a = std::make_shared<AxisTable>();
-  fc_status st = build_axis(in, out, a.get());
+  fc_status st = build_axis(in, out, backend, a.get());
   if (st != FC_OK) return st;
   std::lock_guard<std::mutex> lk(mu);
   if (cache->size() >= 256) cache->clear();
-  (*cache)[{in, out}] = a;
+  (*cache)[{in, out, backend}] = a;
   *t = a;
   return FC_OK;
 }
@@ -414,6 +430,7 @@ void fc_model_cfg_default(fc_model_cfg* c) {
   c->rescale_factor = 1.0 / 255.0;
   c->world_size = 1;
   c->encoder_rank = 0;
+  c->backend = FC_BACKEND_PIL;
 }
 
 fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t** out) {
@@ -447,6 +464,8 @@ fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t*
     return fail(FC_ERR_UNSUPPORTED, "unknown token_dtype");
   if (c.color < FC_COLOR_BT601_LIMITED || c.color > FC_COLOR_BT709_FULL)
     return fail(FC_ERR_UNSUPPORTED, "unknown color matrix");
+  if (c.backend != FC_BACKEND_PIL && c.backend != FC_BACKEND_TORCHVISION)
+    return fail(FC_ERR_UNSUPPORTED, "unknown backend");
   if (c.surface_format != FC_SURFACE_NV12 && c.surface_format != FC_SURFACE_I420)
     return fail(FC_ERR_UNSUPPORTED, "unknown surface format");
 
@@ -476,15 +495,22 @@ fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t*
       st = fail(FC_ERR_OOM, "partition tables: host allocation failed");
     }
   }
-  if (st == FC_OK) st = axis_cached(m.width, P->w2, &P->th);
-  if (st == FC_OK) st = axis_cached(m.height, P->h2, &P->tv);
+  if (st == FC_OK) st = axis_cached(m.width, P->w2, c.backend, &P->th);
+  if (st == FC_OK) st = axis_cached(m.height, P->h2, c.backend, &P->tv);
   if (st == FC_OK) {
     P->lut.resize(3 * 256);
     for (int ch = 0; ch < 3; ++ch)
       for (int v = 0; v < 256; ++v) {
-        const float x = static_cast<float>(static_cast<double>(v) * c.rescale_factor);
-        const float d = x - c.image_mean[ch];
-        P->lut[ch * 256 + v] = d / c.image_std[ch];
+        if (c.backend == FC_BACKEND_TORCHVISION) {  // R21: HF's fused rescale + normalise, float32
+          const float inv = static_cast<float>(1.0 / c.rescale_factor);
+          const float m2 = c.image_mean[ch] * inv, s2 = c.image_std[ch] * inv;
+          const float d = static_cast<float>(v) - m2;
+          P->lut[ch * 256 + v] = d / s2;
+        } else {  // R5
+          const float x = static_cast<float>(static_cast<double>(v) * c.rescale_factor);
+          const float d = x - c.image_mean[ch];
+          P->lut[ch * 256 + v] = d / c.image_std[ch];
+        }
       }
     // the table the kernel stores from: fp32 bits, or (R16) the bf16 bits of
     // the fp32 value rounded to nearest-even, zero-extended (finite values)

@@ -60,7 +60,7 @@ struct TcTables {
 };
 
 struct TcKey {
-  int dev, w, w2, h, h2;
+  int dev, w, w2, h, h2, backend;
   uint32_t lut[768];
   bool operator<(const TcKey& o) const { return std::memcmp(this, &o, sizeof(TcKey)) < 0; }
 };
@@ -242,6 +242,7 @@ fc_status tables(fc_plan_s* P, int dev, const TcTables** out) {
   key.w2 = P->th->out;
   key.h = P->tv->in;
   key.h2 = P->tv->out;
+  key.backend = P->cfg.backend;
   std::memcpy(key.lut, P->lut_dev.data(), sizeof(key.lut));
   std::lock_guard<std::mutex> gk(g_mu);
   std::shared_ptr<TcTables> sp = g_cache->get(key);

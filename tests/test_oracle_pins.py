@@ -439,3 +439,73 @@ def test_codes_normalise_to_tokens(oracle):
     lut = np.array([[oracle.normalize_value(v, c) for v in range(256)] for c in range(3)], np.float32)
     ch = np.arange(1176) // 392
     np.testing.assert_array_equal(lut[ch[None, :], codes].view(np.uint32), tok.view(np.uint32))
+
+
+# ------------------------------------------------------ R21 torchvision backend
+# The oracle's second backend follows torch's uint8 antialiased bicubic (the
+# precision rule in fc_oracle.c make_coeffs) and HF's fused normalisation.  Pinned
+# against the libraries that define them: torch's interpolate, HF's own
+# rescale_and_normalize, and HF's Qwen2VLVideoProcessor end to end.
+@pytest.mark.parametrize("shape", [(320, 240, 392, 280), (1920, 1080, 1008, 560), (1280, 720, 1008, 560),
+                                   (3840, 2160, 1008, 560), (854, 480, 840, 476), (77, 100, 140, 56),
+                                   (1000, 33, 56, 28), (1920, 1080, 224, 224)])
+def test_resize_torchvision_bit_exact_vs_torch(oracle, shape):
+    import torch
+    W, H, W2, H2 = shape
+    rng = np.random.default_rng(W * 7 + H)
+    img = rng.integers(0, 256, (H, W, 3)).astype(np.uint8)
+    t = torch.from_numpy(img).permute(2, 0, 1).contiguous()[None]
+    ref = torch.nn.functional.interpolate(t, size=(H2, W2), mode="bicubic", antialias=True)[0].permute(1, 2, 0).numpy()
+    got = oracle.resize_bicubic(img, W2, H2, backend="torchvision")
+    np.testing.assert_array_equal(got, ref)
+
+
+def test_resize_torchvision_precision_and_difference_from_pillow(oracle):
+    """The two backends share windows and double weights and differ only in the
+    fixed-point precision: torch keeps every weight an int16 (p < 22), Pillow uses 22."""
+    for n_in, n_out in [(1920, 1008), (1080, 560), (320, 392), (100, 100)]:
+        xp, cp, wp, pp = oracle.resize_coeffs(n_in, n_out, "pil", with_precision=True)
+        xt, ct, wt, pt = oracle.resize_coeffs(n_in, n_out, "torchvision", with_precision=True)
+        assert pp == 22 and 13 <= pt < 22
+        np.testing.assert_array_equal(xp, xt)
+        np.testing.assert_array_equal(cp, ct)
+        assert wt.max() < 2 ** 15 <= 2 * int(wt.max()) + 2  # the largest precision whose weights stay int16
+        # rounded at pt bits, the Pillow weights agree to within one unit of 2^(22-pt)
+        assert np.abs(wp - (wt.astype(np.int64) << (22 - pt))).max() <= 2 ** (22 - pt)
+
+
+def test_normalize_torchvision_vs_hf(oracle):
+    """R21's table vs HF's own fused rescale + normalise (torchvision backend)."""
+    import torch
+    vp = _hf_video_processor()
+    x = torch.arange(256, dtype=torch.uint8).reshape(1, 1, 1, 256).expand(1, 3, 1, 256).contiguous()
+    ref = vp.rescale_and_normalize(x, True, 1 / 255, True, tuple(vp.image_mean), tuple(vp.image_std))
+    ref = ref.numpy().reshape(3, 256)
+    got = np.array([[oracle.normalize_value(v, c, backend="torchvision") for v in range(256)] for c in range(3)],
+                   np.float32)
+    np.testing.assert_array_equal(got.view(np.uint32), ref.astype(np.float32).view(np.uint32))
+    pil = np.array([[oracle.normalize_value(v, c) for v in range(256)] for c in range(3)], np.float32)
+    assert 0 < int((pil != got).sum()) < 768 and np.abs(pil - got).max() < 1e-6  # the two formulas differ in the last bits
+
+
+@pytest.mark.parametrize("case", [(320, 240, 8, "uniform"), (320, 240, 5, "natural"), (854, 480, 2, "edges"),
+                                  (200, 120, 3, "uniform")])
+def test_end_to_end_torchvision_vs_hf_video_processor(oracle, case):
+    """The whole torchvision-backend oracle (resize, normalise, pad, layout) vs
+    transformers' Qwen2VLVideoProcessor on the same RGB frames: bit-exact."""
+    import torch
+    W, H, n, kind = case
+    frames = []
+    for i in range(n):
+        y, uv = synth.frame_nv12(W, H, 3 * i, kind, 21)
+        frames.append(oracle.nv12_to_rgb(y, uv, W, H))
+    rgb = np.stack(frames)
+    vp = _hf_video_processor()
+    out = vp(videos=[torch.from_numpy(rgb).permute(0, 3, 1, 2).contiguous()], return_tensors="pt",
+             do_sample_frames=False)
+    ref = out["pixel_values_videos"].numpy().astype(np.float32)
+    h2, w2 = oracle.smart_resize(H, W, min_pixels=128 * 28 * 28, max_pixels=768 * 28 * 28)
+    assert tuple(out["video_grid_thw"][0].tolist()) == oracle.grid_thw(n, h2, w2)
+    rs = np.stack([oracle.resize_bicubic(f, w2, h2, backend="torchvision") for f in rgb])
+    got = oracle.tokens_from_resized(rs, backend="torchvision")
+    np.testing.assert_array_equal(got.view(np.uint32), ref.view(np.uint32))

@@ -49,7 +49,7 @@ def run_case(fc, oracle, cuda, W, H, N, gops, kind="natural", seed=7, world=1, c
     surf = fc.SurfaceTable.from_tensors(dev, N)
     h2, w2 = plan.resized
     ref_tok, ref_src, ref_rs = oracle.preprocess([host[i] for i in idx], W, H, w2, h2, want_rgb=True,
-                                                 matrix=cfg.get("color", "bt601"))
+                                                 matrix=cfg.get("color", "bt601"), backend=cfg.get("backend", "pil"))
     parts = []
     for r in range(world):
         rp = plan.rank(r)
@@ -131,14 +131,14 @@ def test_virtual_ranks_odd_explicit(fc, oracle, cuda, kernel):
 NCPU = len(os.sched_getaffinity(0))
 
 
-def _full_config(fc, oracle, cuda, name, kind="natural", clip=0, chunk=30, expect_kernel="tc"):
+def _full_config(fc, oracle, cuda, name, kind="natural", clip=0, chunk=30, expect_kernel="tc", backend="pil"):
     """A BASELINE config in the bench's launch configuration (one fc_preprocess
     launch over all frames), compared element by element on the WHOLE token
     tensor with the threaded oracle, chunk pairs at a time."""
     import torch
     wl = synth.CONFIGS[name]
     plan = fc.Plan(fc.VideoMeta(wl.width, wl.height, wl.num_frames, wl.fps, wl.gop_start),
-                   fc.ModelCfg(world_size=1, sample_fps=wl.sample_fps))
+                   fc.ModelCfg(world_size=1, sample_fps=wl.sample_fps, backend=backend))
     idx = plan.sampled_indices
     host = synth.frames_nv12(wl, idx, kind, clip=clip)
     dev = synth.to_device(host)
@@ -154,7 +154,7 @@ def _full_config(fc, oracle, cuda, name, kind="natural", clip=0, chunk=30, expec
     for t0 in range(0, gt, chunk):
         t1 = min(gt, t0 + chunk)
         fr = [idx[min(k, len(idx) - 1)] for k in range(2 * t0, 2 * t1)]
-        ref = oracle.preprocess([host[f] for f in fr], wl.width, wl.height, w2, h2, nthreads=NCPU)
+        ref = oracle.preprocess([host[f] for f in fr], wl.width, wl.height, w2, h2, nthreads=NCPU, backend=backend)
         got = tokens[t0 * rpp:t1 * rpp].cpu().numpy()
         exact_total += tol_check(got, ref, f"{name} pairs [{t0}, {t1})")
         size_total += got.size
@@ -676,3 +676,57 @@ def test_submit_equals_plan_then_preprocess(fc, oracle, cuda):
     assert e.value.name == "FC_ERR_MISSING_SURFACE"
     torch.cuda.synchronize()
     assert bool((out == -1.0).all())
+
+
+# ------------------------------------------- NEXT-4 torchvision backend (R21)
+@pytest.mark.parametrize("shape", [(320, 240, None), (1920, 1080, None), (3840, 2160, None), (854, 480, None),
+                                   (200, 120, (56, 84)), (1920, 1080, (224, 224))])
+@pytest.mark.parametrize("kind", ["uniform", "edges"])
+def test_torchvision_backend_shapes(fc, oracle, cuda, kernel, shape, kind):
+    """HF torchvision-backend arithmetic (torch uint8 AA bicubic at its int16
+    precision, fused normalisation): RGB intermediates bit-exact and tokens vs
+    the oracle, through the debug and the production instance."""
+    W, H, hw = shape
+    cfg = dict(sampling="explicit", explicit_indices=[0, 7, 19], backend="torchvision")
+    if hw:
+        cfg.update(resized_height=hw[0], resized_width=hw[1])
+    plan, exact, size = run_case(fc, oracle, cuda, W, H, 30, [0, 15], kind, seed=29, **cfg)
+    assert exact == size
+
+
+def test_torchvision_backend_virtual_ranks(fc, oracle, cuda, kernel):
+    plan, exact, size = run_case(fc, oracle, cuda, 640, 360, 300, list(range(0, 300, 30)), "natural", seed=5,
+                                 world=3, backend="torchvision")
+    assert exact == size
+
+
+def test_torchvision_backend_full_c2(fc, oracle, cuda, kernel):
+    plan, e, s = _full_config(fc, oracle, cuda, "c2", expect_kernel=kernel, backend="torchvision")
+    assert plan.grid_thw == (60, 40, 72) and e == s
+
+
+def test_torchvision_backend_full_c4(fc, oracle, cuda, kernel):
+    plan, e, s = _full_config(fc, oracle, cuda, "c4", kind="uniform", expect_kernel=kernel, backend="torchvision")
+    assert e == s
+
+
+def test_torchvision_backend_bf16_and_codes(fc, oracle, cuda):
+    """bf16 tokens and u8 codes + fc_expand_tokens take the backend's table."""
+    import torch
+    W, H = 320, 240
+    for td in ("bf16", "u8"):
+        plan = make_plan(fc, W, H, 30, [0, 15], sampling="explicit", explicit_indices=[2, 11, 20, 29],
+                         backend="torchvision", token_dtype=td)
+        idx = plan.sampled_indices
+        host = {i: synth.frame_nv12(W, H, i, "uniform", 31, synth.pitch_for(W)) for i in idx}
+        surf = fc.SurfaceTable.from_tensors(synth.to_device(host), 30)
+        h2, w2 = plan.resized
+        ref = oracle.preprocess([host[i] for i in idx], W, H, w2, h2, backend="torchvision")
+        out = fc.preprocess(plan, 0, surf)
+        torch.cuda.synchronize()
+        if td == "bf16":
+            np.testing.assert_array_equal(out.view(torch.int16).cpu().numpy().view(np.uint16), oracle.to_bf16(ref))
+        else:
+            tok = fc.expand_tokens(plan, out, out_dtype="f32")
+            torch.cuda.synchronize()
+            assert tol_check(tok.cpu().numpy(), ref, "codes expanded") == ref.size

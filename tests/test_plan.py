@@ -266,7 +266,8 @@ def test_i420_surface_validation(fc, planes, status):
     assert fc._native.STATUS[st] == status, fc.lib().fc_last_error()
 
 
-@pytest.mark.parametrize("field,value", [("token_dtype", 3), ("color", 4), ("color", -1), ("surface_format", 2)])
+@pytest.mark.parametrize("field,value", [("token_dtype", 3), ("color", 4), ("color", -1), ("surface_format", 2),
+                                         ("backend", 2), ("backend", -1)])
 def test_unknown_variant_enums_rejected(fc, field, value):
     """NEXT-4 variant enums are validated by fc_plan (S:34 structured errors)."""
     meta = fc.VideoMeta(64, 48, 100, (30, 1), [0, 50])
@@ -282,9 +283,9 @@ def test_model_cfg_struct_matches_abi(fc):
     """The ctypes mirror of fc_model_cfg has the C layout: fc_model_cfg_default
     fills the trailing fields with their documented defaults."""
     c = fc._native.ModelCfgC()
-    c.token_dtype, c.color, c.surface_format = 9, 9, 9
+    c.token_dtype, c.color, c.surface_format, c.backend = 9, 9, 9, 9
     fc.lib().fc_model_cfg_default(ctypes.byref(c))
-    assert (c.token_dtype, c.color, c.surface_format, c.world_size, c.encoder_rank) == (0, 0, 0, 1, 0)
+    assert (c.token_dtype, c.color, c.surface_format, c.world_size, c.encoder_rank, c.backend) == (0, 0, 0, 1, 0, 0)
     assert abs(c.rescale_factor - 1 / 255) < 1e-15 and c.patch_size == 14
 
 
@@ -552,3 +553,13 @@ def test_assign_requests_lpt(fc):
 def collections_count(xs):
     import collections
     return collections.Counter(xs)
+
+
+def test_backend_shares_the_plan(fc):
+    """R21: the torchvision backend plans like the PIL one (sampling, sizes,
+    rank split are shared; only the resize and normalise tables differ)."""
+    for W, H in [(1920, 1080), (320, 240), (854, 480)]:
+        a = plan_of(fc, W, H, 120, list(range(0, 120, 30)), world_size=3)
+        b = plan_of(fc, W, H, 120, list(range(0, 120, 30)), world_size=3, backend="torchvision")
+        assert a.resized == b.resized and a.grid_thw == b.grid_thw and a.sampled_indices == b.sampled_indices
+        assert [a.rank(r) for r in range(3)] == [b.rank(r) for r in range(3)]
