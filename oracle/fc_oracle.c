@@ -32,6 +32,12 @@
  *                               index encoding.
  *   oracle_preprocess       O7..O11 end to end.  Pinned: vs HF
  *                               Qwen2VLImageProcessorPil on oracle RGB.
+ *   backend = 1 (R21)       torch's uint8 antialiased bicubic (precision
+ *                               rule in make_coeffs) + HF's fused
+ *                               normalisation.  Pinned: bit-exact vs torch
+ *                               interpolate(antialias=True) on 8 shapes, HF
+ *                               rescale_and_normalize (768 values) and HF
+ *                               Qwen2VLVideoProcessor end to end.
  */
 #include <math.h>
 #include <pthread.h>

@@ -18,7 +18,9 @@ SURVEY = /root/repo/SURVEY.md; readings listed in DESIGN.md "Readings"):
   concatenated tokens, so only validity is checked, plus
   ``brute_force_min_max_pairs`` for optimality on tiny inputs.
 * ``preprocess``     -- O7..O11 via the plain C library ``liboracle.so``
-  (fc_oracle.c): BT.601, Pillow bicubic, HF normalize, Qwen2-VL patch order.
+  (fc_oracle.c): BT.601, Pillow bicubic, HF normalize, Qwen2-VL patch order;
+  ``backend="torchvision"`` (R21): torch's uint8 antialiased bicubic and HF's
+  fused normalisation, pinned against torch and Qwen2VLVideoProcessor.
 """
 from __future__ import annotations
 
