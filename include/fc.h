@@ -32,6 +32,7 @@
 #ifndef FC_H_
 #define FC_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -515,6 +516,44 @@ fc_status fc_ipc_close(void* dev_ptr);
  * Collective: every rank of the plan's world must call it.  Async on stream. */
 fc_status fc_gather(const fc_plan_t* plan, int32_t rank, void* comm, const void* shard, void* full,
                     void* stream);
+
+/* ---- NEXT-4 images: "JPEG is decoded via dedicated hardware" ----
+ * nvJPEG decodes one baseline, 3-component, 4:2:0 JPEG (JFIF YCbCr) into
+ * caller-owned device planes laid out as an FC_SURFACE_I420 surface: Y in
+ * surf->y (pitch_y), Cb in surf->uv and Cr in surf->v (pitch_uv).  Feed the
+ * surface to fc_preprocess with cfg.surface_format = FC_SURFACE_I420 and
+ * cfg.color = FC_COLOR_BT601_FULL (JFIF is full-range BT.601); a single image
+ * is a one-frame request (num_frames 1, explicit index 0), padded to the
+ * temporal patch like an odd frame count, grid (1, H'/14, W'/14).
+ * The decoder is library code: the hardware JPEG engines (nvJPEG's hardware
+ * backend) when the GPU and driver offer them, else nvJPEG's CUDA backend.
+ * A decoder serialises its decodes (one nvJPEG state); use one per thread
+ * for concurrency. */
+typedef struct fc_jpeg_decoder_s fc_jpeg_decoder_t;
+typedef enum {
+  FC_JPEG_BACKEND_AUTO = 0,     /* hardware if available, else CUDA */
+  FC_JPEG_BACKEND_HARDWARE = 1, /* the JPEG engines only (error if absent) */
+  FC_JPEG_BACKEND_CUDA = 2      /* nvJPEG's CUDA decoder */
+} fc_jpeg_backend;
+typedef enum { FC_JPEG_420 = 0, FC_JPEG_OTHER = 1 } fc_jpeg_subsampling;
+/* backend: fc_jpeg_backend.  Errors: FC_ERR_INVALID_ARG (NULL out, unknown
+ * backend), FC_ERR_UNSUPPORTED / FC_ERR_CUDA (backend unavailable). */
+fc_status fc_jpeg_decoder_create(int32_t backend, fc_jpeg_decoder_t** out);
+void fc_jpeg_decoder_destroy(fc_jpeg_decoder_t* dec);
+/* The backend a decoder opened (FC_JPEG_BACKEND_HARDWARE or _CUDA), -1 for NULL. */
+int32_t fc_jpeg_decoder_backend(const fc_jpeg_decoder_t* dec);
+/* Header parse on the host: luma size and whether the image is 3-component
+ * 4:2:0 (FC_JPEG_420).  data: host pointer to the whole JPEG file, len bytes.
+ * Errors: FC_ERR_INVALID_ARG (NULL, not a JPEG), FC_ERR_UNSUPPORTED. */
+fc_status fc_jpeg_info(fc_jpeg_decoder_t* dec, const uint8_t* data, size_t len, int32_t* width, int32_t* height,
+                       int32_t* subsampling);
+/* Decode into `surf` (device planes, capacity >= height rows x pitch; the
+ * caller keeps them alive) on `stream` (cudaStream_t; NULL = legacy default).
+ * Requires a 4:2:0 image of even width and height (FC_ERR_UNSUPPORTED
+ * otherwise) and pitch_y >= width, pitch_uv >= width/2 (FC_ERR_INVALID_ARG).
+ * data is a host pointer; nothing is enqueued on error. */
+fc_status fc_jpeg_decode_i420(fc_jpeg_decoder_t* dec, const uint8_t* data, size_t len, const fc_nv12_surface* surf,
+                              void* stream);
 
 const char* fc_status_string(fc_status s);
 const char* fc_last_error(void);

@@ -22,7 +22,8 @@ from ._native import FcError, FC_TOKEN_COLS, check, lib
 
 __all__ = ["VideoMeta", "ModelCfg", "Plan", "SurfaceTable", "preprocess", "preprocess_debug", "preprocess_batch",
            "expand_tokens", "preprocess_paged", "PageTable", "RaggedIndex", "paged_copy",
-           "NcclComm", "gather", "exchange_schedule", "last_kernel", "assign_requests", "submit", "ipc_export", "PeerBuffer", "FcError", "FC_TOKEN_COLS", "lib"]
+           "NcclComm", "gather", "exchange_schedule", "last_kernel", "assign_requests", "submit", "ipc_export", "PeerBuffer", "FcError", "FC_TOKEN_COLS", "lib",
+           "JpegDecoder", "image_cfg", "preprocess_jpeg"]
 
 
 @dataclass
@@ -542,3 +543,77 @@ def gather(plan: Plan, rank: int, comm: NcclComm | None, shard, full=None, strea
                           ctypes.c_void_p(full.data_ptr()) if full is not None else None,
                           _stream_ptr(stream)), "fc_gather")
     return full if rank == enc else None
+
+
+# ---------------------------------------------------------------- JPEG images
+class JpegDecoder:
+    """NEXT-4 image path ("JPEG is decoded via dedicated hardware"):
+    nvJPEG (hardware engines when offered, else its CUDA decoder) decodes a
+    4:2:0 JPEG into device I420 planes that the fused kernel consumes like a
+    decoded video frame (fc.h fc_jpeg_*)."""
+
+    def __init__(self, backend: str = "auto"):
+        h = ctypes.c_void_p()
+        check(lib().fc_jpeg_decoder_create(_native.JPEG_BACKENDS[backend], ctypes.byref(h)), "fc_jpeg_decoder_create")
+        self.handle = h
+        # why the hardware backend was not taken (auto mode), from the library's last error
+        self.hardware_error = (lib().fc_last_error().decode(errors="replace")
+                               if backend == "auto" and lib().fc_jpeg_decoder_backend(h) != 1 else "")
+
+    @property
+    def backend(self) -> str:
+        return {1: "hardware", 2: "cuda"}[lib().fc_jpeg_decoder_backend(self.handle)]
+
+    def info(self, data: bytes) -> tuple[int, int, bool]:
+        w, h, css = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        check(lib().fc_jpeg_info(self.handle, data, len(data), ctypes.byref(w), ctypes.byref(h), ctypes.byref(css)),
+              "fc_jpeg_info")
+        return w.value, h.value, css.value == 0
+
+    def decode(self, data: bytes, stream=None):
+        """-> (y [H, pitch], u [H/2, pitch_c], v [H/2, pitch_c]) uint8 device tensors
+        (pitches rounded up to 256 bytes, NVDEC-like)."""
+        import torch
+        w, h, _ = self.info(data)
+        py, pc = (w + 255) // 256 * 256, (w // 2 + 255) // 256 * 256
+        y = torch.empty((h, py), dtype=torch.uint8, device="cuda")
+        u = torch.empty((h // 2, pc), dtype=torch.uint8, device="cuda")
+        v = torch.empty((h // 2, pc), dtype=torch.uint8, device="cuda")
+        s = _native.Nv12SurfaceC(y.data_ptr(), u.data_ptr(), py, pc, v.data_ptr())
+        check(lib().fc_jpeg_decode_i420(self.handle, data, len(data), ctypes.byref(s), _stream_ptr(stream)),
+              "fc_jpeg_decode_i420")
+        return y, u, v
+
+    def close(self) -> None:
+        if self.handle:
+            lib().fc_jpeg_decoder_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def image_cfg(**kw) -> ModelCfg:
+    """Preprocessing of a JPEG image through the video path: full-range BT.601
+    (JFIF), I420 surfaces, one explicitly sampled frame (padded to the temporal
+    patch); other fields as given (e.g. the image processor's pixel budget)."""
+    kw.setdefault("color", "bt601_full")
+    kw.setdefault("surface_format", "i420")
+    kw.setdefault("sampling", "explicit")
+    kw.setdefault("explicit_indices", [0])
+    return ModelCfg(**kw)
+
+
+def preprocess_jpeg(decoder: JpegDecoder, data: bytes, cfg: ModelCfg | None = None, stream=None):
+    """One JPEG image -> (tokens [H'/14 * W'/14, 1176], grid_thw (1, H'/14, W'/14), plan)."""
+    cfg = cfg or image_cfg()
+    w, h, _ = decoder.info(data)
+    planes = decoder.decode(data, stream)
+    plan = Plan(VideoMeta(w, h, 1, (1, 1), [0]), cfg)
+    surf = SurfaceTable(1)
+    surf.set(0, *planes)
+    tokens = preprocess(plan, 0, surf, stream=stream)
+    return tokens, plan.grid_thw, plan, planes

@@ -107,7 +107,10 @@ EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_g
            "fc_preprocess_colsplit", "fc_scatter_columns", "fc_exchange_schedule", "fc_last_kernel",
            "fc_assign_requests", "fc_submit", "fc_ipc_export", "fc_ipc_export_range", "fc_ipc_import",
            "fc_ipc_close", "fc_pages_create", "fc_pages_destroy", "fc_pages_alloc", "fc_pages_index",
-           "fc_pages_free_consumed", "fc_pages_release", "fc_pages_stats", "fc_paged_copy"]
+           "fc_pages_free_consumed", "fc_pages_release", "fc_pages_stats", "fc_paged_copy",
+           "fc_jpeg_decoder_create", "fc_jpeg_decoder_destroy", "fc_jpeg_decoder_backend", "fc_jpeg_info",
+           "fc_jpeg_decode_i420"]
+JPEG_BACKENDS = {"auto": 0, "hardware": 1, "cuda": 2}
 
 _lib = None
 
@@ -172,10 +175,18 @@ def lib() -> ctypes.CDLL:
     L.fc_paged_copy.argtypes = [ctypes.c_int, ctypes.POINTER(RaggedIndexC), vp, i64, i32, i64, vp, vp]
     L.fc_last_kernel.argtypes = []
     L.fc_last_kernel.restype = ctypes.c_int32
+    L.fc_jpeg_decoder_create.argtypes = [i32, ctypes.POINTER(vp)]
+    L.fc_jpeg_decoder_destroy.argtypes = [vp]
+    L.fc_jpeg_decoder_destroy.restype = None
+    L.fc_jpeg_decoder_backend.argtypes = [vp]
+    L.fc_jpeg_decoder_backend.restype = ctypes.c_int32
+    L.fc_jpeg_info.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t, pi32, pi32, pi32]
+    L.fc_jpeg_decode_i420.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(Nv12SurfaceC), vp]
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("fc_model_cfg_default", "fc_plan_destroy", "fc_pages_destroy", "fc_status_string", "fc_last_error",
-                        "fc_abi_version", "fc_kernel_launches", "fc_last_kernel"):
+                        "fc_abi_version", "fc_kernel_launches", "fc_last_kernel", "fc_jpeg_decoder_destroy",
+                        "fc_jpeg_decoder_backend"):
             fn.restype = ctypes.c_int
     _lib = L
     return L

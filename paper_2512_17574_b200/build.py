@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libfc.so")
 SOURCES = ["fc_plan.cpp", "fc_kernels.cu", "fc_inst_ks1.cu", "fc_inst_ks2.cu", "fc_inst_ks3.cu", "fc_inst_ks4.cu",
-           "fc_expand.cu", "fc_gather.cpp", "fc_tc.cu", "fc_pages.cu"]
+           "fc_expand.cu", "fc_gather.cpp", "fc_tc.cu", "fc_pages.cu", "fc_jpeg.cpp"]
 HEADERS = ["fc_internal.h", "fc_device.cuh", "fc_fused.cuh", "fc_tc.cuh", "fc_launch.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -63,8 +63,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if bad:
         raise subprocess.CalledProcessError(1, bad[0])
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", libdir, "-l:libnccl.so.2",
-           "-Xlinker", "-rpath," + libdir, "-cudart", "static"]
+    cuda_lib = os.path.join(os.path.dirname(os.path.dirname(NVCC)), "lib64")  # libnvjpeg (JPEG images, NEXT-4)
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-L", libdir, "-l:libnccl.so.2", "-L", cuda_lib, "-lnvjpeg",
+           "-Xlinker", "-rpath," + libdir, "-Xlinker", "-rpath," + cuda_lib, "-cudart", "static"]
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB

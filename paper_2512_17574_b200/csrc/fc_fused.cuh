@@ -34,7 +34,7 @@ namespace fc {
 #define FC_PREF 1  // per-band table reads issued a band ahead (A/B knob)
 #endif
 #ifndef FC_HG1
-#define FC_HG1 3  // H-pass planes interleaved per MMA group, narrow windows (A/B knob)
+#define FC_HG1 2  // H-pass planes interleaved per MMA group, narrow windows (A/B: 2 beats 3 by 1% on c2, 6 spills)
 #endif
 constexpr int kChunkRows = 16;             // source rows per chunk
 constexpr int kTileN = 8;                  // outputs per H-pass MMA tile (N of m16n8k32)
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
         // refill the stage just converted with chunk k + nstages; the issuing
         // warp owns no H tile, so this runs beside the H pass, off the critical path
         if (issuer && k + NS < r.klast) issue_chunk<I420>(p, r.pair, SX0, k + NS, raw + buf * 2 * RAWF, &full[buf]);
-        // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of 3 for ILP
+        // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of HG for ILP
         if (hact) {
           const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + 2 * (hp & 1);  // bytes of rows 2hp, 2hp+1
           constexpr int HG = KSH == 1 ? FC_HG1 : 2;  // planes interleaved per group (ILP vs registers)

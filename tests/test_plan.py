@@ -563,3 +563,14 @@ def test_backend_shares_the_plan(fc):
         b = plan_of(fc, W, H, 120, list(range(0, 120, 30)), world_size=3, backend="torchvision")
         assert a.resized == b.resized and a.grid_thw == b.grid_thw and a.sampled_indices == b.sampled_indices
         assert [a.rank(r) for r in range(3)] == [b.rank(r) for r in range(3)]
+
+
+def test_jpeg_decoder_argument_errors(fc):
+    """fc_jpeg_* argument checks happen before any nvJPEG / device call."""
+    h = ctypes.c_void_p()
+    assert fc._native.STATUS[fc.lib().fc_jpeg_decoder_create(7, ctypes.byref(h))] == "FC_ERR_INVALID_ARG"
+    assert fc._native.STATUS[fc.lib().fc_jpeg_decoder_create(0, None)] == "FC_ERR_INVALID_ARG"
+    w = ctypes.c_int32()
+    assert fc._native.STATUS[fc.lib().fc_jpeg_info(None, b"x", 1, ctypes.byref(w), ctypes.byref(w), None)] == \
+        "FC_ERR_INVALID_ARG"
+    assert fc.lib().fc_jpeg_decoder_backend(None) == -1
