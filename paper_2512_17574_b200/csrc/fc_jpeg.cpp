@@ -29,7 +29,8 @@ namespace {
 fc_status nvj_fail(nvjpegStatus_t s, const char* what) {
   const fc_status st = s == NVJPEG_STATUS_BAD_JPEG || s == NVJPEG_STATUS_INCOMPLETE_BITSTREAM
                            ? FC_ERR_INVALID_ARG
-                       : s == NVJPEG_STATUS_JPEG_NOT_SUPPORTED || s == NVJPEG_STATUS_IMPLEMENTATION_NOT_SUPPORTED
+                       : s == NVJPEG_STATUS_JPEG_NOT_SUPPORTED || s == NVJPEG_STATUS_IMPLEMENTATION_NOT_SUPPORTED ||
+                                 s == NVJPEG_STATUS_ARCH_MISMATCH  // e.g. no hardware backend for this GPU
                            ? FC_ERR_UNSUPPORTED
                        : s == NVJPEG_STATUS_ALLOCATOR_FAILURE ? FC_ERR_OOM
                                                               : FC_ERR_CUDA;
