@@ -134,7 +134,7 @@ static void build_mma_tables(const fc_plan_s* P, int sw, MmaTables* m) {
     int outs[8];
     h_outs(tt, outs);
     const int first = std::min(tt / htiles * sw + 8 * (tt % htiles), th.out - 1);
-    m->hxs[tt] = th.xmin[first] & ~7;  // 8-byte aligned LDS.64 A loads
+    m->hxs[tt] = th.xmin[first] & ~7;  // 8 columns = 16 bytes of a row-pair line: aligned LDS.128 A loads
     ksh = std::max(ksh, group_ks(th, outs, m->hxs[tt]));
   }
   for (int grp = 0; grp < gh2 * 4; ++grp) {
