@@ -53,6 +53,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const void* tmap, int x, 
       : "memory");
 }
 
+// Programmatic dependent launch (the launcher sets the attribute): the next
+// launch on the stream may start its prologue while this grid drains; its
+// threads wait here for every prerequisite grid to complete (and its memory
+// to be visible) before touching global data.  No-ops without the attribute.
+__device__ __forceinline__ void grid_dependency_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- integer math
 // a: two signed 16-bit coefficients; b: pixel bytes 0,1 (lo) or 2,3 (hi)
 __device__ __forceinline__ int dp2a_lo(uint32_t a, uint32_t b, int c) {

@@ -217,6 +217,12 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
   for (int i = tid; i < 6 * CH * SWP / 16; i += kThreads)
     reinterpret_cast<uint4*>(rgb)[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
+  // (PDL) the prologue above only reads the plan's constant tables; the NV12
+  // surfaces, launch descriptor and token buffer may belong to the previous
+  // launch on the stream, so everything below waits for it; the next launch
+  // may begin its own prologue as soon as this one's CTAs start retiring
+  grid_launch_dependents();
+  grid_dependency_wait();
 
   const int total = p.npairs * p.nstrips * p.gh2;
   int i0 = static_cast<int>((static_cast<long long>(blockIdx.x) * total) / gridDim.x);

@@ -768,8 +768,28 @@ static fc_status launch_jobs(fc_plan_s* P, const std::vector<Job>& jobs, void* s
     cudaMemsetAsync(cta_t, 0, 3 * sizeof(unsigned long long) * grid, s);
     prm.cta_t = cta_t;
   }
-  fn<<<grid, kThreads, g.smem, s>>>(prm);
-  e = cudaGetLastError();
+  {
+    // programmatic dependent launch: this launch's prologue (shared-memory
+    // tables, barrier init) overlaps the previous launch's tail on the stream;
+    // the kernel waits (griddepcontrol.wait) before any global access.
+    // FC_PDL=0 turns it off (A/B runs).
+    static const bool pdl = [] {
+      const char* v = std::getenv("FC_PDL");
+      return v ? std::atoi(v) != 0 : true;
+    }();
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kThreads);
+    lc.dynamicSmemBytes = g.smem;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    e = cudaLaunchKernelEx(&lc, fn, prm);
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (cta_t) {  // experiment: CTA lifetime distribution (start/end, ns from the first start)
     prm.cta_t = nullptr;
     std::vector<unsigned long long> t(3 * grid);
