@@ -30,6 +30,12 @@
 
 namespace fc {
 
+#ifndef FC_HG2
+#define FC_HG2 2  // the same for wide windows (KSH > 1)
+#endif
+#ifndef FC_LB_WIDE
+#define FC_LB_WIDE 3  // min CTAs/SM the wide-window instances are compiled for (register cap; A/B knob)
+#endif
 #ifndef FC_PREF
 #define FC_PREF 1  // per-band table reads issued a band ahead (A/B knob)
 #endif
@@ -181,7 +187,7 @@ __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, 
 template <int KSH, int KSV, bool DBG, int TOK, bool PAGED = false, bool I420 = false, bool COLS = false>
 // Narrow-window instances (KSH = KSV = 1: c2, c3, c5) fit 64 registers without
 // spills and run 4 CTAs/SM (with 2 TMA stages); wider windows keep 80 / 3.
-__global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
+__global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : FC_LB_WIDE)
     fc_fused_kernel(const __grid_constant__ Params p) {
   constexpr int SW = kStrip;
   constexpr int CH = kChunkRows;
@@ -399,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : 3)
         // ---- a6: horizontal pass (MMA) -> ring bytes; planes in groups of HG for ILP
         if (hact) {
           const uint32_t dA = ring_s + (hwA * RS + ho) * 4 + 2 * (hp & 1);  // bytes of rows 2hp, 2hp+1
-          constexpr int HG = KSH == 1 ? FC_HG1 : 2;  // planes interleaved per group (ILP vs registers)
+          constexpr int HG = KSH == 1 ? FC_HG1 : FC_HG2;  // planes interleaved per group (ILP vs registers)
 #pragma unroll
           for (int fg = 0; fg < 6; fg += HG) {
             uint32_t a[HG][KSH][4];
