@@ -173,11 +173,13 @@ __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, 
 // 16-row chunk:
 //   lane 0 of warp 7 refills the raw stage just converted with the chunk
 //       nstages ahead (2-D TMA, mbarrier expect_tx) beside the H pass;
-//   all warps: a5 colour (dp2a) -> RGB planes; barrier;
+//   all warps: a5 colour (dp2a), items of 8 px x 2 rows -> row-pair
+//       interleaved RGB planes; barrier;
 //   warps 0..6: a6 horizontal pass, warp w owns output tile w (8 columns) of
 //       the strip; three byte-plane MMAs per 16 rows x 8 outputs (MMA rows
-//       g / g+8 = source rows 2g / 2g+1) -> saturating pack -> u8 ring (4
-//       source rows per 32-bit word, one 16-bit store per column pair); barrier.
+//       g / g+8 = the two rows of row pair (g>>1)|(g&1)<<2, A fragment = one
+//       LDS.128) -> saturating pack -> u8 ring (4 source rows per 32-bit word,
+//       one 16-bit store per column pair); barrier.
 // Per band: a7 vertical pass, warp w owns 8-row group (w&3) and the three
 // channels of frame w>>2; one MMA tile per 14-column patch, then a8 table +
 // a9 patch-order stores; barrier.
