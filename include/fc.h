@@ -555,6 +555,39 @@ fc_status fc_jpeg_info(fc_jpeg_decoder_t* dec, const uint8_t* data, size_t len, 
 fc_status fc_jpeg_decode_i420(fc_jpeg_decoder_t* dec, const uint8_t* data, size_t len, const fc_nv12_surface* surf,
                               void* stream);
 
+/* ---- NEXT-3 (partial): stall-free GOP_s dispatch (Alg. 2) ----
+ * A request's decode work is split into GOP_s segments (runs of GOPs a decode
+ * unit decodes from their keyframe).  Worker w (of num_workers
+ * threads, Alg. 2 l.6) runs its segments {s : worker_of[s] == w} in increasing
+ * s by calling fn(ctx, s, w) on its own thread; at most max_in_flight
+ * segments run at once (N decode units, l.10).  A worker that finishes a
+ * segment and has more keeps its unit (l.12-13: "the remaining GOP_s within the
+ * same worker is prioritized"); a worker that runs dry releases its
+ * unit and wakes a waiting worker.  fn returns 0 on success; a nonzero return
+ * stops new dispatches and the call returns FC_ERR_CUDA after the running
+ * segments end.  trace (host, optional, 3 * num_segments int64): per
+ * completion in order, (segment, worker, fn's return).  Blocks until every
+ * segment has run.  Errors: FC_ERR_INVALID_ARG (negative counts, worker out
+ * of range, NULL fn), FC_ERR_OOM. */
+typedef int32_t (*fc_segment_fn)(void* ctx, int64_t segment, int32_t worker);
+fc_status fc_dispatch_segments(const int32_t* worker_of, int64_t num_segments, int32_t num_workers,
+                               int32_t max_in_flight, fc_segment_fn fn, void* ctx, int64_t* trace);
+
+/* Decode the target frames of a Motion-JPEG request -- every frame an
+ * independent 4:2:0 JPEG, i.e. a one-frame GOP, so only targets are decoded
+ * -- into I420 surfaces through fc_dispatch_segments: the n targets
+ * (data[i], lengths[i]: host pointers, in order) are cut into num_segments
+ * contiguous GOP_s segments dealt round-robin to num_workers threads, each with
+ * its own nvJPEG decoder (backend: fc_jpeg_backend) and CUDA stream; at most
+ * max_in_flight segments decode at once.  surfaces[i] receives target i
+ * (device planes as in fc_jpeg_decode_i420).  Returns after every decode has
+ * completed on the device, so any stream may consume the surfaces.  trace as
+ * in fc_dispatch_segments.  Errors: as fc_jpeg_decode_i420 (the first
+ * failure), FC_ERR_INVALID_ARG for bad counts. */
+fc_status fc_decode_mjpeg(const uint8_t* const* data, const size_t* lengths, int64_t n,
+                          const fc_nv12_surface* surfaces, int32_t num_segments, int32_t num_workers,
+                          int32_t max_in_flight, int32_t backend, int64_t* trace);
+
 const char* fc_status_string(fc_status s);
 const char* fc_last_error(void);
 int32_t fc_abi_version(void);

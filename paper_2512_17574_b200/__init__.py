@@ -23,7 +23,7 @@ from ._native import FcError, FC_TOKEN_COLS, check, lib
 __all__ = ["VideoMeta", "ModelCfg", "Plan", "SurfaceTable", "preprocess", "preprocess_debug", "preprocess_batch",
            "expand_tokens", "preprocess_paged", "PageTable", "RaggedIndex", "paged_copy",
            "NcclComm", "gather", "exchange_schedule", "last_kernel", "assign_requests", "submit", "ipc_export", "PeerBuffer", "FcError", "FC_TOKEN_COLS", "lib",
-           "JpegDecoder", "image_cfg", "preprocess_jpeg"]
+           "JpegDecoder", "image_cfg", "preprocess_jpeg", "dispatch_segments", "decode_mjpeg"]
 
 
 @dataclass
@@ -617,3 +617,51 @@ def preprocess_jpeg(decoder: JpegDecoder, data: bytes, cfg: ModelCfg | None = No
     surf.set(0, *planes)
     tokens = preprocess(plan, 0, surf, stream=stream)
     return tokens, plan.grid_thw, plan, planes
+
+
+# ------------------------------------------------- stall-free GOP_s dispatch
+def dispatch_segments(worker_of: Sequence[int], num_workers: int, max_in_flight: int, fn) -> list[tuple[int, int, int]]:
+    """fc_dispatch_segments (Alg. 2): run fn(segment, worker) -> int (0 = ok) on
+    num_workers threads, at most max_in_flight at once, a worker keeping its
+    unit for its next segment.  Returns the completion trace
+    [(segment, worker, status)].  (fn runs on library threads; a Python fn
+    takes the GIL per call.)"""
+    n = len(worker_of)
+    wo = (ctypes.c_int32 * max(n, 1))(*worker_of)
+    trace = (ctypes.c_int64 * max(3 * n, 1))()
+
+    def cb(_ctx, seg, w):
+        try:
+            return int(fn(int(seg), int(w)))
+        except Exception:  # a raising callback is a failed segment
+            return 1
+    cfn = _native.SEGMENT_FN(cb)
+    check(lib().fc_dispatch_segments(wo, n, num_workers, max_in_flight, cfn, None, trace), "fc_dispatch_segments")
+    return [(trace[3 * i], trace[3 * i + 1], trace[3 * i + 2]) for i in range(n)]
+
+
+def decode_mjpeg(frames: Sequence[bytes], segments: int = 4, workers: int = 2, max_in_flight: int = 2,
+                 backend: str = "auto"):
+    """fc_decode_mjpeg: the target frames of a Motion-JPEG request (each an
+    independent 4:2:0 JPEG) -> a list of (y, u, v) device tensors, decoded by
+    `workers` threads over GOP_s segments with at most `max_in_flight` at once
+    (Alg. 2).  Returns (planes, trace)."""
+    import torch
+    n = len(frames)
+    info = JpegDecoder(backend)
+    planes, arr = [], (_native.Nv12SurfaceC * max(n, 1))()
+    for i, f in enumerate(frames):
+        w, h, _ = info.info(f)
+        py, pc = (w + 255) // 256 * 256, (w // 2 + 255) // 256 * 256
+        y = torch.empty((h, py), dtype=torch.uint8, device="cuda")
+        u = torch.empty((h // 2, pc), dtype=torch.uint8, device="cuda")
+        v = torch.empty((h // 2, pc), dtype=torch.uint8, device="cuda")
+        arr[i] = _native.Nv12SurfaceC(y.data_ptr(), u.data_ptr(), py, pc, v.data_ptr())
+        planes.append((y, u, v))
+    info.close()
+    data = (ctypes.c_char_p * max(n, 1))(*frames)
+    lens = (ctypes.c_size_t * max(n, 1))(*[len(f) for f in frames])
+    trace = (ctypes.c_int64 * max(3 * min(segments, n), 1))()
+    check(lib().fc_decode_mjpeg(data, lens, n, arr, segments, workers, max_in_flight,
+                                _native.JPEG_BACKENDS[backend], trace), "fc_decode_mjpeg")
+    return planes, [(trace[3 * i], trace[3 * i + 1], trace[3 * i + 2]) for i in range(min(segments, n))]

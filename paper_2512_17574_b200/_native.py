@@ -109,7 +109,8 @@ EXPORTS = ["fc_model_cfg_default", "fc_plan", "fc_plan_destroy", "fc_plan_info_g
            "fc_ipc_close", "fc_pages_create", "fc_pages_destroy", "fc_pages_alloc", "fc_pages_index",
            "fc_pages_free_consumed", "fc_pages_release", "fc_pages_stats", "fc_paged_copy",
            "fc_jpeg_decoder_create", "fc_jpeg_decoder_destroy", "fc_jpeg_decoder_backend", "fc_jpeg_info",
-           "fc_jpeg_decode_i420"]
+           "fc_jpeg_decode_i420", "fc_dispatch_segments", "fc_decode_mjpeg"]
+SEGMENT_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32)
 JPEG_BACKENDS = {"auto": 0, "hardware": 1, "cuda": 2}
 
 _lib = None
@@ -182,6 +183,10 @@ def lib() -> ctypes.CDLL:
     L.fc_jpeg_decoder_backend.restype = ctypes.c_int32
     L.fc_jpeg_info.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t, pi32, pi32, pi32]
     L.fc_jpeg_decode_i420.argtypes = [vp, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(Nv12SurfaceC), vp]
+    L.fc_dispatch_segments.argtypes = [ctypes.POINTER(ctypes.c_int32), i64, i32, i32, SEGMENT_FN, vp,
+                                       ctypes.POINTER(ctypes.c_int64)]
+    L.fc_decode_mjpeg.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_size_t), i64,
+                                  ctypes.POINTER(Nv12SurfaceC), i32, i32, i32, i32, ctypes.POINTER(ctypes.c_int64)]
     for name in EXPORTS:
         fn = getattr(L, name)
         if name not in ("fc_model_cfg_default", "fc_plan_destroy", "fc_pages_destroy", "fc_status_string", "fc_last_error",

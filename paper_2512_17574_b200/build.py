@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libfc.so")
 SOURCES = ["fc_plan.cpp", "fc_kernels.cu", "fc_inst_ks1.cu", "fc_inst_ks2.cu", "fc_inst_ks3.cu", "fc_inst_ks4.cu",
-           "fc_expand.cu", "fc_gather.cpp", "fc_tc.cu", "fc_pages.cu", "fc_jpeg.cpp"]
+           "fc_expand.cu", "fc_gather.cpp", "fc_tc.cu", "fc_pages.cu", "fc_jpeg.cpp", "fc_sched.cpp"]
 HEADERS = ["fc_internal.h", "fc_device.cuh", "fc_fused.cuh", "fc_tc.cuh", "fc_launch.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -8,10 +8,12 @@
 // offer it, else nvJPEG's CUDA backend); parity starts at its output planes.
 #include <nvjpeg.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <new>
 #include <string>
+#include <vector>
 
 #include "fc_internal.h"
 
@@ -145,6 +147,79 @@ fc_status fc_jpeg_decode_i420(fc_jpeg_decoder_t* d, const uint8_t* data, size_t 
   }
   if (r != NVJPEG_STATUS_SUCCESS) return nvj_fail(r, d->batched ? "nvjpegDecodeBatched" : "nvjpegDecode");
   return FC_OK;
+}
+
+namespace {
+struct MjpegJob {
+  const uint8_t* const* data;
+  const size_t* lengths;
+  const fc_nv12_surface* surfaces;
+  int64_t n;
+  int32_t segments;
+  std::vector<fc_jpeg_decoder_t*> dec;
+  std::vector<cudaStream_t> streams;
+  std::mutex mu;
+  fc_status first = FC_OK;
+  std::string first_msg;
+};
+
+// One GOP_s segment on worker w's decoder and stream: the targets
+// [s*n/S, (s+1)*n/S), then a wait for the stream (the unit is busy until then).
+int32_t mjpeg_segment(void* ctx, int64_t s, int32_t w) {
+  auto* j = static_cast<MjpegJob*>(ctx);
+  const int64_t b = s * j->n / j->segments, e = (s + 1) * j->n / j->segments;
+  fc_status st = FC_OK;
+  for (int64_t i = b; i < e && st == FC_OK; ++i)
+    st = fc_jpeg_decode_i420(j->dec[w], j->data[i], j->lengths[i], &j->surfaces[i], j->streams[w]);
+  if (st == FC_OK && cudaStreamSynchronize(j->streams[w]) != cudaSuccess) st = fail(FC_ERR_CUDA, "decode stream");
+  if (st != FC_OK) {
+    std::lock_guard<std::mutex> lk(j->mu);
+    if (j->first == FC_OK) {
+      j->first = st;
+      j->first_msg = fc_last_error();
+    }
+    return static_cast<int32_t>(st);
+  }
+  return 0;
+}
+}  // namespace
+
+fc_status fc_decode_mjpeg(const uint8_t* const* data, const size_t* lengths, int64_t n,
+                          const fc_nv12_surface* surfaces, int32_t num_segments, int32_t num_workers,
+                          int32_t max_in_flight, int32_t backend, int64_t* trace) {
+  if (n < 0 || (n > 0 && (!data || !lengths || !surfaces)) || num_segments < 1 || num_workers < 1 ||
+      max_in_flight < 1)
+    return fail(FC_ERR_INVALID_ARG, "bad MJPEG decode arguments");
+  if (n == 0) return FC_OK;
+  MjpegJob j;
+  j.data = data;
+  j.lengths = lengths;
+  j.surfaces = surfaces;
+  j.n = n;
+  j.segments = static_cast<int32_t>(std::min<int64_t>(num_segments, n));
+  const int32_t workers = std::min(num_workers, j.segments);
+  fc_status st = FC_OK;
+  for (int w = 0; w < workers && st == FC_OK; ++w) {
+    fc_jpeg_decoder_t* d = nullptr;
+    st = fc_jpeg_decoder_create(backend, &d);
+    if (st != FC_OK) break;
+    j.dec.push_back(d);
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+      st = fail(FC_ERR_CUDA, "decode stream");
+      break;
+    }
+    j.streams.push_back(s);
+  }
+  if (st == FC_OK) {
+    std::vector<int32_t> worker_of(j.segments);
+    for (int32_t s = 0; s < j.segments; ++s) worker_of[s] = s % workers;  // round-robin GOP_s_VEC per worker
+    st = fc_dispatch_segments(worker_of.data(), j.segments, workers, max_in_flight, mjpeg_segment, &j, trace);
+    if (st != FC_OK && j.first != FC_OK) st = fail(j.first, j.first_msg);
+  }
+  for (cudaStream_t s : j.streams) cudaStreamDestroy(s);
+  for (fc_jpeg_decoder_t* d : j.dec) fc_jpeg_decoder_destroy(d);
+  return st;
 }
 
 }  // extern "C"

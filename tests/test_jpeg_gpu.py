@@ -85,3 +85,31 @@ def test_jpeg_unsupported_inputs(fc, cuda, decoder):
     with pytest.raises(fc.FcError):
         decoder.decode(b"\xff\xd8not a jpeg at all" * 4)
     assert decoder.info(_jpeg(rgb, subsampling=0))[2] is False
+
+
+def test_mjpeg_stall_free_decode_matches_single_decodes(fc, oracle, cuda, decoder):
+    """NEXT-3 (partial): a Motion-JPEG request (every frame an independent
+    JPEG, a one-frame GOP) decoded over GOP_s segments by 3 workers with at
+    most 2 in flight (Alg. 2): each target's planes equal a single decode, and
+    the request's tokens equal the oracle on those planes."""
+    import torch
+    W, H = 640, 360
+    frames = [_jpeg(_image(W, H, 40 + i)) for i in range(10)]
+    planes, trace = fc.decode_mjpeg(frames, segments=5, workers=3, max_in_flight=2)
+    assert sorted(s for s, _, _ in trace) == list(range(5)) and all(st == 0 for _, _, st in trace)
+    for i, f in enumerate(frames):
+        ref = decoder.decode(f)
+        torch.cuda.synchronize()
+        for a, b, wv in zip(planes[i], ref, (W, W // 2, W // 2)):  # visible bytes (pitch padding is unset)
+            assert torch.equal(a[:, :wv], b[:, :wv])
+    plan = fc.Plan(fc.VideoMeta(W, H, len(frames), (30, 1), [0]),
+                   fc.image_cfg(sampling="fps_stride", explicit_indices=None, sample_fps=30.0, min_frames=2))
+    surf = fc.SurfaceTable(len(frames))
+    for i in plan.sampled_indices:
+        surf.set(i, *planes[i])
+    tokens = fc.preprocess(plan, 0, surf)
+    torch.cuda.synchronize()
+    h2, w2 = plan.resized
+    host = [tuple(p.cpu().numpy() for p in planes[i]) for i in plan.sampled_indices]
+    ref = oracle.preprocess_i420(host, W, H, w2, h2, matrix="bt601_full")
+    np.testing.assert_array_equal(tokens.cpu().numpy().view(np.uint32), ref.view(np.uint32))
