@@ -36,6 +36,9 @@ namespace fc {
 #ifndef FC_LB_WIDE
 #define FC_LB_WIDE 3  // min CTAs/SM the wide-window instances are compiled for (register cap; A/B knob)
 #endif
+#ifndef FC_PREF_VB
+#define FC_PREF_VB 0  // L1 prefetch of the band's V fragments at the band start (A/B knob)
+#endif
 #ifndef FC_PREF
 #define FC_PREF 1  // per-band table reads issued a band ahead (A/B knob)
 #endif
@@ -338,6 +341,12 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : FC_LB_W
       const int kneed = min(p.nchunks, (vend_nx + CH - 1) / CH);
       if (hb_ + 1 < r.hb1) vend_nx = __ldg(p.vx + yo0 + 55) + __ldg(p.vcnt + yo0 + 55);
       const int ys_pf = __ldg(p.vys + hb_ * 4 + vjg);  // consumed by this band's V pass, after the chunks
+#if FC_PREF_VB
+      // the warp's V weight fragments of this band (KSV*3 blocks of 256 B): one
+      // L1 prefetch per 128-B line, so the V pass's fragment loads hit L1
+      if (lane < KSV * 6)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p.vfr + static_cast<size_t>(hb_ * 4 + vjg) * KSV * 3 * 64 + lane * 32));
+#endif
 #else
       const int kneed = min(p.nchunks, (__ldg(p.vx + yo0 + 27) + __ldg(p.vcnt + yo0 + 27) + CH - 1) / CH);
 #endif
