@@ -33,6 +33,9 @@ namespace fc {
 #ifndef FC_HG2
 #define FC_HG2 2  // the same for wide windows (KSH > 1)
 #endif
+#ifndef FC_LB_NARROW
+#define FC_LB_NARROW 4  // min CTAs/SM of the narrow-window instances (64 registers; A/B knob)
+#endif
 #ifndef FC_LB_WIDE
 #define FC_LB_WIDE 3  // min CTAs/SM the wide-window instances are compiled for (register cap; A/B knob)
 #endif
@@ -192,7 +195,7 @@ __device__ __forceinline__ void issue_chunk(const Params& p, int pair, int SX0, 
 template <int KSH, int KSV, bool DBG, int TOK, bool PAGED = false, bool I420 = false, bool COLS = false>
 // Narrow-window instances (KSH = KSV = 1: c2, c3, c5) fit 64 registers without
 // spills and run 4 CTAs/SM (with 2 TMA stages); wider windows keep 80 / 3.
-__global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? 4 : FC_LB_WIDE)
+__global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? FC_LB_NARROW : FC_LB_WIDE)
     fc_fused_kernel(const __grid_constant__ Params p) {
   constexpr int SW = kStrip;
   constexpr int CH = kChunkRows;
