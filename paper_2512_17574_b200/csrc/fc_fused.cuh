@@ -39,6 +39,26 @@ namespace fc {
 #ifndef FC_LB_WIDE
 #define FC_LB_WIDE 3  // min CTAs/SM the wide-window instances are compiled for (register cap; A/B knob)
 #endif
+// FC_CHECKED=1 builds (tools/checked_build.sh): every shared-memory and token
+// address the kernel forms is range-checked and a violation traps -- the
+// bounds evidence compute-sanitizer no longer provides on the GPU pool.
+#ifndef FC_CHECKED
+#define FC_CHECKED 0
+#endif
+#if FC_CHECKED
+#include <cstdio>
+#define FC_CHK(c, what)                                                                          \
+  do {                                                                                           \
+    if (!(c)) {                                                                                  \
+      printf("fc check failed: %s (block %d thread %d)\n", what, blockIdx.x, threadIdx.x);      \
+      __trap();                                                                                  \
+    }                                                                                            \
+  } while (0)
+#else
+#define FC_CHK(c, what) \
+  do {                  \
+  } while (0)
+#endif
 #ifndef FC_PREF_VB
 #define FC_PREF_VB 0  // L1 prefetch of the band's V fragments at the band start (A/B knob)
 #endif
@@ -360,6 +380,9 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? FC_LB_NARRO
         mbar_wait(&full[buf], (seq >> p.stage_shift) & 1);
         // ---- a5: NV12 -> RGB planes, 8 pixels x 2 rows per item
         auto convert = [&](int oy, int ouv, int orgb, int e) {
+            FC_CHK(oy >= 0 && oy + p.BW + 8 <= 2 * RAWF && ouv >= 0 && ouv + (I420 ? 4 * p.BW + 4 : 8) <= 2 * RAWF,
+                   "colour raw read outside its stage");
+            FC_CHK(orgb >= 0 && orgb + 2 * CH * SWP + 16 <= 6 * CH * SWP, "colour store outside the RGB planes");
             const uint2 Ye = *reinterpret_cast<const uint2*>(rawb + oy);          // even row, 8 pixels
             const uint2 Yo = *reinterpret_cast<const uint2*>(rawb + oy + p.BW);   // odd row
             uint2 UVv;
@@ -427,6 +450,9 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? FC_LB_NARRO
             for (int e = 0; e < HG; ++e)
 #pragma unroll
               for (int kk = 0; kk < KSH; ++kk) {
+                FC_CHK(hA + (fg + e) * CH * SWP + 64 * kk >= rgb_s &&
+                           hA + (fg + e) * CH * SWP + 64 * kk + 16 <= rgb_s + 6 * CH * SWP,
+                       "H A fragment outside the RGB planes");
                 lds128(a[e][kk], hA + (fg + e) * CH * SWP + 64 * kk);  // k-step kk: 32 columns x 2 rows
               }
             int d2[HG][4], d1[HG][4], d0[HG][4];
@@ -440,6 +466,8 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? FC_LB_NARRO
               int v[4];
 #pragma unroll
               for (int i = 0; i < 4; ++i) v[i] = combine_planes(d2[e][i], d1[e][i], d0[e][i]) >> 22;
+              FC_CHK(!hst0 || (dA + off >= ring_s && dA + off + 2 <= ring_s + p.TRW * RS * 4), "H ring store outside the ring");
+              FC_CHK(!hst1 || (dA + off + 4 >= ring_s && dA + off + 6 <= ring_s + p.TRW * RS * 4), "H ring store outside the ring");
               if (hst0) sts16(dA + off, pack_sat_u8(v[2], v[0], 0u));      // column ho: rows 2hp, 2hp+1
               if (hst1) sts16(dA + off + 4, pack_sat_u8(v[3], v[1], 0u));  // column ho + 1
             }
@@ -532,6 +560,9 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? FC_LB_NARRO
 #pragma unroll
               for (int kk = 0; kk < KSV; ++kk) {
                 const uint32_t co = (e * SW + 14 * (q0 + e2)) * 4;
+                FC_CHK(rb[kk][0] + co >= ring_s && rb[kk][0] + co + 8 <= ring_s + p.TRW * RS * 4 &&
+                           rb[kk][1] + co >= ring_s && rb[kk][1] + co + 8 <= ring_s + p.TRW * RS * 4,
+                       "V ring read outside the ring");
                 const uint2 lo = lds64(rb[kk][0] + co);  // columns 2g, 2g+1; rows k 4t..4t+3
                 const uint2 hi = lds64(rb[kk][1] + co);  // k + 16
                 a[e2][kk][0] = lo.x;
@@ -552,10 +583,13 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? FC_LB_NARRO
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
                 sv[i] = combine_planes(d2[e2][i], d1[e2][i], d0[e2][i]);  // S = 2^21 + sum T*iv (exact)
-                if constexpr (TOK == FC_TOKENS_U8)
+                if constexpr (TOK == FC_TOKENS_U8) {
                   o[i] = static_cast<uint32_t>(add_min_relu(sv[i], 0, (1 << 30) - 1)) >> 22;  // the u8 code (NEXT-1)
-                else  // LUT[clip8(S)] = extended table at floor(S / 2^22) (arithmetic shift)
+                } else {  // LUT[clip8(S)] = extended table at floor(S / 2^22) (arithmetic shift)
+                  FC_CHK((sv[i] >> 22) >= -kLutLo && (sv[i] >> 22) < 256 + kLutLo,  // every lane: any u8 input stays inside
+                         "V value outside the extended normalisation table");
                   o[i] = lds32(lutc + (static_cast<uint32_t>(sv[i] >> 20) & ~3u));
+                }
               }
               if constexpr (COLS) {  // NEXT-1: column blocks [W][rows][C] (the paper's last-dimension split)
                 const long long rq = static_cast<long long>(r.pair) * static_cast<long long>(pair_rows) +
@@ -576,6 +610,12 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? FC_LB_NARRO
                 st_cs_pred2(pb + static_cast<size_t>(prow[1][q]) * kCols + (j1 % 14) * 14, o[1], o[3], jok1 && xok);
               } else {
                 TokT* op = tp + (q >> 1) * 4 * kCols + (q & 1) * kCols;  // wb += q/2, wm = q&1
+                FC_CHK(p.tokj != nullptr ||
+                           ((!(jok0 && xok) || (op >= static_cast<TokT*>(p.tokens) &&
+                                                op + 2 <= static_cast<TokT*>(p.tokens) + static_cast<size_t>(p.npairs) * pair_rows * kCols)) &&
+                            (!(jok1 && xok) || (op + djo >= static_cast<TokT*>(p.tokens) &&
+                                                op + djo + 2 <= static_cast<TokT*>(p.tokens) + static_cast<size_t>(p.npairs) * pair_rows * kCols))),
+                       "token store outside the launch's rows");
                 st_cs_pred2(op, o[0], o[2], jok0 && xok);        // row j0: columns 2g, 2g+1
                 st_cs_pred2(op + djo, o[1], o[3], jok1 && xok);  // row j1
               }
