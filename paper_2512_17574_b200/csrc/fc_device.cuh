@@ -149,6 +149,35 @@ __device__ __forceinline__ void yuv2rgb_4x2(uint32_t ye, uint32_t yo, uint32_t u
   row(yo, Ro, Go, Bo);
 }
 
+// The same two rows with the chroma terms formed once per chroma pair: c_ch =
+// cU*U + cV*V + bias (one dp2a each, shared by the 2x2 pixels of the pair),
+// then per pixel and channel one dp2a adding cY*Y -- the Y byte is selected by
+// the coefficient pair (cY in the low or the high half), so no byte shuffles.
+__device__ __forceinline__ void yuv2rgb_4x2c(uint32_t ye, uint32_t yo, uint32_t uvw, uint32_t& Re, uint32_t& Ge,
+                                             uint32_t& Be, uint32_t& Ro, uint32_t& Go, uint32_t& Bo, uint32_t kR,
+                                             uint32_t kG, uint32_t kGv, uint32_t kB, int bR, int bG, int bB) {
+  const uint32_t kY0 = kR & 0xFFFFu, kY1 = kY0 << 16;                // (cY, 0), (0, cY)
+  const uint32_t kRc = kR & 0xFFFF0000u;                              // (0, cRV)  on (U, V)
+  const uint32_t kGc = (kG >> 16) | (kGv & 0xFFFF0000u);              // (cGU, cGV)
+  const uint32_t kBc = kB >> 16;                                      // (cBU, 0)
+  const int r0 = dp2a_lo(kRc, uvw, bR), r1 = dp2a_hi(kRc, uvw, bR);  // chroma pair 0 (pixels 0,1), 1 (2,3)
+  const int g0 = dp2a_lo(kGc, uvw, bG), g1 = dp2a_hi(kGc, uvw, bG);
+  const int b0 = dp2a_lo(kBc, uvw, bB), b1 = dp2a_hi(kBc, uvw, bB);
+  auto row = [&](uint32_t yw, uint32_t& R, uint32_t& G, uint32_t& B) {
+    const uint32_t r01 = pack_sat_u16(dp2a_lo(kY1, yw, r0), dp2a_lo(kY0, yw, r0));
+    const uint32_t r23 = pack_sat_u16(dp2a_hi(kY1, yw, r1), dp2a_hi(kY0, yw, r1));
+    const uint32_t g01 = pack_sat_u16(dp2a_lo(kY1, yw, g0), dp2a_lo(kY0, yw, g0));
+    const uint32_t g23 = pack_sat_u16(dp2a_hi(kY1, yw, g1), dp2a_hi(kY0, yw, g1));
+    const uint32_t b01 = pack_sat_u16(dp2a_lo(kY1, yw, b0), dp2a_lo(kY0, yw, b0));
+    const uint32_t b23 = pack_sat_u16(dp2a_hi(kY1, yw, b1), dp2a_hi(kY0, yw, b1));
+    R = __byte_perm(r01, r23, 0x7531);
+    G = __byte_perm(g01, g23, 0x7531);
+    B = __byte_perm(b01, b23, 0x7531);
+  };
+  row(ye, Re, Ge, Be);
+  row(yo, Ro, Go, Bo);
+}
+
 // ---------------------------------------------------------------- int8 MMA
 // D = A(16x32 u8, row) * B(32x8, col) + C, s32.  Fragment layout (g = lane/4,
 // t = lane%4; verified on B200 by tools/ubench/mma_layout.cu):

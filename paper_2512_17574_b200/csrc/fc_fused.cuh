@@ -59,6 +59,9 @@ namespace fc {
   do {                  \
   } while (0)
 #endif
+#ifndef FC_COLOR_C
+#define FC_COLOR_C 1  // narrow windows: colour with chroma terms per chroma pair (yuv2rgb_4x2c; A/B knob)
+#endif
 #ifndef FC_PREF_VB
 #define FC_PREF_VB 0  // L1 prefetch of the band's V fragments at the band start (A/B knob)
 #endif
@@ -395,10 +398,17 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? FC_LB_NARRO
             }
             // per channel: even row px 0-3, odd row px 0-3, even px 4-7, odd px 4-7
             uint4 Rv, Gv, Bv;
+            if constexpr (FC_COLOR_C && KSH == 1) {  // c2 -0.5%; c4 (KSH = 2) +1.2%, so wide windows keep 4x2
+            yuv2rgb_4x2c(Ye.x, Yo.x, UVv.x, Rv.x, Gv.x, Bv.x, Rv.y, Gv.y, Bv.y, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR,
+                         p.cbG, p.cbB);
+            yuv2rgb_4x2c(Ye.y, Yo.y, UVv.y, Rv.z, Gv.z, Bv.z, Rv.w, Gv.w, Bv.w, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR,
+                         p.cbG, p.cbB);
+            } else {
             yuv2rgb_4x2(Ye.x, Yo.x, UVv.x, Rv.x, Gv.x, Bv.x, Rv.y, Gv.y, Bv.y, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR,
                         p.cbG, p.cbB);
             yuv2rgb_4x2(Ye.y, Yo.y, UVv.y, Rv.z, Gv.z, Bv.z, Rv.w, Gv.w, Bv.w, p.ckR, p.ckG, p.ckGv, p.ckB, p.cbR,
                         p.cbG, p.cbB);
+            }
             uint8_t* dst = rgb + orgb;  // 16-byte aligned (row-pair stride 2SWP = 0 mod 16)
             *reinterpret_cast<uint4*>(dst) = Rv;
             *reinterpret_cast<uint4*>(dst + CH * SWP) = Gv;
