@@ -134,7 +134,7 @@ def algorithmic_bytes(plan, wl, rank_plan=None, tok_bytes=4):
 
 
 # ------------------------------------------------------------ CPU oracle arm
-def oracle_sample(wl, pairs, nthreads, matrix="bt601"):
+def oracle_sample(wl, pairs, nthreads, matrix="bt601", backend="pil"):
     """Run the oracle (as it stands) on `pairs` temporal pairs of workload wl.
     Returns (seconds, frames)."""
     from oracle import oracle
@@ -143,7 +143,8 @@ def oracle_sample(wl, pairs, nthreads, matrix="bt601"):
     host = synth.frames_nv12(wl, take, "natural")
     h2, w2 = oracle.smart_resize(wl.height, wl.width)
     t0 = time.perf_counter()
-    oracle.preprocess([host[i] for i in take], wl.width, wl.height, w2, h2, nthreads=nthreads, matrix=matrix)
+    oracle.preprocess([host[i] for i in take], wl.width, wl.height, w2, h2, nthreads=nthreads, matrix=matrix,
+                      backend=backend)
     return time.perf_counter() - t0, len(take)
 
 
@@ -228,7 +229,8 @@ def run_ours(args):
     if replicas:
         u8x = colx = p2px = False
     cfg = fc.ModelCfg(world_size=1 if replicas else world, sample_fps=wl.sample_fps,
-                      token_dtype="u8" if u8x else args.tokens, color=args.color, surface_format=args.surface)
+                      token_dtype="u8" if u8x else args.tokens, color=args.color, surface_format=args.surface,
+                      backend=args.backend)
     tok_bytes = 2 if args.tokens == "bf16" else 4
     plan0 = fc.Plan(meta, cfg)
     rp = plan0.rank(0 if replicas else rank)
@@ -535,7 +537,8 @@ def run_ours(args):
             abytes = clips * max(algorithmic_bytes(plan0, wl, r, 1 if u8x else tok_bytes) for r in plan0.ranks())
             kern_for_roof = kern_max
         achieved = abytes / (kern_for_roof * 1e-3) / 1e9
-        same_kernel = world == 1 and args.tokens == "f32" and args.color == "bt601" and args.surface == "nv12"
+        same_kernel = (world == 1 and args.tokens == "f32" and args.color == "bt601" and args.surface == "nv12"
+                       and args.backend == "pil")
         traffic = load_traffic(args.config) if same_kernel else None
         # second roofline: the kernel is bound by instruction issue;
         # warp instructions per launch from the committed ncu capture of this config
@@ -557,7 +560,7 @@ def run_ours(args):
                        "resized_hw": list(plan0.resized), "grid_thw": list(plan0.grid_thw),
                        "token_bytes": clips_all * plan0.token_rows * 1176 * tok_bytes,
                        "parallelism": (f"replicas{world} (whole clips, LPT)" if replicas else f"gop-dp{world}"),
-                       "color": args.color, "surface": args.surface,
+                       "color": args.color, "surface": args.surface, "backend": args.backend,
                        "l2": "per-step inputs+outputs (1.19 GB for c2) exceed the 126 MB L2; no flush",
                        "kernel_ms_avg": round(kern_max if world > 1 else kern_avg, 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -582,8 +585,8 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             cores = len(os.sched_getaffinity(0))
             pairs = min(plan0.grid_thw[0], 60)
-            dt, f = oracle_sample(wl, pairs, cores, args.color)
-            dt1, f1 = oracle_sample(wl, 1, 1, args.color)  # one temporal pair on one core
+            dt, f = oracle_sample(wl, pairs, cores, args.color, args.backend)
+            dt1, f1 = oracle_sample(wl, 1, 1, args.color, args.backend)  # one temporal pair on one core
             line["cpu_baseline"] = {"value": round(f / dt, 3), "unit": "frames/s", "cores": cores,
                                     "kind": "oracle",
                                     "sample": f"{f} sampled frames ({pairs} temporal pairs) of {args.config}, "
@@ -616,6 +619,9 @@ def main():
                          "(each rank's kernel writes its codes into the encoder's buffer over NVLink)")
     ap.add_argument("--color", default="bt601", choices=["bt601", "bt709", "bt601_full", "bt709_full"],
                     help="YUV->RGB matrix (NEXT-4 variant; the BASELINE metric is bt601)")
+    ap.add_argument("--backend", default="pil", choices=["pil", "torchvision"],
+                    help="HF processor arithmetic (DESIGN.md R21): Pillow bicubic + HF normalise, or torch's "
+                         "uint8 antialiased bicubic + the fused normalisation (same kernel, other tables)")
     ap.add_argument("--surface", default="nv12", choices=["nv12", "i420"],
                     help="decoded surface layout: NV12 (interleaved chroma) or I420 (planar U, V)")
     args = ap.parse_args()
