@@ -339,6 +339,18 @@ def run_ours(args):
         fc.Plan(meta, cfg)
     plan_us = (time.perf_counter() - tp0) / 20 * 1e6
 
+    # L2 (126 MB on B200): a step whose own bytes (this rank's NV12 read + token
+    # write) stay under 2x L2 could reuse cached inputs/outputs across steps, so
+    # such steps are timed one by one with a 256 MB scratch write in between
+    # (outside the events); larger steps stream through L2 on their own
+    L2_BYTES = 126 * 2 ** 20
+    my_step_bytes = clips * max(algorithmic_bytes(plan0, wl, plan0.rank(r), 1 if u8x else tok_bytes)
+                                for r in ([xrank] if world > 1 and not replicas else [0]))
+    if world == 1 or replicas:
+        my_step_bytes = clips * algorithmic_bytes(plan0, wl, tok_bytes=tok_bytes)
+    flush = my_step_bytes < 2 * L2_BYTES
+    scratch = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device="cuda") if flush else None
+
     keep = []
     for _ in range(args.warmup):
         step(keep)
@@ -349,17 +361,26 @@ def run_ours(args):
     sevs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]  # step boundaries
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = fc.lib().fc_kernel_launches()
+    fevs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in range(args.steps)] if flush else None
     with ClockSampler(local) as clk:  # the headline pass: no per-step instrumentation
         torch.cuda.synchronize()
-        t0.record(stream)
-        for k in range(args.steps):
-            step(keep)
-        t1.record(stream)
+        if flush:  # cold L2 at every step: scratch write, then the step between its own events
+            for k in range(args.steps):
+                scratch.zero_()
+                fevs[k][0].record(stream)
+                step(keep)
+                fevs[k][1].record(stream)
+        else:
+            t0.record(stream)
+            for k in range(args.steps):
+                step(keep)
+            t1.record(stream)
         torch.cuda.synchronize()
     launches = fc.lib().fc_kernel_launches() - launches0
     if world > 1:
         dist.barrier()
-    total_ms = t0.elapsed_time(t1)
+    total_ms = sum(a.elapsed_time(b) for a, b in fevs) if flush else t0.elapsed_time(t1)
     # a second pass with per-step events (step boundaries, kernel launch) for
     # the median / min / kernel-time statistics
     torch.cuda.synchronize()
@@ -561,7 +582,9 @@ def run_ours(args):
                        "token_bytes": clips_all * plan0.token_rows * 1176 * tok_bytes,
                        "parallelism": (f"replicas{world} (whole clips, LPT)" if replicas else f"gop-dp{world}"),
                        "color": args.color, "surface": args.surface, "backend": args.backend,
-                       "l2": "per-step inputs+outputs (1.19 GB for c2) exceed the 126 MB L2; no flush",
+                       "l2": (f"L2 flushed between timed steps (256 MB scratch write outside the step events): "
+                              f"{my_step_bytes / 1e6:.0f} MB per step < 2x the 126 MB L2" if flush else
+                              f"per-step inputs+outputs ({my_step_bytes / 1e9:.2f} GB) exceed the 126 MB L2; no flush"),
                        "kernel_ms_avg": round(kern_max if world > 1 else kern_avg, 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,

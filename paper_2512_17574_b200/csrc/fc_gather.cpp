@@ -187,6 +187,7 @@ fc_status fc_exchange_schedule(const fc_plan_t* P, int32_t rank, fc_exchange_kin
 }
 
 fc_status fc_gather(const fc_plan_t* P, int32_t rank, void* comm, const void* shard, void* full, void* stream) {
+  NvtxRange nvtx("fc_gather");
   std::vector<fc_transfer> xs;
   fc_status st = schedule(P, rank, FC_XCHG_GATHER, &xs);
   if (st != FC_OK) return st;

@@ -1,6 +1,7 @@
 // fc_internal.h -- private types shared by the host planner, the runtime and
 // the CUDA launcher of libfc.so.  Not part of the ABI (include/fc.h is).
 #pragma once
+#include <nvtx3/nvToolsExt.h>
 #include <cstdint>
 #include <memory>
 #include <mutex>
@@ -83,4 +84,13 @@ void set_error(const std::string& msg);
 fc_status fail(fc_status s, const std::string& msg);
 fc_status build_axis(int in, int out, int backend, AxisTable* t);
 fc_status axis_cached(int in, int out, int backend, std::shared_ptr<const AxisTable>* t);
+
+// NVTX range around a C-ABI entry point (nvtx3, header-only: a no-op unless a
+// profiler injects itself), so nsys / ncu timelines show the library's calls.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 }  // namespace fc

@@ -120,6 +120,7 @@ fc_status fc_jpeg_info(fc_jpeg_decoder_t* d, const uint8_t* data, size_t len, in
 
 fc_status fc_jpeg_decode_i420(fc_jpeg_decoder_t* d, const uint8_t* data, size_t len, const fc_nv12_surface* surf,
                               void* stream) {
+  NvtxRange nvtx("fc_jpeg_decode_i420");
   if (!d || !data || !len || !surf || !surf->y || !surf->uv || !surf->v)
     return fail(FC_ERR_INVALID_ARG, "NULL argument");
   int32_t w = 0, h = 0, css = 0;

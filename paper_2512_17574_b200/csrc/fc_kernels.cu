@@ -881,11 +881,13 @@ extern "C" {
 
 fc_status fc_preprocess(const fc_plan_t* plan, int32_t rank, const fc_nv12_surface* surfaces,
                         int64_t num_surfaces, void* tokens, int64_t grid_thw[3], void* stream) {
+  NvtxRange nvtx("fc_preprocess");
   return preprocess_impl(plan, rank, surfaces, num_surfaces, tokens, grid_thw, stream, nullptr, nullptr);
 }
 
 fc_status fc_submit(const fc_video_meta* meta, const fc_model_cfg* cfg, int32_t rank, const fc_nv12_surface* surfaces,
                     int64_t num_surfaces, void* tokens, void* stream, fc_plan_t** plan_out) {
+  NvtxRange nvtx("fc_submit");
   if (!plan_out) return fail(FC_ERR_INVALID_ARG, "plan_out is NULL");
   *plan_out = nullptr;
   fc_plan_t* P = nullptr;
@@ -920,6 +922,7 @@ fc_status fc_preprocess_debug(const fc_plan_t* plan, int32_t rank, const fc_nv12
 fc_status fc_preprocess_batch(const fc_plan_t* const* plans, const int32_t* ranks, int32_t count,
                               const fc_nv12_surface* const* surfaces, const int64_t* num_surfaces,
                               void* const* tokens, void* stream) {
+  NvtxRange nvtx("fc_preprocess_batch");
   if (count < 0 || (count > 0 && (!plans || !ranks || !surfaces || !num_surfaces || !tokens)))
     return fail(FC_ERR_INVALID_ARG, "batch arguments");
   // validate every job before any launch; then one launch per maximal run of

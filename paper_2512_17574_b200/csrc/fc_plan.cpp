@@ -434,6 +434,7 @@ void fc_model_cfg_default(fc_model_cfg* c) {
 }
 
 fc_status fc_plan(const fc_video_meta* meta, const fc_model_cfg* cfg, fc_plan_t** out) {
+  NvtxRange nvtx("fc_plan");
   if (!out) return fail(FC_ERR_INVALID_ARG, "out is NULL");
   *out = nullptr;
   if (!meta || !cfg) return fail(FC_ERR_INVALID_ARG, "meta/cfg is NULL");

@@ -39,6 +39,7 @@ using namespace fc;
 
 extern "C" fc_status fc_dispatch_segments(const int32_t* worker_of, int64_t num_segments, int32_t num_workers,
                                           int32_t max_in_flight, fc_segment_fn fn, void* ctx, int64_t* trace) {
+  NvtxRange nvtx("fc_dispatch_segments");
   if (num_segments < 0 || num_workers < 1 || num_workers > 1024 || max_in_flight < 1 || !fn ||
       (num_segments > 0 && !worker_of))
     return fail(FC_ERR_INVALID_ARG, "bad segment dispatch arguments");
