@@ -59,6 +59,9 @@ namespace fc {
   do {                  \
   } while (0)
 #endif
+#ifndef FC_BAND_BAR
+#define FC_BAND_BAR 0  // CTA barrier after every band's V pass (redundant; A/B knob)
+#endif
 #ifndef FC_COLOR_C
 #define FC_COLOR_C 1  // narrow windows: colour with chroma terms per chroma pair (yuv2rgb_4x2c; A/B knob)
 #endif
@@ -643,7 +646,13 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? FC_LB_NARRO
           }
         }
       }
+#if FC_BAND_BAR
       bar_sync(1, kComputeThreads);  // ring may be overwritten by the next chunks
+#endif
+      // (no barrier here: the V pass only reads shared memory, and the next
+      // ring writes -- the H pass of the next chunk -- come after that chunk's
+      // colour->H barrier, which every warp reaches only after its V pass; a
+      // warp done early starts converting the next chunk meanwhile)
     }
   }
   if (p.cta_t != nullptr && tid == 0) {
