@@ -59,6 +59,9 @@ namespace fc {
   do {                  \
   } while (0)
 #endif
+#ifndef FC_VG1
+#define FC_VG1 1  // V pass: patches per MMA group for KSV = 1 (A/B knob)
+#endif
 #ifndef FC_BAND_BAR
 #define FC_BAND_BAR 0  // CTA barrier after every band's V pass (redundant; A/B knob)
 #endif
@@ -563,7 +566,7 @@ __global__ void __launch_bounds__(kThreads, (KSH == 1 && KSV == 1) ? FC_LB_NARRO
           const uint32_t lutc = lut_s + (c * kLutN + kLutLo) * 4;  // entry of v = 0
           TokT* tp = tb + (c * 2 + f) * 196;
           // patches per MMA group: 2 for KSV = 2 (c4 -2.9%), 1 for narrow windows (2: c2 +0.4%; 4 spills)
-          constexpr int VG = KSV == 2 ? 2 : 1;
+          constexpr int VG = KSV == 2 ? 2 : FC_VG1;
 #pragma unroll
           for (int q0 = 0; q0 < kStrip / 14; q0 += VG) {
             if (q0 >= npatch) break;
